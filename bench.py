@@ -1,0 +1,330 @@
+"""Benchmark of the Q(f,f) hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config hs12|hs8|mm10|hs4]
+
+One step = one Q(f,f) evaluation of every cell of the rank's batch (one
+``bfq_eval`` launch).  Default workload = BASELINE config 3 (hard spheres,
+N=L=12, 65,536 cells per GPU; weak scaling: each rank evaluates its own
+65,536-cell shard of a 65,536*N-cell global batch, no data-path collective).
+Rank 0 prints one JSON line.  See DESIGN.md §Measurement.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (operator file, cells per GPU, generator, description)
+    "hs12": ("hs_n12", 65536, "pm", "config3: hard spheres N=L=12, perturbed Maxwellians"),
+    "hs8": ("hs_n8", 4096, "pm", "config2: hard spheres N=L=8, perturbed Maxwellians"),
+    "mm10": ("mm_n10", 32768, "bimodal", "config5 operator: Maxwell N=L=10, bimodal cells (single Q eval)"),
+    "hs4": ("hs_n4", 65536, "pm", "hard spheres N=L=4 (small)"),
+}
+METRIC = "Q(f,f) cell-evals/s (fp64, hard spheres L=N=12) and FP64/HBM roofline frac"
+FP64_PEAK_TFLOPS = 37.1  # DMMA.8x8x4 sustained, measured on this pool (profiles/fp64_peak.txt)
+
+
+def env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh)
+    except OSError:
+        return {}
+
+
+def make_cells(cfg_name, n_k, l_max, n, seed, start):
+    from paper_2605_28475_b200 import inputs
+
+    gen = CONFIGS[cfg_name][2]
+    if gen == "pm":
+        return inputs.perturbed_maxwellians(n_k, l_max, n, seed=seed, start=start)
+    return inputs.bimodal(n_k, l_max, n, seed=seed, start=start)
+
+
+# ------------------------------------------------------------------ CPU legs
+def _cpu_worker(args):
+    path, cells = args
+    from oracle import q_oracle
+    from paper_2605_28475_b200.operator import load_cache
+
+    try:
+        from threadpoolctl import threadpool_limits
+    except ImportError:  # pragma: no cover
+        threadpool_limits = None
+    op = q_oracle.OracleOperator.from_operator(load_cache(path))
+    rs = op.r[:, :, :, op.slice_tau]
+    ctx = threadpool_limits(limits=1) if threadpool_limits else None
+    if ctx:
+        ctx.__enter__()
+    t0 = time.perf_counter()
+    for c in cells:
+        q_oracle.q_angular_first(op, c, r_slices=rs)
+    dt = time.perf_counter() - t0
+    if ctx:
+        ctx.__exit__(None, None, None)
+    return len(cells), dt
+
+
+def cpu_port_rate(cfg_name, cells, budget_s=15.0, cores=None):
+    """Oracle port (numpy restatement of q_angular_first) on host cores: cells/s."""
+    import multiprocessing as mp
+
+    path = os.path.join(ROOT, "operators", CONFIGS[cfg_name][0] + ".bfct")
+    cores = cores or os.cpu_count() or 1
+    # calibrate on one cell, then give every worker ~budget_s of work
+    n1, dt1 = _cpu_worker((path, cells[:1]))
+    per_worker = max(1, int(budget_s / max(dt1, 1e-6)))
+    n = min(cells.shape[0], per_worker * cores)
+    chunks = [(path, cells[i::cores][: per_worker]) for i in range(cores)]
+    chunks = [c for c in chunks if len(c[1])]
+    t0 = time.perf_counter()
+    with mp.get_context("spawn").Pool(len(chunks)) as pool:
+        res = pool.map(_cpu_worker, chunks)
+    wall = time.perf_counter() - t0
+    done = sum(r[0] for r in res)
+    busy = max(r[1] for r in res)
+    return {"value": done / busy, "cells": done, "cores": len(chunks), "wall_s": wall, "busy_s": busy,
+            "single_cell_s": dt1}
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            out, _ = self.proc.communicate(timeout=10)
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in getattr(self, "lines", []):
+            parts = [p.strip() for p in line.split(",")]
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except (ValueError, IndexError):
+                continue
+            for name, val in zip(names, parts[4:8]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ arms
+def run_reference(args, rank, world):
+    """--impl reference: the reference's CPU path (oracle port of
+    contraction.q_angular_first) on all host cores, rank 0 only."""
+    if rank != 0:
+        return
+    opfile, n_cells, _, desc = CONFIGS[args.config]
+    from paper_2605_28475_b200.operator import load_cache
+
+    op = load_cache(os.path.join(ROOT, "operators", opfile + ".bfct"))
+    cells = make_cells(args.config, op.cfg.n_k, op.cfg.l_max, 256, seed=args.seed, start=0)
+    rates = []
+    for _ in range(args.warmup):
+        cpu_port_rate(args.config, cells, budget_s=2.0)
+    for _ in range(args.steps):
+        rates.append(cpu_port_rate(args.config, cells, budget_s=args.cpu_budget)["value"])
+    last = cpu_port_rate(args.config, cells[:64], budget_s=1.0)
+    v = statistics.median(rates)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "cells/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.json distributions)",
+        "config": {"workload": desc, "cells_per_gpu": n_cells, "operator": opfile},
+        "cpu_baseline": {"value": v, "unit": "cells/s", "cores": last["cores"], "kind": "port",
+                         "sample": f"~{args.cpu_budget:.0f} s of per-core work per step, cells of {desc}"},
+        "e2e": {"value": v, "unit": "cells/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+
+    from paper_2605_28475_b200 import engine
+    from paper_2605_28475_b200.operator import load_cache
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    opfile, n_cells, _, desc = CONFIGS[args.config]
+    if args.cells:
+        n_cells = args.cells
+    op = load_cache(os.path.join(ROOT, "operators", opfile + ".bfct"))
+    plan = engine.plan_for(op, local_rank)
+    cfg = op.cfg
+    host = make_cells(args.config, cfg.n_k, cfg.l_max, n_cells, seed=args.seed, start=rank * n_cells)
+    f = torch.from_numpy(host).to(dev)
+    q = torch.empty_like(f)
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(max(args.warmup, 0)):
+        engine.evaluate_batch(plan, f, out=q)
+    barrier()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        t0 = time.perf_counter()
+        for i in range(args.steps):
+            starts[i].record(stream)
+            engine.evaluate_batch(plan, f, out=q)
+            ends[i].record(stream)
+        barrier()
+        wall = time.perf_counter() - t0
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = starts[0].elapsed_time(ends[-1])
+    t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = n_cells * world * args.steps / (total_ms / 1e3)
+
+    # conservation diagnostics of the last step, all-reduced (max |production|)
+    mom = torch.empty((n_cells, 5), dtype=torch.float64, device=dev)
+    plan.moments_device(q.data_ptr(), mom.data_ptr(), n_cells, stream.cuda_stream)
+    diag = mom.abs().amax(dim=0)
+    if dist is not None:
+        dist.all_reduce(diag, op=dist.ReduceOp.MAX)
+    conservation_max = float(diag.max().item())
+
+    # end-to-end through the C ABI with host buffers (pinned), copies timed
+    e2e = None
+    if args.e2e_steps > 0:
+        hin = torch.from_numpy(host).pin_memory()
+        hout = torch.empty_like(hin).pin_memory()
+        from paper_2605_28475_b200 import _lib
+
+        lib = _lib.lib()
+        lib.bfq_eval_host(plan.handle, hin.data_ptr(), None, hout.data_ptr(), n_cells)  # warm
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            _lib.check(lib.bfq_eval_host(plan.handle, hin.data_ptr(), None, hout.data_ptr(), n_cells))
+        el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        if dist is not None:
+            dist.all_reduce(el, op=dist.ReduceOp.MAX)
+        bytes_ = n_cells * cfg.n_dof * 8
+        e2e = {"value": n_cells * world * args.e2e_steps / float(el.item()), "unit": "cells/s",
+               "h2d_bytes_per_step": bytes_, "d2h_bytes_per_step": bytes_, "steps": args.e2e_steps,
+               "path": "bfq_eval_host (C ABI, pinned host buffers, chunked H2D/Q/D2H pipeline)"}
+
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+    flops_cell, bytes_cell = plan.flops_per_cell, plan.bytes_per_cell
+    achieved = flops_cell * n_cells / (statistics.mean(step_ms) / 1e3) / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("bytes_per_launch")
+        except (OSError, ValueError):
+            traffic = None
+    line = {
+        "metric": METRIC, "value": value, "unit": "cells/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.json distributions)",
+        "config": {"workload": desc, "operator": opfile, "cells_per_gpu": n_cells, "global_cells": n_cells * world,
+                   "parallelism": f"cells sharded over {world} GPU(s), no data-path collective",
+                   "l2": "inputs larger than L2 (%.2f GB per GPU vs 126 MB)" % (host.nbytes / 1e9),
+                   "seed": args.seed},
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                     "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
+                     "peak_source": "measured FP64 DMMA.8x8x4 sustained (profiles/fp64_peak.txt); "
+                                    "MEASURED_PEAKS.json has no fp64 entry",
+                     "flops_per_cell": flops_cell, "exec_dmma_macs_per_cell": plan.info["exec_macs_per_cell"],
+                     "hbm_frac": bytes_cell * n_cells / (statistics.mean(step_ms) / 1e3) / 1e9
+                     / measured_peaks().get("hbm_gbs", 6456.5)},
+        "e2e": e2e,
+        "gpu_launches": args.steps,
+        "clocks": clk.summary(),
+        "conservation_max_abs": conservation_max,
+        "wall_s": wall,
+    }
+    if world == 1 and not args.no_cpu:
+        cpu = cpu_port_rate(args.config, host[:256], budget_s=args.cpu_budget)
+        line["cpu_baseline"] = {"value": cpu["value"], "unit": "cells/s", "cores": cpu["cores"], "kind": "port",
+                                "sample": f"{cpu['cells']} cells of the same batch, ~{args.cpu_budget:.0f} s per core "
+                                          "(numpy restatement of q_angular_first, 1 thread per process)"}
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="hs12", choices=sorted(CONFIGS))
+    ap.add_argument("--cells", type=int, default=0, help="override cells per GPU")
+    ap.add_argument("--seed", type=int, default=20260520)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local_rank = env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,157 @@
+"""ctypes binding of ``libbfq.so`` (the C ABI declared in ``include/bfq.h``).
+
+The shared library is built in-tree by ``__graft_entry__.build()``.  There is
+no fallback: if the library is missing every entry point raises, so a GPU
+code path can never silently degrade to a CPU implementation.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libbfq.so")
+
+BFQ_OK = 0
+BFQ_EINVAL = -1
+BFQ_EUNSORTED = -2
+BFQ_ECUDA = -3
+BFQ_ENOMEM = -4
+BFQ_ESMEM = -5
+BFQ_EIO = -6
+BFQ_EFORMAT = -7
+BFQ_EINTEGRITY = -8
+BFQ_EDIVERGED = -9
+
+# every symbol include/bfq.h declares (checked by tests/test_abi.py)
+EXPORTED_SYMBOLS = (
+    "bfq_plan_create",
+    "bfq_plan_create_bfct",
+    "bfq_plan_destroy",
+    "bfq_plan_get_info",
+    "bfq_plan_work",
+    "bfq_eval",
+    "bfq_eval_host",
+    "bfq_rk4_step",
+    "bfq_moments",
+    "bfq_host_plan_info",
+    "bfq_strerror",
+    "bfq_last_error",
+)
+
+_i32p = ctypes.POINTER(ctypes.c_int32)
+_i64p = ctypes.POINTER(ctypes.c_int64)
+_f64p = ctypes.POINTER(ctypes.c_double)
+
+
+class BfqDesc(ctypes.Structure):
+    _fields_ = [
+        ("k_max", ctypes.c_int32),
+        ("l_max", ctypes.c_int32),
+        ("gamma", ctypes.c_double),
+        ("n_t", ctypes.c_int32),
+        ("n_g", ctypes.c_int64),
+        ("n_s", ctypes.c_int64),
+        ("triplets", _i32p),
+        ("q1", _i32p),
+        ("q2", _i32p),
+        ("q3", _i32p),
+        ("tau", _i32p),
+        ("g", _f64p),
+        ("slice_starts", _i64p),
+        ("slice_tau", _i32p),
+        ("slice_q1", _i32p),
+        ("r", _f64p),
+        ("conservation", ctypes.c_int32),
+        ("detailed_balance", ctypes.c_int32),
+    ]
+
+
+class BfqPlanInfo(ctypes.Structure):
+    _fields_ = [
+        ("n_k", ctypes.c_int32),
+        ("n_q", ctypes.c_int32),
+        ("n_t", ctypes.c_int32),
+        ("n_g", ctypes.c_int64),
+        ("n_s", ctypes.c_int64),
+        ("folded", ctypes.c_int32),
+        ("cells_per_cta", ctypes.c_int32),
+        ("warps_per_cta", ctypes.c_int32),
+        ("stages", ctypes.c_int32),
+        ("smem_bytes", ctypes.c_int32),
+        ("items_per_tile", ctypes.c_int32),
+        ("exec_macs_per_cell", ctypes.c_double),
+        ("operator_bytes", ctypes.c_double),
+    ]
+
+
+class EngineUnavailable(RuntimeError):
+    """The CUDA engine library is not built or cannot be loaded."""
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def _declare(lib):
+    vp = ctypes.c_void_p
+    lib.bfq_plan_create.argtypes = [ctypes.POINTER(BfqDesc), ctypes.c_int, ctypes.POINTER(vp)]
+    lib.bfq_plan_create_bfct.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(vp)]
+    lib.bfq_plan_destroy.argtypes = [vp]
+    lib.bfq_plan_get_info.argtypes = [vp, ctypes.POINTER(BfqPlanInfo)]
+    lib.bfq_plan_work.argtypes = [vp, _f64p, _f64p]
+    lib.bfq_eval.argtypes = [vp, vp, vp, vp, ctypes.c_int64, vp]
+    lib.bfq_eval_host.argtypes = [vp, vp, vp, vp, ctypes.c_int64]
+    lib.bfq_rk4_step.argtypes = [vp, vp, vp, ctypes.c_int64, ctypes.c_double, vp, vp]
+    lib.bfq_moments.argtypes = [vp, vp, vp, ctypes.c_int64, vp]
+    lib.bfq_host_plan_info.argtypes = [ctypes.POINTER(BfqDesc), ctypes.c_int, ctypes.POINTER(BfqPlanInfo)]
+    lib.bfq_strerror.argtypes = [ctypes.c_int]
+    lib.bfq_strerror.restype = ctypes.c_char_p
+    lib.bfq_last_error.argtypes = []
+    lib.bfq_last_error.restype = ctypes.c_char_p
+    for name in EXPORTED_SYMBOLS:
+        if name not in ("bfq_strerror", "bfq_last_error"):
+            getattr(lib, name).restype = ctypes.c_int
+
+
+def lib():
+    """Load (once) and return the engine library; raise if it is absent."""
+    global _lib
+    if _lib is None:
+        with _lock:
+            if _lib is None:
+                if not os.path.exists(LIB_PATH):
+                    raise EngineUnavailable(
+                        f"{LIB_PATH} is missing: build the CUDA engine with "
+                        "`python -c 'import __graft_entry__ as g; g.build()'`"
+                    )
+                try:
+                    handle = ctypes.CDLL(LIB_PATH)
+                except OSError as exc:  # pragma: no cover - environment specific
+                    raise EngineUnavailable(f"cannot load {LIB_PATH}: {exc}") from exc
+                _declare(handle)
+                _lib = handle
+    return _lib
+
+
+def check(code: int) -> None:
+    """Map a BFQ_E* code to the reference's exception types."""
+    if code == BFQ_OK:
+        return
+    l = lib()
+    msg = f"{l.bfq_strerror(code).decode()}: {l.bfq_last_error().decode()}"
+    if code in (BFQ_EINVAL, BFQ_EUNSORTED, BFQ_ESMEM):
+        raise ValueError(msg)
+    if code == BFQ_EFORMAT:
+        from .operator import CacheFormatError
+
+        raise CacheFormatError(msg)
+    if code == BFQ_EINTEGRITY:
+        from .operator import CacheIntegrityError
+
+        raise CacheIntegrityError(msg)
+    if code == BFQ_EIO:
+        raise OSError(msg)
+    raise RuntimeError(msg)

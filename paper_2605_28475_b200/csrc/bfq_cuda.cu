@@ -1,0 +1,740 @@
+// B200 (sm_100a) kernels and C ABI of the Q(f,f) engine.
+//
+// Q[k1,q1] = sum_tau sum_{a,b} R[k1,a,b,tau] Phi_{tau,q1}[a,b]
+// Phi_{tau,q1}[a,b] = sum_{z in slice(tau,q1)} g_z f2[a,q2_z] f3[b,q3_z]
+// (the reference's angular-first order, contraction.py:293-317).
+//
+// One CTA = one cell tile (cells staged in shared memory) x one l1 group x a
+// run of m1-units.  Every compute warp owns 8 output rows "pairs" = (m1, cell)
+// and walks all channels tau of its l1 group:
+//   stage 1  Phi_pair = A B^T over the slice rows, DMMA.8x8x4 (M=a, N=b, K=rows),
+//            operands gathered from the staged f (the CG table read is
+//            broadcast across the warp's cells),                   contraction.py:306-308
+//   stage 2  out[pair,k1] += Phi[pair,(a,b)] R_tau[k1,(a,b)], DMMA.8x8x4
+//            (M=pairs, N=k1, K=n_k^2), R_tau streamed into a shared
+//            ring by cp.async.bulk + mbarrier from a producer warp,   contraction.py:309
+//   scatter  the accumulator of the pair IS Q[cell][k1][q1]: written once at
+//            the end, no atomics, deterministic;                    contraction.py:310-312
+//   epilogue exact 0.0 on the five invariant slots                  kinematic.py:594-610
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "bfq_internal.h"
+
+using namespace bfq;
+
+#define BFQ_CUDA_TRY(expr)                                                          \
+  do {                                                                              \
+    cudaError_t e_ = (expr);                                                        \
+    if (e_ != cudaSuccess) {                                                        \
+      set_error(std::string(#expr) + ": " + cudaGetErrorString(e_));               \
+      return BFQ_ECUDA;                                                             \
+    }                                                                               \
+  } while (0)
+
+namespace {
+
+struct DevProgram {
+  KernelConfig cfg;
+  bool bilinear = false;
+  ChanEntry* chans = nullptr;
+  Group* groups = nullptr;
+  Item* items = nullptr;
+  int n_items = 0;
+  double exec_macs_per_cell = 0.0;
+};
+
+struct KParams {
+  const double* f2;
+  const double* f3;
+  double* q;
+  long long n_cells;
+  long long n_tiles;
+  const double* R;
+  const Row* rows;
+  const int* sstart;
+  const ChanEntry* chans;
+  const Group* groups;
+  const Item* items;
+  int nk, nq, qs, k2s, k2p;
+  int cells, m1t, nw, nstage;
+  int conservation;
+};
+
+// ------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n" ::"r"(
+                   smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ Row load_row(const Row* rows, int z) {
+  const int4 v = __ldg(reinterpret_cast<const int4*>(rows) + z);
+  Row r;
+  r.q2 = v.x;
+  r.q3 = v.y;
+  r.g = __hiloint2double(v.w, v.z);
+  return r;
+}
+
+// ------------------------------------------------------------ the Q kernel
+template <int MT, int CG, bool BILIN>
+__global__ void __launch_bounds__(160, 1) bfq_q_kernel(const KParams p) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r0 = lane >> 2, kq = lane & 3;
+  const int NK = p.nk, QS = p.qs, K2S = p.k2s, CELLS = p.cells;
+
+  const long long item_idx = (long long)blockIdx.x / p.n_tiles;
+  const long long tile = (long long)blockIdx.x - item_idx * p.n_tiles;
+  const Item item = p.items[item_idx];
+  const Group grp = p.groups[item.l1];
+
+  // shared layout: barriers | R ring | Phi (per warp, 8 pairs) | f (cells)
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
+  uint64_t* empty = full + 8;
+  double* rs = reinterpret_cast<double*>(smem_raw + 128);
+  double* phis = rs + (size_t)p.nstage * NK * K2S;
+  double* fs = phis + (size_t)p.nw * 8 * K2S;
+  const int cell_elems = NK * QS;
+  const int nf = BILIN ? 2 : 1;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < p.nstage; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], (unsigned)item.n_units);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  // Phi padding columns (n_k^2 .. k2p) are read by stage 2 and must be 0.
+  for (int i = threadIdx.x; i < p.nw * 8 * K2S; i += blockDim.x) phis[i] = 0.0;
+  // stage the tile's cells: global (cell, k, q) -> shared (cell, k, q padded to QS)
+  {
+    const int ncq = NK * p.nq;
+    for (int arr = 0; arr < nf; ++arr) {
+      const double* src = arr == 0 ? p.f2 : p.f3;
+      for (int c = 0; c < CELLS; ++c) {
+        const long long cell = tile * CELLS + c;
+        double* dst = fs + (size_t)(arr * CELLS + c) * cell_elems;
+        const bool ok = cell < p.n_cells;
+        const double* s = src + (ok ? cell : 0) * (long long)ncq;
+        for (int i = threadIdx.x; i < ncq; i += blockDim.x) {
+          const int k = i / p.nq, q = i - k * p.nq;
+          dst[k * QS + q] = ok ? __ldg(s + i) : 0.0;
+        }
+      }
+    }
+  }
+  __syncthreads();
+
+  const int nch = grp.n_chan;
+  const unsigned rbytes = (unsigned)(NK * K2S * sizeof(double));
+
+  if (warp == p.nw) {
+    // ---------------- producer: stream R_tau blocks of this l1 group
+    if (lane == 0) {
+      for (int i = 0; i < nch; ++i) {
+        const int s = i % p.nstage;
+        if (i >= p.nstage) mbar_wait(&empty[s], (unsigned)((i / p.nstage) - 1) & 1u);
+        const ChanEntry ce = p.chans[grp.chan_off + i];
+        mbar_arrive_expect_tx(&full[s], rbytes);
+        bulk_g2s(rs + (size_t)s * NK * K2S, p.R + (size_t)ce.tau * NK * K2S, rbytes, &full[s]);
+      }
+    }
+    return;
+  }
+  if (warp >= item.n_units) return;
+
+  // ---------------- compute warp
+  const int unit = item.unit_base + warp;
+  double* phw = phis + (size_t)warp * 8 * K2S;
+  bool rowok[MT];
+  int rowoff[MT];
+#pragma unroll
+  for (int i = 0; i < MT; ++i) {
+    rowok[i] = (r0 + 8 * i) < NK;
+    rowoff[i] = (r0 + 8 * i) * QS;
+  }
+  double acc2[MT][2];
+#pragma unroll
+  for (int j = 0; j < MT; ++j) acc2[j][0] = acc2[j][1] = 0.0;
+
+  for (int i = 0; i < nch; ++i) {
+    const ChanEntry ce = p.chans[grp.chan_off + i];
+    const double wgt = ce.weight2 ? 2.0 : 1.0;
+    // ---- stage 1: Phi for this warp's 8 (m1, cell) pairs
+    for (int ml = 0; ml < p.m1t; ++ml) {
+      const int m1 = unit * p.m1t + ml;
+      int zs = 0, ze = 0;
+      if (m1 < grp.d1) {
+        zs = __ldg(p.sstart + ce.slice_base + m1);
+        ze = __ldg(p.sstart + ce.slice_base + m1 + 1);
+      }
+      for (int cg = 0; cg < CELLS; cg += CG) {
+        double acc[CG][MT][MT][2];
+#pragma unroll
+        for (int cc = 0; cc < CG; ++cc)
+#pragma unroll
+          for (int a = 0; a < MT; ++a)
+#pragma unroll
+            for (int b = 0; b < MT; ++b) acc[cc][a][b][0] = acc[cc][a][b][1] = 0.0;
+        for (int z0 = zs; z0 < ze; z0 += 4) {
+          const int z = z0 + kq;
+          Row rw;
+          if (z < ze) rw = load_row(p.rows, z);
+          else { rw.q2 = 0; rw.q3 = 0; rw.g = 0.0; }
+#pragma unroll
+          for (int cc = 0; cc < CG; ++cc) {
+            const double* fa = fs + (size_t)(cg + cc) * cell_elems + rw.q2;
+            const double* fb = fs + (size_t)((BILIN ? CELLS : 0) + cg + cc) * cell_elems + rw.q3;
+            double av[MT], bv[MT];
+#pragma unroll
+            for (int t = 0; t < MT; ++t) {
+              av[t] = rowok[t] ? rw.g * fa[rowoff[t]] : 0.0;
+              bv[t] = rowok[t] ? fb[rowoff[t]] : 0.0;
+            }
+#pragma unroll
+            for (int a = 0; a < MT; ++a)
+#pragma unroll
+              for (int b = 0; b < MT; ++b) dmma884(acc[cc][a][b][0], acc[cc][a][b][1], av[a], bv[b]);
+          }
+        }
+        // accumulator (a = 8A + r0, b = 8B + 2kq + e) -> Phi row of the pair
+#pragma unroll
+        for (int cc = 0; cc < CG; ++cc) {
+          double* ph = phw + (size_t)(ml * CELLS + cg + cc) * K2S;
+#pragma unroll
+          for (int a = 0; a < MT; ++a)
+#pragma unroll
+            for (int b = 0; b < MT; ++b)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const int ia = 8 * a + r0, ib = 8 * b + 2 * kq + e;
+                if (ia < NK && ib < NK) ph[ia * NK + ib] = wgt * acc[cc][a][b][e];
+              }
+        }
+      }
+    }
+    __syncwarp();
+    // ---- stage 2: out[pair, k1] += Phi[pair, :] . R_tau[k1, :]
+    const int s = i % p.nstage;
+    mbar_wait(&full[s], (unsigned)(i / p.nstage) & 1u);
+    const double* rb = rs + (size_t)s * NK * K2S + kq;
+    const double* pa = phw + (size_t)r0 * K2S + kq;
+#pragma unroll 4
+    for (int k0 = 0; k0 < p.k2p; k0 += 4) {
+      const double av = pa[k0];
+      double bv[MT];
+#pragma unroll
+      for (int j = 0; j < MT; ++j) bv[j] = rowok[j] ? rb[(size_t)(r0 + 8 * j) * K2S + k0] : 0.0;
+#pragma unroll
+      for (int j = 0; j < MT; ++j) dmma884(acc2[j][0], acc2[j][1], av, bv[j]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+
+  // ---------------- epilogue: pair r0 = (m1 = unit*m1t + r0/CELLS, cell = r0%CELLS)
+  const int ml = r0 / CELLS, c = r0 - ml * CELLS;
+  const int m1 = unit * p.m1t + ml;
+  const long long cell = tile * CELLS + c;
+  if (m1 < grp.d1 && cell < p.n_cells) {
+    const int l1 = grp.l1, q1 = l1 * l1 + m1;
+    double* qc = p.q + cell * (long long)NK * p.nq + q1;
+#pragma unroll
+    for (int j = 0; j < MT; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int k1 = 8 * j + 2 * kq + e;
+        if (k1 < NK) {
+          double v = acc2[j][e];
+          if (p.conservation && ((k1 == 0 && l1 <= 1) || (k1 == 1 && l1 == 0))) v = 0.0;
+          qc[(size_t)k1 * p.nq] = v;
+        }
+      }
+  }
+}
+
+typedef void (*QKernel)(const KParams);
+
+template <bool BILIN>
+QKernel pick_kernel(int mt, int cg) {
+  if (mt == 1) {
+    if (cg == 8) return bfq_q_kernel<1, 8, BILIN>;
+    if (cg == 4) return bfq_q_kernel<1, 4, BILIN>;
+    if (cg == 2) return bfq_q_kernel<1, 2, BILIN>;
+    return bfq_q_kernel<1, 1, BILIN>;
+  }
+  if (mt == 2) {
+    if (cg == 2) return bfq_q_kernel<2, 2, BILIN>;
+    return bfq_q_kernel<2, 1, BILIN>;
+  }
+  if (mt == 3) return bfq_q_kernel<3, 1, BILIN>;
+  return nullptr;
+}
+
+// ------------------------------------------------------------ small kernels
+// basis.moments (basis.py:346-363): mass c[0,0]; momentum (c[0,3], c[0,1], c[0,2]);
+// energy 0.5*(3*mass - sqrt(6)*c[1,0]).
+__global__ void moments_kernel(const double* c, double* out, long long n_cells, int nk, int nq, int l_max) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n_cells) return;
+  const double* v = c + i * (long long)nk * nq;
+  const double mass = v[0];
+  const double px = l_max >= 1 ? v[3] : 0.0, py = l_max >= 1 ? v[1] : 0.0, pz = l_max >= 1 ? v[2] : 0.0;
+  const double e2 = nk >= 2 ? v[nq] : 0.0;
+  double* o = out + i * 5;
+  o[0] = mass;
+  o[1] = px;
+  o[2] = py;
+  o[3] = pz;
+  o[4] = 0.5 * (3.0 * mass + (-2.449489742783178) * e2);
+}
+
+// RK4 stage helpers (harness.py:97-102).  Stage argument y + a*k is formed
+// in one pass; the final combination also flags non-finite entries.
+__global__ void axpy_kernel(const double* __restrict__ y, const double* __restrict__ k, double a,
+                            double* __restrict__ out, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = __dadd_rn(y[i], __dmul_rn(a, k[i]));  // numpy order: y + (a*k)
+}
+
+// y += dt/6 (k1 + 2 k2 + 2 k3 + k4) with k1..k3 accumulated in `acc` as
+// acc = k1 + 2k2 + 2k3 (built by rk4_accum) and k4 passed separately.
+__global__ void rk4_accum_kernel(double* __restrict__ acc, const double* __restrict__ k, double w, long long n,
+                                 int first) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    acc[i] = first ? k[i] : __dadd_rn(acc[i], __dmul_rn(w, k[i]));
+}
+
+__global__ void rk4_final_kernel(double* __restrict__ y, const double* __restrict__ acc,
+                                 const double* __restrict__ k4, double dt, long long n, int* flag) {
+  int bad = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    // same association as y + (dt/6)*(k1 + 2k2 + 2k3 + k4)
+    const double v = __dadd_rn(y[i], __dmul_rn(dt / 6.0, __dadd_rn(acc[i], k4[i])));
+    y[i] = v;
+    bad |= !isfinite(v);
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicExch(flag, 1);
+}
+
+}  // namespace
+
+// ------------------------------------------------------------ the plan
+struct bfq_plan {
+  int device = 0;
+  HostPlan hp;
+  double* R = nullptr;
+  Row* rows = nullptr;
+  int* sstart = nullptr;
+  DevProgram sym, full;
+  size_t operator_bytes = 0;
+};
+
+namespace {
+
+template <class T>
+int upload(const std::vector<T>& v, T** out, size_t& total) {
+  if (v.empty()) {
+    *out = nullptr;
+    return BFQ_OK;
+  }
+  BFQ_CUDA_TRY(cudaMalloc((void**)out, v.size() * sizeof(T)));
+  BFQ_CUDA_TRY(cudaMemcpy(*out, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  total += v.size() * sizeof(T);
+  return BFQ_OK;
+}
+
+int upload_program(const Program& pg, DevProgram& dp, size_t& total) {
+  dp.cfg = pg.cfg;
+  dp.bilinear = pg.bilinear;
+  dp.n_items = (int)pg.items.size();
+  dp.exec_macs_per_cell = pg.exec_macs_per_cell;
+  int rc;
+  if ((rc = upload(pg.chans, &dp.chans, total))) return rc;
+  if ((rc = upload(pg.groups, &dp.groups, total))) return rc;
+  if ((rc = upload(pg.items, &dp.items, total))) return rc;
+  QKernel k = pg.bilinear ? pick_kernel<true>(pg.cfg.mt, pg.cfg.cg) : pick_kernel<false>(pg.cfg.mt, pg.cfg.cg);
+  if (!k) {
+    set_error("no kernel instantiation for this tiling");
+    return BFQ_EINVAL;
+  }
+  BFQ_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, pg.cfg.smem));
+  return BFQ_OK;
+}
+
+void free_program(DevProgram& dp) {
+  cudaFree(dp.chans);
+  cudaFree(dp.groups);
+  cudaFree(dp.items);
+  dp.chans = nullptr;
+  dp.groups = nullptr;
+  dp.items = nullptr;
+}
+
+int launch_q(const bfq_plan* plan, const DevProgram& dp, const double* f2, const double* f3, double* q,
+             int64_t n_cells, cudaStream_t st) {
+  const HostPlan& hp = plan->hp;
+  if (n_cells == 0) return BFQ_OK;
+  KParams p;
+  p.f2 = f2;
+  p.f3 = f3 ? f3 : f2;
+  p.q = q;
+  p.n_cells = n_cells;
+  p.n_tiles = (n_cells + dp.cfg.cells - 1) / dp.cfg.cells;
+  p.R = plan->R;
+  p.rows = plan->rows;
+  p.sstart = plan->sstart;
+  p.chans = dp.chans;
+  p.groups = dp.groups;
+  p.items = dp.items;
+  p.nk = hp.n_k;
+  p.nq = hp.n_q;
+  p.qs = hp.qs;
+  p.k2s = hp.k2s;
+  p.k2p = hp.k2p;
+  p.cells = dp.cfg.cells;
+  p.m1t = dp.cfg.m1t;
+  p.nw = dp.cfg.nw;
+  p.nstage = dp.cfg.nstage;
+  p.conservation = hp.conservation ? 1 : 0;
+  const long long blocks = p.n_tiles * (long long)dp.n_items;
+  if (blocks > 0x7fffffffLL) {
+    set_error("too many cells for one launch");
+    return BFQ_EINVAL;
+  }
+  QKernel k = dp.bilinear ? pick_kernel<true>(dp.cfg.mt, dp.cfg.cg) : pick_kernel<false>(dp.cfg.mt, dp.cfg.cg);
+  k<<<(unsigned)blocks, (dp.cfg.nw + 1) * 32, dp.cfg.smem, st>>>(p);
+  BFQ_CUDA_TRY(cudaGetLastError());
+  return BFQ_OK;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+int plan_from_desc(const bfq_desc* desc, int device, bfq_plan** out) {
+  if (!desc || !out) {
+    set_error("null argument");
+    return BFQ_EINVAL;
+  }
+  *out = nullptr;
+  int ndev = 0;
+  BFQ_CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) {
+    set_error("device ordinal out of range");
+    return BFQ_EINVAL;
+  }
+  DeviceGuard guard(device);
+  int smem_optin = 0;
+  BFQ_CUDA_TRY(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+  std::unique_ptr<bfq_plan> plan(new (std::nothrow) bfq_plan());
+  if (!plan) {
+    set_error("host allocation failed");
+    return BFQ_ENOMEM;
+  }
+  plan->device = device;
+  int rc = build_host_plan(*desc, smem_optin, plan->hp);
+  if (rc) return rc;
+  size_t total = 0;
+  if ((rc = upload(plan->hp.rblocks, &plan->R, total)) || (rc = upload(plan->hp.rows, &plan->rows, total)) ||
+      (rc = upload(plan->hp.sstart, &plan->sstart, total)) ||
+      (rc = upload_program(plan->hp.sym, plan->sym, total)) ||
+      (rc = upload_program(plan->hp.full, plan->full, total))) {
+    bfq_plan_destroy(plan.release());
+    return rc;
+  }
+  plan->operator_bytes = total;
+  // host copies of the bulk data are no longer needed
+  std::vector<double>().swap(plan->hp.rblocks);
+  *out = plan.release();
+  return BFQ_OK;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------ C ABI
+extern "C" {
+
+int bfq_plan_create(const bfq_desc* desc, int device, bfq_plan** out) { return plan_from_desc(desc, device, out); }
+
+int bfq_plan_create_bfct(const char* path, int device, bfq_plan** out) {
+  if (!path || !out) {
+    set_error("null argument");
+    return BFQ_EINVAL;
+  }
+  BfctImage img;
+  int rc = read_bfct(path, img);
+  if (rc) return rc;
+  return plan_from_desc(&img.desc, device, out);
+}
+
+int bfq_plan_destroy(bfq_plan* plan) {
+  if (!plan) return BFQ_OK;
+  {
+    DeviceGuard guard(plan->device);
+    cudaFree(plan->R);
+    cudaFree(plan->rows);
+    cudaFree(plan->sstart);
+    free_program(plan->sym);
+    free_program(plan->full);
+  }
+  delete plan;
+  return BFQ_OK;
+}
+
+int bfq_plan_get_info(const bfq_plan* plan, bfq_plan_info* info) {
+  if (!plan || !info) {
+    set_error("null argument");
+    return BFQ_EINVAL;
+  }
+  const HostPlan& hp = plan->hp;
+  info->n_k = hp.n_k;
+  info->n_q = hp.n_q;
+  info->n_t = hp.n_t;
+  info->n_g = hp.n_g;
+  info->n_s = hp.n_s;
+  info->folded = hp.folded ? 1 : 0;
+  info->cells_per_cta = plan->sym.cfg.cells;
+  info->warps_per_cta = plan->sym.cfg.nw;
+  info->stages = plan->sym.cfg.nstage;
+  info->smem_bytes = plan->sym.cfg.smem;
+  info->items_per_tile = plan->sym.n_items;
+  info->exec_macs_per_cell = plan->sym.exec_macs_per_cell;
+  info->operator_bytes = (double)plan->operator_bytes;
+  return BFQ_OK;
+}
+
+int bfq_plan_work(const bfq_plan* plan, double* flops_per_cell, double* bytes_per_cell) {
+  if (!plan) {
+    set_error("null plan");
+    return BFQ_EINVAL;
+  }
+  if (flops_per_cell) *flops_per_cell = plan->hp.alg_flops_per_cell;
+  if (bytes_per_cell) *bytes_per_cell = plan->hp.alg_bytes_per_cell;
+  return BFQ_OK;
+}
+
+int bfq_eval(const bfq_plan* plan, const double* f2, const double* f3, double* q, int64_t n_cells, void* stream) {
+  if (!plan || n_cells < 0) {
+    set_error("invalid plan or cell count");
+    return BFQ_EINVAL;
+  }
+  if (n_cells > 0 && (!f2 || !q)) {
+    set_error("null buffer");
+    return BFQ_EINVAL;
+  }
+  DeviceGuard guard(plan->device);
+  const bool same = (f3 == nullptr || f3 == f2);
+  return launch_q(plan, same ? plan->sym : plan->full, f2, same ? f2 : f3, q, n_cells, (cudaStream_t)stream);
+}
+
+int bfq_eval_host(const bfq_plan* plan, const double* f2, const double* f3, double* q, int64_t n_cells) {
+  if (!plan || n_cells < 0 || (n_cells > 0 && (!f2 || !q))) {
+    set_error("invalid argument");
+    return BFQ_EINVAL;
+  }
+  if (n_cells == 0) return BFQ_OK;
+  DeviceGuard guard(plan->device);
+  const bool same = (f3 == nullptr || f3 == f2);
+  const size_t ndof = (size_t)plan->hp.n_k * plan->hp.n_q;
+  // chunked, two-stream pipeline: H2D(i+1) and D2H(i-1) overlap Q(i)
+  const int64_t chunk = std::min<int64_t>(n_cells, 4096);
+  const int nbuf = 2;
+  cudaStream_t st[nbuf];
+  double* dbuf[nbuf] = {nullptr, nullptr};
+  int rc = BFQ_OK;
+  for (int b = 0; b < nbuf; ++b) {
+    if (cudaStreamCreateWithFlags(&st[b], cudaStreamNonBlocking) != cudaSuccess) {
+      set_error("stream creation failed");
+      return BFQ_ECUDA;
+    }
+  }
+  const size_t per = chunk * ndof;
+  for (int b = 0; b < nbuf && rc == BFQ_OK; ++b)
+    if (cudaMalloc(&dbuf[b], per * sizeof(double) * (same ? 2 : 3)) != cudaSuccess) {
+      set_error("device allocation failed");
+      rc = BFQ_ENOMEM;
+    }
+  for (int64_t c0 = 0, i = 0; c0 < n_cells && rc == BFQ_OK; c0 += chunk, ++i) {
+    const int b = (int)(i % nbuf);
+    const int64_t n = std::min<int64_t>(chunk, n_cells - c0);
+    double* d2 = dbuf[b];
+    double* dq = d2 + per;
+    double* d3 = same ? d2 : dq + per;
+    const size_t bytes = n * ndof * sizeof(double);
+    if (cudaMemcpyAsync(d2, f2 + c0 * ndof, bytes, cudaMemcpyHostToDevice, st[b]) != cudaSuccess ||
+        (!same && cudaMemcpyAsync(d3, f3 + c0 * ndof, bytes, cudaMemcpyHostToDevice, st[b]) != cudaSuccess)) {
+      set_error("host-to-device copy failed");
+      rc = BFQ_ECUDA;
+      break;
+    }
+    rc = launch_q(plan, same ? plan->sym : plan->full, d2, d3, dq, n, st[b]);
+    if (rc) break;
+    if (cudaMemcpyAsync(q + c0 * ndof, dq, bytes, cudaMemcpyDeviceToHost, st[b]) != cudaSuccess) {
+      set_error("device-to-host copy failed");
+      rc = BFQ_ECUDA;
+    }
+  }
+  for (int b = 0; b < nbuf; ++b) {
+    if (cudaStreamSynchronize(st[b]) != cudaSuccess && rc == BFQ_OK) {
+      set_error(cudaGetErrorString(cudaGetLastError()));
+      rc = BFQ_ECUDA;
+    }
+    cudaFree(dbuf[b]);
+    cudaStreamDestroy(st[b]);
+  }
+  return rc;
+}
+
+int bfq_rk4_step(const bfq_plan* plan, double* y, double* work, int64_t n_cells, double dt, int32_t* flag,
+                 void* stream) {
+  if (!plan || !y || !work || !flag || n_cells < 0) {
+    set_error("invalid argument");
+    return BFQ_EINVAL;
+  }
+  if (n_cells == 0) return BFQ_OK;
+  DeviceGuard guard(plan->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const long long n = n_cells * (long long)plan->hp.n_k * plan->hp.n_q;
+  double* k = work;         // current stage derivative
+  double* arg = work + n;   // stage argument
+  double* acc = work + 2 * n;
+  const int tb = 256;
+  const int gb = (int)std::min<long long>((n + tb - 1) / tb, 148LL * 16);
+  int rc;
+  // k1 = Q(y)
+  if ((rc = launch_q(plan, plan->sym, y, y, k, n_cells, st))) return rc;
+  rk4_accum_kernel<<<gb, tb, 0, st>>>(acc, k, 1.0, n, 1);
+  axpy_kernel<<<gb, tb, 0, st>>>(y, k, 0.5 * dt, arg, n);
+  // k2 = Q(y + dt/2 k1)
+  if ((rc = launch_q(plan, plan->sym, arg, arg, k, n_cells, st))) return rc;
+  rk4_accum_kernel<<<gb, tb, 0, st>>>(acc, k, 2.0, n, 0);
+  axpy_kernel<<<gb, tb, 0, st>>>(y, k, 0.5 * dt, arg, n);
+  // k3 = Q(y + dt/2 k2)
+  if ((rc = launch_q(plan, plan->sym, arg, arg, k, n_cells, st))) return rc;
+  rk4_accum_kernel<<<gb, tb, 0, st>>>(acc, k, 2.0, n, 0);
+  axpy_kernel<<<gb, tb, 0, st>>>(y, k, dt, arg, n);
+  // k4 = Q(y + dt k3)
+  if ((rc = launch_q(plan, plan->sym, arg, arg, k, n_cells, st))) return rc;
+  rk4_final_kernel<<<gb, tb, 0, st>>>(y, acc, k, dt, n, flag);
+  BFQ_CUDA_TRY(cudaGetLastError());
+  return BFQ_OK;
+}
+
+int bfq_moments(const bfq_plan* plan, const double* c, double* out, int64_t n_cells, void* stream) {
+  if (!plan || n_cells < 0 || (n_cells > 0 && (!c || !out))) {
+    set_error("invalid argument");
+    return BFQ_EINVAL;
+  }
+  if (n_cells == 0) return BFQ_OK;
+  DeviceGuard guard(plan->device);
+  const int tb = 128;
+  moments_kernel<<<(unsigned)((n_cells + tb - 1) / tb), tb, 0, (cudaStream_t)stream>>>(
+      c, out, n_cells, plan->hp.n_k, plan->hp.n_q, plan->hp.l_max);
+  BFQ_CUDA_TRY(cudaGetLastError());
+  return BFQ_OK;
+}
+
+int bfq_host_plan_info(const bfq_desc* desc, int smem_limit, bfq_plan_info* info) {
+  if (!desc || !info) {
+    set_error("null argument");
+    return BFQ_EINVAL;
+  }
+  HostPlan hp;
+  int rc = build_host_plan(*desc, smem_limit, hp);
+  if (rc) return rc;
+  info->n_k = hp.n_k;
+  info->n_q = hp.n_q;
+  info->n_t = hp.n_t;
+  info->n_g = hp.n_g;
+  info->n_s = hp.n_s;
+  info->folded = hp.folded ? 1 : 0;
+  info->cells_per_cta = hp.sym.cfg.cells;
+  info->warps_per_cta = hp.sym.cfg.nw;
+  info->stages = hp.sym.cfg.nstage;
+  info->smem_bytes = hp.sym.cfg.smem;
+  info->items_per_tile = (int)hp.sym.items.size();
+  info->exec_macs_per_cell = hp.sym.exec_macs_per_cell;
+  info->operator_bytes = (double)(hp.rblocks.size() * sizeof(double) + hp.rows.size() * sizeof(Row) +
+                                  hp.sstart.size() * sizeof(int32_t));
+  return BFQ_OK;
+}
+
+const char* bfq_strerror(int code) {
+  switch (code) {
+    case BFQ_OK: return "success";
+    case BFQ_EINVAL: return "invalid argument or operator";
+    case BFQ_EUNSORTED: return "COO rows must be sorted and grouped by (tau, q1)";
+    case BFQ_ECUDA: return "CUDA error";
+    case BFQ_ENOMEM: return "out of memory";
+    case BFQ_ESMEM: return "no kernel configuration fits in shared memory";
+    case BFQ_EIO: return "I/O error";
+    case BFQ_EFORMAT: return "unrecognized or incompatible cache layout";
+    case BFQ_EINTEGRITY: return "cache payload does not match its checksum or advertised sizes";
+    case BFQ_EDIVERGED: return "integration diverged";
+    default: return "unknown error";
+  }
+}
+
+const char* bfq_last_error(void) { return get_error().c_str(); }
+
+}  // extern "C"

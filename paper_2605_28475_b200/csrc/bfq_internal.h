@@ -1,0 +1,105 @@
+// Internal structures shared by the host-side plan builder (bfq_plan.cpp) and
+// the device code (bfq_cuda.cu).  Not part of the ABI.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "bfq.h"
+
+namespace bfq {
+
+// One COO row as the kernel reads it: 16 bytes, one LDG.128 per row.
+struct alignas(16) Row {
+  int32_t q2;
+  int32_t q3;
+  double g;
+};
+
+// Channel-program entry: which R block to stream and where its slices start.
+struct alignas(16) ChanEntry {
+  int32_t tau;         // R block index (0-based channel)
+  int32_t slice_base;  // index into the expanded slice-start table; slice of m1 = base + m1
+  int32_t weight2;     // 1: contribution doubled (slot-symmetry fold, l2 < l3)
+  int32_t pad;
+};
+
+// Output-degree group: all channels sharing l1, i.e. one set of output columns.
+struct alignas(16) Group {
+  int32_t chan_off;  // first entry in the channel program
+  int32_t n_chan;
+  int32_t d1;        // 2*l1 + 1
+  int32_t l1;
+};
+
+// One CTA's work inside a cell tile: a run of m1-units of one l1 group.
+struct alignas(16) Item {
+  int32_t l1;
+  int32_t unit_base;
+  int32_t n_units;  // = active compute warps
+  int32_t pad;
+};
+
+// Kernel shape chosen at plan time for one program (folded or full).
+struct KernelConfig {
+  int mt = 0;      // ceil(n_k / 8): 8x8 DMMA tiles per radial axis
+  int cg = 0;      // cells per stage-1 register group
+  int cells = 0;   // cells per CTA tile
+  int m1t = 0;     // output m1 values per warp unit (cells * m1t == 8 DMMA rows)
+  int nw = 0;      // compute warps per CTA
+  int nstage = 0;  // R-block ring depth
+  int nf = 1;      // f arrays staged per cell (2 for bilinear Q(f2,f3))
+  int smem = 0;    // dynamic shared memory bytes
+};
+
+// Host image of one channel program (everything the kernel needs besides f and R).
+struct Program {
+  bool bilinear = false;
+  KernelConfig cfg;
+  std::vector<ChanEntry> chans;
+  std::vector<Group> groups;  // indexed by l1
+  std::vector<Item> items;    // heavy first
+  double exec_macs_per_cell = 0.0;
+};
+
+struct HostPlan {
+  int n_k = 0, n_q = 0, l_max = 0, k_max = 0, n_t = 0;
+  int64_t n_g = 0, n_s = 0;
+  double gamma = 0.0;
+  int qs = 0;   // smem row stride of f (doubles)
+  int k2p = 0;  // n_k^2 rounded up to 4 (stage-2 K extent)
+  int k2s = 0;  // row stride of Phi and R blocks (doubles)
+  bool conservation = false, detailed_balance = false;
+  bool folded = false;  // slot symmetry verified -> Q(f,f) uses the folded program
+  std::vector<int32_t> triplets;  // [n_t*3]
+  std::vector<Row> rows;          // [n_g] in table order
+  std::vector<int32_t> sstart;    // expanded slice starts: per channel d1 slices (+1 end)
+  std::vector<int32_t> chan_sbase;
+  std::vector<double> rblocks;    // [n_t][n_k][k2s], rblocks[t][k1][a*n_k+b] = R[k1,a,b,t]
+  Program sym;                    // Q(f,f) program (folded when `folded`)
+  Program full;                   // Q(f2,f3) program (all channels, weight 1)
+  double alg_flops_per_cell = 0.0, alg_bytes_per_cell = 0.0;
+};
+
+// Thread-local error detail.
+void set_error(const std::string& msg);
+const std::string& get_error();
+
+// Validate a descriptor and build the host image.  Returns BFQ_OK or a code.
+int build_host_plan(const bfq_desc& d, int smem_limit, HostPlan& hp);
+
+// Read a BFCT cache file (cache.py:21-39,66-89) into owned vectors + desc.
+struct BfctImage {
+  int32_t k_max = 0, l_max = 0;
+  double gamma = 0.0;
+  uint32_t flags = 0;
+  std::vector<int32_t> triplets, q1, q2, q3, tau, slice_tau, slice_q1;
+  std::vector<int64_t> slice_starts;
+  std::vector<double> g, r;
+  bfq_desc desc{};
+};
+int read_bfct(const char* path, BfctImage& img);
+
+uint32_t crc32_update(uint32_t crc, const unsigned char* data, size_t n);
+
+}  // namespace bfq

@@ -1,0 +1,374 @@
+// Host-side plan construction for the Q(f,f) engine: operator validation,
+// slot-symmetry folding, device data layout, kernel configuration and the
+// per-tile CTA schedule.  Pure C++ (no CUDA); bfq_cuda.cu uploads the result.
+//
+// Reference semantics followed here:
+//   * operator validation        -- FactorizedOperator.__post_init__, contraction.py:86-108
+//   * (tau, q1) sort guard        -- q_angular_first, contraction.py:297-301
+//   * slices over (tau, q1)       -- angular.py:272-285, cache.py:147-150
+//   * R layout (n_k,n_k,n_k,N_T)  -- kinematic.py:574-578, cache.py:61,139
+//   * BFCT file format            -- cache.py:1-19, :41, :52-63, :92-166
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <unordered_map>
+
+#include "bfq_internal.h"
+
+namespace bfq {
+
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+const std::string& get_error() { return g_err; }
+
+static int fail(int code, const std::string& msg) {
+  set_error(msg);
+  return code;
+}
+
+static inline int isqrt_floor(int x) {
+  int r = (int)std::sqrt((double)x);
+  while (r * r > x) --r;
+  while ((r + 1) * (r + 1) <= x) ++r;
+  return r;
+}
+
+// Stride rule for fp64 fragment gathers: lanes 0-15 of a DMMA operand load
+// touch rows r0 in 0..3 at columns c in 0..3 (row*stride + c).  With
+// stride = +-4 (mod 16) doubles those 16 addresses fall in 16 distinct
+// 8-byte bank pairs, i.e. one wavefront per 16 lanes.
+static int conflict_free_stride(int n) {
+  int s = (n + 3) / 4 * 4;
+  while (s % 16 != 4 && s % 16 != 12) s += 4;
+  return s;
+}
+
+static bool choose_config(int nk, int qs, int k2s, int nf, int smem_limit, KernelConfig& c) {
+  c.mt = (nk + 7) / 8;
+  c.nf = nf;
+  static const int cells_opts[] = {8, 4, 2, 1};
+  static const int ws[][2] = {{4, 2}, {4, 1}, {2, 2}, {2, 1}, {1, 1}};
+  for (int cells : cells_opts) {
+    for (auto& w : ws) {
+      long smem = 128 + (long)w[1] * nk * k2s * 8 + (long)w[0] * 8 * k2s * 8 +
+                  (long)nf * cells * nk * qs * 8;
+      if (smem <= smem_limit) {
+        c.cells = cells;
+        c.m1t = 8 / cells;
+        c.nw = w[0];
+        c.nstage = w[1];
+        c.smem = (int)smem;
+        c.cg = c.mt == 1 ? std::min(cells, 8) : (c.mt == 2 ? std::min(cells, 2) : 1);
+        return true;
+      }
+    }
+  }
+  return false;
+}
+
+// Build the CTA schedule of one program: per l1 group, units of m1t output
+// columns, packed nw units per CTA; ordered heavy-first.
+static void build_items(const HostPlan& hp, Program& pg) {
+  const KernelConfig& c = pg.cfg;
+  struct W {
+    Item it;
+    double work;
+  };
+  std::vector<W> all;
+  double total = 0.0;
+  const double stage2 = (double)c.mt * 256.0 * (hp.k2p / 4);
+  for (const Group& gr : pg.groups) {
+    if (gr.n_chan == 0) continue;
+    const int units = (gr.d1 + c.m1t - 1) / c.m1t;
+    const int n_items = (units + c.nw - 1) / c.nw;
+    int u = 0;
+    for (int i = 0; i < n_items; ++i) {
+      const int n = units / n_items + (i < units % n_items ? 1 : 0);
+      double work = 0.0;
+      for (int uu = u; uu < u + n; ++uu) {
+        for (int e = 0; e < gr.n_chan; ++e) {
+          const ChanEntry& ce = pg.chans[gr.chan_off + e];
+          for (int ml = 0; ml < c.m1t; ++ml) {
+            const int m1 = uu * c.m1t + ml;
+            if (m1 >= gr.d1) continue;
+            const int rows = hp.sstart[ce.slice_base + m1 + 1] - hp.sstart[ce.slice_base + m1];
+            work += (double)c.cells * c.mt * c.mt * 256.0 * ((rows + 3) / 4);
+          }
+          work += stage2;
+        }
+      }
+      all.push_back({Item{gr.l1, u, n, 0}, work});
+      total += work;
+      u += n;
+    }
+  }
+  std::stable_sort(all.begin(), all.end(), [](const W& a, const W& b) { return a.work > b.work; });
+  pg.items.clear();
+  for (auto& w : all) pg.items.push_back(w.it);
+  pg.exec_macs_per_cell = total / c.cells;
+}
+
+int build_host_plan(const bfq_desc& d, int smem_limit, HostPlan& hp) {
+  if (d.k_max < 0 || d.l_max < 0) return fail(BFQ_EINVAL, "truncation limits must be non-negative");
+  if (d.n_t <= 0 || d.n_g <= 0 || d.n_s <= 0) return fail(BFQ_EINVAL, "empty operator");
+  if (!d.triplets || !d.q1 || !d.q2 || !d.q3 || !d.tau || !d.g || !d.slice_starts ||
+      !d.slice_tau || !d.slice_q1 || !d.r)
+    return fail(BFQ_EINVAL, "null pointer in operator description");
+  if (d.n_s > d.n_g) return fail(BFQ_EINVAL, "slice count cannot exceed row count");
+  const int nk = d.k_max + 1, L = d.l_max, nq = (L + 1) * (L + 1);
+  if (nk > 24) return fail(BFQ_EINVAL, "n_k > 24 not supported by the DMMA tiling");
+  hp.n_k = nk;
+  hp.n_q = nq;
+  hp.k_max = d.k_max;
+  hp.l_max = L;
+  hp.n_t = d.n_t;
+  hp.n_g = d.n_g;
+  hp.n_s = d.n_s;
+  hp.gamma = d.gamma;
+  hp.conservation = d.conservation != 0;
+  hp.detailed_balance = d.detailed_balance != 0;
+  hp.qs = conflict_free_stride(nq);
+  hp.k2p = (nk * nk + 3) / 4 * 4;
+  hp.k2s = conflict_free_stride(hp.k2p);
+
+  // channel table (angular.py:119-135)
+  hp.triplets.assign(d.triplets, d.triplets + 3 * (size_t)d.n_t);
+  std::unordered_map<long, int> chan_of;
+  for (int t = 0; t < d.n_t; ++t) {
+    const int l1 = hp.triplets[3 * t], l2 = hp.triplets[3 * t + 1], l3 = hp.triplets[3 * t + 2];
+    if (l1 < 0 || l2 < 0 || l3 < 0 || l1 > L || l2 > L || l3 > L)
+      return fail(BFQ_EINVAL, "channel triplet out of range");
+    chan_of[((long)l1 * 64 + l2) * 64 + l3] = t;
+  }
+
+  // rows: range checks (contraction.py:90-95), degree consistency, sort guard
+  auto lq = [](int q) { return isqrt_floor(q); };
+  hp.rows.resize(d.n_g);
+  for (int64_t z = 0; z < d.n_g; ++z) {
+    const int t = d.tau[z], q1 = d.q1[z], q2 = d.q2[z], q3 = d.q3[z];
+    if (t < 0 || t >= d.n_t) return fail(BFQ_EINVAL, "channel index out of range");
+    if (q1 < 0 || q1 >= nq || q2 < 0 || q2 >= nq || q3 < 0 || q3 >= nq)
+      return fail(BFQ_EINVAL, "angular index out of range");
+    if (lq(q1) != hp.triplets[3 * t] || lq(q2) != hp.triplets[3 * t + 1] ||
+        lq(q3) != hp.triplets[3 * t + 2])
+      return fail(BFQ_EINVAL, "row degrees disagree with its channel triplet");
+    if (z > 0) {
+      const long kprev = (long)d.tau[z - 1] * nq + d.q1[z - 1], key = (long)t * nq + q1;
+      if (key < kprev) return fail(BFQ_EUNSORTED, "COO rows must be sorted and grouped by (tau, q1)");
+    }
+    hp.rows[z] = Row{q2, q3, d.g[z]};
+  }
+  // slices (angular.py:275-285): consistent with the rows they cover
+  if (d.slice_starts[0] != 0 || d.slice_starts[d.n_s] != d.n_g)
+    return fail(BFQ_EINVAL, "slice_starts must span [0, n_g]");
+  for (int64_t s = 0; s < d.n_s; ++s) {
+    const int64_t a = d.slice_starts[s], b = d.slice_starts[s + 1];
+    if (b <= a) return fail(BFQ_EINVAL, "empty or decreasing slice");
+    for (int64_t z = a; z < b; ++z)
+      if (d.tau[z] != d.slice_tau[s] || d.q1[z] != d.slice_q1[s])
+        return fail(BFQ_EINVAL, "slice does not match the (tau, q1) of its rows");
+    if (s > 0 && d.slice_tau[s] == d.slice_tau[s - 1] && d.slice_q1[s] == d.slice_q1[s - 1])
+      return fail(BFQ_EINVAL, "duplicate (tau, q1) slice");
+  }
+
+  // expanded slice table: every (tau, m1) gets a (possibly empty) row range
+  hp.chan_sbase.resize(d.n_t);
+  hp.sstart.clear();
+  {
+    std::vector<long> keys(d.n_g);
+    for (int64_t z = 0; z < d.n_g; ++z) keys[z] = (long)d.tau[z] * nq + d.q1[z];
+    for (int t = 0; t < d.n_t; ++t) {
+      const int l1 = hp.triplets[3 * t];
+      hp.chan_sbase[t] = (int)hp.sstart.size();
+      for (int m1 = 0; m1 < 2 * l1 + 1; ++m1) {
+        const long key = (long)t * nq + l1 * l1 + m1;
+        hp.sstart.push_back((int32_t)(std::lower_bound(keys.begin(), keys.end(), key) - keys.begin()));
+      }
+    }
+    hp.sstart.push_back((int32_t)d.n_g);
+  }
+
+  // R blocks: rblocks[t][k1][a*nk+b] = R[k1,a,b,t]; zero padding to k2s
+  const size_t blk = (size_t)nk * hp.k2s;
+  hp.rblocks.assign((size_t)d.n_t * blk, 0.0);
+  for (int k1 = 0; k1 < nk; ++k1)
+    for (int a = 0; a < nk; ++a)
+      for (int b = 0; b < nk; ++b) {
+        const double* src = d.r + (((size_t)k1 * nk + a) * nk + b) * d.n_t;
+        for (int t = 0; t < d.n_t; ++t) hp.rblocks[t * blk + (size_t)k1 * hp.k2s + a * nk + b] = src[t];
+      }
+
+  // slot-symmetry check (SURVEY §7 hard part f): table closed under
+  // (q2,q3,(l1,l2,l3)) <-> (q3,q2,(l1,l3,l2)) with identical g, and R exactly
+  // symmetric under (k2,k3,tau) <-> (k3,k2,tau').  Then the tau and tau'
+  // contributions to Q(f,f) are equal and only l2 <= l3 channels are evaluated.
+  bool fold = true;
+  std::vector<int> swap_of(d.n_t, -1);
+  for (int t = 0; t < d.n_t && fold; ++t) {
+    auto it = chan_of.find(((long)hp.triplets[3 * t] * 64 + hp.triplets[3 * t + 2]) * 64 + hp.triplets[3 * t + 1]);
+    if (it == chan_of.end()) fold = false;
+    else swap_of[t] = it->second;
+  }
+  if (fold) {
+    for (int t = 0; t < d.n_t && fold; ++t) {
+      const int u = swap_of[t];
+      for (int k1 = 0; k1 < nk && fold; ++k1)
+        for (int a = 0; a < nk && fold; ++a)
+          for (int b = 0; b < nk; ++b)
+            if (hp.rblocks[t * blk + (size_t)k1 * hp.k2s + a * nk + b] !=
+                hp.rblocks[u * blk + (size_t)k1 * hp.k2s + b * nk + a]) {
+              fold = false;
+              break;
+            }
+    }
+  }
+  if (fold) {
+    std::unordered_map<uint64_t, double> gmap;
+    gmap.reserve(d.n_g * 2);
+    auto rk = [&](int t, int q1, int q2, int q3) {
+      return (((uint64_t)t * nq + q1) * nq + q2) * nq + q3;
+    };
+    for (int64_t z = 0; z < d.n_g; ++z) gmap[rk(d.tau[z], d.q1[z], d.q2[z], d.q3[z])] = d.g[z];
+    for (int64_t z = 0; z < d.n_g && fold; ++z) {
+      auto it = gmap.find(rk(swap_of[d.tau[z]], d.q1[z], d.q3[z], d.q2[z]));
+      if (it == gmap.end() || it->second != d.g[z]) fold = false;
+    }
+  }
+  hp.folded = fold;
+
+  // channel programs, grouped by l1 (output columns)
+  auto make_program = [&](Program& pg, bool bilinear, bool use_fold) -> bool {
+    pg.bilinear = bilinear;
+    pg.chans.clear();
+    pg.groups.assign(L + 1, Group{0, 0, 0, 0});
+    for (int l1 = 0; l1 <= L; ++l1) {
+      pg.groups[l1].chan_off = (int)pg.chans.size();
+      pg.groups[l1].d1 = 2 * l1 + 1;
+      pg.groups[l1].l1 = l1;
+      for (int t = 0; t < d.n_t; ++t) {
+        if (hp.triplets[3 * t] != l1) continue;
+        const int l2 = hp.triplets[3 * t + 1], l3 = hp.triplets[3 * t + 2];
+        int w2 = 0;
+        if (use_fold) {
+          if (l2 > l3) continue;
+          w2 = l2 < l3 ? 1 : 0;
+        }
+        pg.chans.push_back(ChanEntry{t, hp.chan_sbase[t], w2, 0});
+      }
+      pg.groups[l1].n_chan = (int)pg.chans.size() - pg.groups[l1].chan_off;
+    }
+    if (!choose_config(nk, hp.qs, hp.k2s, bilinear ? 2 : 1, smem_limit, pg.cfg)) return false;
+    build_items(hp, pg);
+    return true;
+  };
+  if (!make_program(hp.sym, false, fold) || !make_program(hp.full, true, false))
+    return fail(BFQ_ESMEM, "no kernel configuration fits in shared memory for this n_k, l_max");
+
+  hp.alg_flops_per_cell = 2.0 * ((double)d.n_g * nk * nk + (double)d.n_s * nk * nk * nk);
+  hp.alg_bytes_per_cell = 16.0 * nk * nq;
+  return BFQ_OK;
+}
+
+// ---------------------------------------------------------------- BFCT reader
+uint32_t crc32_update(uint32_t crc, const unsigned char* data, size_t n) {
+  static uint32_t table[256];
+  static bool init = false;
+  if (!init) {
+    for (uint32_t i = 0; i < 256; ++i) {
+      uint32_t c = i;
+      for (int k = 0; k < 8; ++k) c = (c & 1) ? (0xEDB88320u ^ (c >> 1)) : (c >> 1);
+      table[i] = c;
+    }
+    init = true;
+  }
+  crc = ~crc;
+  for (size_t i = 0; i < n; ++i) crc = table[(crc ^ data[i]) & 0xFF] ^ (crc >> 8);
+  return ~crc;
+}
+
+template <class T>
+static T rd(const unsigned char* p) {
+  T v;
+  std::memcpy(&v, p, sizeof(T));
+  return v;
+}
+
+int read_bfct(const char* path, BfctImage& img) {
+  FILE* fp = std::fopen(path, "rb");
+  if (!fp) return fail(BFQ_EIO, std::string("cannot open ") + path);
+  std::vector<unsigned char> blob;
+  unsigned char buf[1 << 16];
+  size_t n;
+  while ((n = std::fread(buf, 1, sizeof buf, fp)) > 0) blob.insert(blob.end(), buf, buf + n);
+  std::fclose(fp);
+  // header "<4sIIId9IIQII" = 80 bytes (cache.py:41)
+  const size_t H = 80;
+  if (blob.size() < H) return fail(BFQ_EFORMAT, "file too short for a cache header");
+  if (std::memcmp(blob.data(), "BFCT", 4) != 0) return fail(BFQ_EFORMAT, "bad magic");
+  const uint32_t version = rd<uint32_t>(&blob[4]);
+  if (version != 1) return fail(BFQ_EFORMAT, "cache format version unsupported (expected 1)");
+  img.k_max = (int32_t)rd<uint32_t>(&blob[8]);
+  img.l_max = (int32_t)rd<uint32_t>(&blob[12]);
+  img.gamma = rd<double>(&blob[16]);
+  // 9 x u32 grid spec at 24..59
+  const uint32_t n_t = rd<uint32_t>(&blob[60]);
+  const uint64_t n_g = rd<uint64_t>(&blob[64]);
+  img.flags = rd<uint32_t>(&blob[72]);
+  const uint32_t crc = rd<uint32_t>(&blob[76]);
+  const unsigned char* pay = blob.data() + H;
+  const size_t plen = blob.size() - H;
+  if (crc32_update(0, pay, plen) != crc) return fail(BFQ_EINTEGRITY, "payload checksum mismatch");
+  const uint64_t nk = (uint64_t)img.k_max + 1;
+  const uint64_t expected = (uint64_t)n_t * 12 + n_g * 24 + nk * nk * nk * n_t * 8;
+  if (plen != expected) return fail(BFQ_EINTEGRITY, "payload size disagrees with header");
+  size_t off = 0;
+  img.triplets.resize((size_t)n_t * 3);
+  for (size_t i = 0; i < img.triplets.size(); ++i, off += 4) img.triplets[i] = (int32_t)rd<uint32_t>(pay + off);
+  auto col = [&](std::vector<int32_t>& v) {
+    v.resize(n_g);
+    for (uint64_t i = 0; i < n_g; ++i, off += 4) v[i] = (int32_t)rd<uint32_t>(pay + off) - 1;  // 1-based -> 0-based
+  };
+  col(img.q1);
+  col(img.q2);
+  col(img.q3);
+  col(img.tau);
+  img.g.resize(n_g);
+  std::memcpy(img.g.data(), pay + off, n_g * 8);
+  off += n_g * 8;
+  img.r.resize(nk * nk * nk * n_t);
+  std::memcpy(img.r.data(), pay + off, img.r.size() * 8);
+  // slices: boundaries of key = tau*(l_max+1)^2 + q1 (cache.py:147-150)
+  const long nq = (long)(img.l_max + 1) * (img.l_max + 1);
+  img.slice_starts.clear();
+  for (uint64_t z = 0; z < n_g; ++z) {
+    if (z == 0 || (long)img.tau[z] * nq + img.q1[z] != (long)img.tau[z - 1] * nq + img.q1[z - 1]) {
+      img.slice_starts.push_back((int64_t)z);
+      img.slice_tau.push_back(img.tau[z]);
+      img.slice_q1.push_back(img.q1[z]);
+    }
+  }
+  img.slice_starts.push_back((int64_t)n_g);
+  bfq_desc& d = img.desc;
+  d.k_max = img.k_max;
+  d.l_max = img.l_max;
+  d.gamma = img.gamma;
+  d.n_t = (int32_t)n_t;
+  d.n_g = (int64_t)n_g;
+  d.n_s = (int64_t)img.slice_tau.size();
+  d.triplets = img.triplets.data();
+  d.q1 = img.q1.data();
+  d.q2 = img.q2.data();
+  d.q3 = img.q3.data();
+  d.tau = img.tau.data();
+  d.g = img.g.data();
+  d.slice_starts = img.slice_starts.data();
+  d.slice_tau = img.slice_tau.data();
+  d.slice_q1 = img.slice_q1.data();
+  d.r = img.r.data();
+  d.conservation = (img.flags & 1) ? 1 : 0;
+  d.detailed_balance = (img.flags & 2) ? 1 : 0;
+  return BFQ_OK;
+}
+
+}  // namespace bfq
