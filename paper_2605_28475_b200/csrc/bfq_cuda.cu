@@ -70,10 +70,31 @@ struct KParams {
 };
 
 // ------------------------------------------------------------ PTX helpers
+// Not volatile: the scheduler may move shared loads across DMMAs.
 __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(d0), "+d"(d1)
-               : "d"(a), "d"(b));
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+
+// Gather from the staged cells: read-only after the staging barrier, so a
+// plain (non-volatile) asm the compiler may schedule freely.
+__device__ __forceinline__ double lds_ro(uint32_t addr) {
+  double v;
+  asm("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(addr));
+  return v;
+}
+
+// Loads/stores of buffers rewritten inside the kernel (Phi, R ring): volatile
+// so they stay ordered with the warp syncs and mbarrier waits.
+__device__ __forceinline__ double lds_v(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(addr) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void sts_v(uint32_t addr, double v) {
+  asm volatile("st.shared.f64 [%0], %1;\n" ::"r"(addr), "d"(v) : "memory");
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -125,89 +146,112 @@ __device__ __forceinline__ Row load_row(const Row* rows, int z) {
   return r;
 }
 
+__device__ __forceinline__ Row fetch_row(const Row* rows, int z, int ze) {
+  if (z < ze) return load_row(rows, z);
+  Row r;
+  r.q2 = 0;
+  r.q3 = 0;
+  r.g = 0.0;
+  return r;
+}
+
 // ------------------------------------------------------------ the Q kernel
+// Block = nw compute warps + 2 producer warps (one per team).
 template <int MT, int CG, bool BILIN>
-__global__ void __launch_bounds__(160, 1) bfq_q_kernel(const KParams p) {
+__global__ void __launch_bounds__(320, 1) bfq_q_kernel(const KParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r0 = lane >> 2, kq = lane & 3;
-  const int NK = p.nk, QS = p.qs, K2S = p.k2s, CELLS = p.cells;
+  const int NK = p.nk, QS = p.qs, K2S = p.k2s, CELLS = p.cells, NST = p.nstage;
 
   const long long item_idx = (long long)blockIdx.x / p.n_tiles;
   const long long tile = (long long)blockIdx.x - item_idx * p.n_tiles;
   const Item item = p.items[item_idx];
-  const Group grp = p.groups[item.l1];
 
-  // shared layout: barriers | R ring | Phi (per warp, 8 pairs) | f (cells)
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
+  // shared layout: barriers | R rings (team, stage) | Phi (per warp, 8 pairs) | f (cells)
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);  // [team*4 + stage]
   uint64_t* empty = full + 8;
   double* rs = reinterpret_cast<double*>(smem_raw + 128);
-  double* phis = rs + (size_t)p.nstage * NK * K2S;
+  const size_t rblk = (size_t)NK * K2S;
+  double* phis = rs + 2 * (size_t)NST * rblk;
   double* fs = phis + (size_t)p.nw * 8 * K2S;
   const int cell_elems = NK * QS;
   const int nf = BILIN ? 2 : 1;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < p.nstage; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], (unsigned)item.n_units);
-    }
+    for (int t = 0; t < 2; ++t)
+      for (int s = 0; s < NST; ++s) {
+        mbar_init(&full[t * 4 + s], 1);
+        mbar_init(&empty[t * 4 + s], (unsigned)max(item.nunits[t], 1));
+      }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   // Phi padding columns (n_k^2 .. k2p) are read by stage 2 and must be 0.
   for (int i = threadIdx.x; i < p.nw * 8 * K2S; i += blockDim.x) phis[i] = 0.0;
-  // stage the tile's cells: global (cell, k, q) -> shared (cell, k, q padded to QS)
+  // stage the tile's cells: global (cell, k, q) -> shared (cell, k, q padded to QS);
+  // one warp per (array, cell, k) row, lanes over q
   {
-    const int ncq = NK * p.nq;
-    for (int arr = 0; arr < nf; ++arr) {
-      const double* src = arr == 0 ? p.f2 : p.f3;
-      for (int c = 0; c < CELLS; ++c) {
-        const long long cell = tile * CELLS + c;
-        double* dst = fs + (size_t)(arr * CELLS + c) * cell_elems;
-        const bool ok = cell < p.n_cells;
-        const double* s = src + (ok ? cell : 0) * (long long)ncq;
-        for (int i = threadIdx.x; i < ncq; i += blockDim.x) {
-          const int k = i / p.nq, q = i - k * p.nq;
-          dst[k * QS + q] = ok ? __ldg(s + i) : 0.0;
-        }
-      }
+    const int rows_total = nf * CELLS * NK;
+    const int nwarps = blockDim.x >> 5;
+    for (int row = warp; row < rows_total; row += nwarps) {
+      const int arr = row / (CELLS * NK);
+      const int rem = row - arr * CELLS * NK;
+      const int c = rem / NK, k = rem - c * NK;
+      const long long cell = tile * CELLS + c;
+      const double* src = (arr == 0 ? p.f2 : p.f3) + (cell < p.n_cells ? cell : 0) * (long long)NK * p.nq +
+                          (long long)k * p.nq;
+      double* dst = fs + (size_t)(arr * CELLS + c) * cell_elems + (size_t)k * QS;
+      const bool ok = cell < p.n_cells;
+      for (int q = lane; q < p.nq; q += 32) dst[q] = ok ? __ldg(src + q) : 0.0;
     }
   }
   __syncthreads();
 
-  const int nch = grp.n_chan;
-  const unsigned rbytes = (unsigned)(NK * K2S * sizeof(double));
-
-  if (warp == p.nw) {
-    // ---------------- producer: stream R_tau blocks of this l1 group
-    if (lane == 0) {
-      for (int i = 0; i < nch; ++i) {
-        const int s = i % p.nstage;
-        if (i >= p.nstage) mbar_wait(&empty[s], (unsigned)((i / p.nstage) - 1) & 1u);
+  const unsigned rbytes = (unsigned)(rblk * sizeof(double));
+  if (warp >= p.nw) {
+    // ---------------- producers: producer warp t streams team t's R_tau blocks
+    const int t = warp - p.nw;
+    if (lane == 0 && item.nunits[t] > 0) {
+      const Group grp = p.groups[item.l1[t]];
+      double* ring = rs + (size_t)t * NST * rblk;
+      for (int i = 0; i < grp.n_chan; ++i) {
+        const int s = i % NST;
+        if (i >= NST) mbar_wait(&empty[t * 4 + s], (unsigned)((i / NST) - 1) & 1u);
         const ChanEntry ce = p.chans[grp.chan_off + i];
-        mbar_arrive_expect_tx(&full[s], rbytes);
-        bulk_g2s(rs + (size_t)s * NK * K2S, p.R + (size_t)ce.tau * NK * K2S, rbytes, &full[s]);
+        mbar_arrive_expect_tx(&full[t * 4 + s], rbytes);
+        bulk_g2s(ring + (size_t)s * rblk, p.R + (size_t)ce.tau * rblk, rbytes, &full[t * 4 + s]);
       }
     }
     return;
   }
-  if (warp >= item.n_units) return;
+  const int team = warp < item.nunits[0] ? 0 : 1;
+  const int twarp = team == 0 ? warp : warp - item.nunits[0];
+  if (team == 1 && twarp >= item.nunits[1]) return;
 
   // ---------------- compute warp
-  const int unit = item.unit_base + warp;
-  double* phw = phis + (size_t)warp * 8 * K2S;
-  bool rowok[MT];
-  int rowoff[MT];
+  const Group grp = p.groups[item.l1[team]];
+  const int unit = item.ubase[team] + twarp;
+  uint64_t* tfull = full + team * 4;
+  uint64_t* tempty = empty + team * 4;
+  const uint32_t ring_u32 = smem_u32(rs + (size_t)team * NST * rblk);
+  const uint32_t phw_u32 = smem_u32(phis + (size_t)warp * 8 * K2S);
+  const uint32_t fs_u32 = smem_u32(fs);
+  const uint32_t cell_bytes = (uint32_t)cell_elems * 8u;
+  // Operand rows beyond n_k (DMMA padding) read a clamped valid row: their
+  // products only reach accumulator entries (a or b >= n_k, k1 >= n_k) that
+  // are never stored, so no zero padding or predication is needed.
+  uint32_t frow[MT], rrow[MT];
 #pragma unroll
   for (int i = 0; i < MT; ++i) {
-    rowok[i] = (r0 + 8 * i) < NK;
-    rowoff[i] = (r0 + 8 * i) * QS;
+    const int r = min(r0 + 8 * i, NK - 1);
+    frow[i] = (uint32_t)(r * QS) * 8u;
+    rrow[i] = (uint32_t)(r * K2S + kq) * 8u;
   }
   double acc2[MT][2];
 #pragma unroll
   for (int j = 0; j < MT; ++j) acc2[j][0] = acc2[j][1] = 0.0;
 
-  for (int i = 0; i < nch; ++i) {
+  for (int i = 0; i < grp.n_chan; ++i) {
     const ChanEntry ce = p.chans[grp.chan_off + i];
     const double wgt = ce.weight2 ? 2.0 : 1.0;
     // ---- stage 1: Phi for this warp's 8 (m1, cell) pairs
@@ -226,20 +270,22 @@ __global__ void __launch_bounds__(160, 1) bfq_q_kernel(const KParams p) {
           for (int a = 0; a < MT; ++a)
 #pragma unroll
             for (int b = 0; b < MT; ++b) acc[cc][a][b][0] = acc[cc][a][b][1] = 0.0;
+        const uint32_t fa0 = fs_u32 + (uint32_t)cg * cell_bytes;
+        const uint32_t fb0 = fs_u32 + (uint32_t)((BILIN ? CELLS : 0) + cg) * cell_bytes;
+        // software-pipelined over k-steps: the CG-table row of step s+1 is in
+        // flight while step s issues its gathers and DMMAs
+        Row nxt = fetch_row(p.rows, zs + kq, ze);
         for (int z0 = zs; z0 < ze; z0 += 4) {
-          const int z = z0 + kq;
-          Row rw;
-          if (z < ze) rw = load_row(p.rows, z);
-          else { rw.q2 = 0; rw.q3 = 0; rw.g = 0.0; }
+          const Row rw = nxt;
+          nxt = fetch_row(p.rows, z0 + 4 + kq, ze);
+          const uint32_t qa = fa0 + (uint32_t)rw.q2 * 8u, qb = fb0 + (uint32_t)rw.q3 * 8u;
 #pragma unroll
           for (int cc = 0; cc < CG; ++cc) {
-            const double* fa = fs + (size_t)(cg + cc) * cell_elems + rw.q2;
-            const double* fb = fs + (size_t)((BILIN ? CELLS : 0) + cg + cc) * cell_elems + rw.q3;
             double av[MT], bv[MT];
 #pragma unroll
             for (int t = 0; t < MT; ++t) {
-              av[t] = rowok[t] ? rw.g * fa[rowoff[t]] : 0.0;
-              bv[t] = rowok[t] ? fb[rowoff[t]] : 0.0;
+              av[t] = rw.g * lds_ro(qa + cc * cell_bytes + frow[t]);
+              bv[t] = lds_ro(qb + cc * cell_bytes + frow[t]);
             }
 #pragma unroll
             for (int a = 0; a < MT; ++a)
@@ -250,7 +296,7 @@ __global__ void __launch_bounds__(160, 1) bfq_q_kernel(const KParams p) {
         // accumulator (a = 8A + r0, b = 8B + 2kq + e) -> Phi row of the pair
 #pragma unroll
         for (int cc = 0; cc < CG; ++cc) {
-          double* ph = phw + (size_t)(ml * CELLS + cg + cc) * K2S;
+          const uint32_t ph = phw_u32 + (uint32_t)((ml * CELLS + cg + cc) * K2S) * 8u;
 #pragma unroll
           for (int a = 0; a < MT; ++a)
 #pragma unroll
@@ -258,28 +304,28 @@ __global__ void __launch_bounds__(160, 1) bfq_q_kernel(const KParams p) {
 #pragma unroll
               for (int e = 0; e < 2; ++e) {
                 const int ia = 8 * a + r0, ib = 8 * b + 2 * kq + e;
-                if (ia < NK && ib < NK) ph[ia * NK + ib] = wgt * acc[cc][a][b][e];
+                if (ia < NK && ib < NK) sts_v(ph + (uint32_t)(ia * NK + ib) * 8u, wgt * acc[cc][a][b][e]);
               }
         }
       }
     }
     __syncwarp();
     // ---- stage 2: out[pair, k1] += Phi[pair, :] . R_tau[k1, :]
-    const int s = i % p.nstage;
-    mbar_wait(&full[s], (unsigned)(i / p.nstage) & 1u);
-    const double* rb = rs + (size_t)s * NK * K2S + kq;
-    const double* pa = phw + (size_t)r0 * K2S + kq;
+    const int s = i % NST;
+    mbar_wait(&tfull[s], (unsigned)(i / NST) & 1u);
+    const uint32_t rb = ring_u32 + (uint32_t)(s * rblk) * 8u;
+    const uint32_t pa = phw_u32 + (uint32_t)(r0 * K2S + kq) * 8u;
 #pragma unroll 4
     for (int k0 = 0; k0 < p.k2p; k0 += 4) {
-      const double av = pa[k0];
+      const double av = lds_v(pa + k0 * 8);
       double bv[MT];
 #pragma unroll
-      for (int j = 0; j < MT; ++j) bv[j] = rowok[j] ? rb[(size_t)(r0 + 8 * j) * K2S + k0] : 0.0;
+      for (int j = 0; j < MT; ++j) bv[j] = lds_v(rb + rrow[j] + k0 * 8);
 #pragma unroll
       for (int j = 0; j < MT; ++j) dmma884(acc2[j][0], acc2[j][1], av, bv[j]);
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
+    if (lane == 0) mbar_arrive(&tempty[s]);
   }
 
   // ---------------- epilogue: pair r0 = (m1 = unit*m1t + r0/CELLS, cell = r0%CELLS)
@@ -314,10 +360,16 @@ QKernel pick_kernel(int mt, int cg) {
     return bfq_q_kernel<1, 1, BILIN>;
   }
   if (mt == 2) {
+    if (cg == 8) return bfq_q_kernel<2, 8, BILIN>;
+    if (cg == 4) return bfq_q_kernel<2, 4, BILIN>;
     if (cg == 2) return bfq_q_kernel<2, 2, BILIN>;
     return bfq_q_kernel<2, 1, BILIN>;
   }
-  if (mt == 3) return bfq_q_kernel<3, 1, BILIN>;
+  if (mt == 3) {
+    if (cg == 4) return bfq_q_kernel<3, 4, BILIN>;
+    if (cg == 2) return bfq_q_kernel<3, 2, BILIN>;
+    return bfq_q_kernel<3, 1, BILIN>;
+  }
   return nullptr;
 }
 
@@ -394,7 +446,7 @@ int upload(const std::vector<T>& v, T** out, size_t& total) {
   return BFQ_OK;
 }
 
-int upload_program(const Program& pg, DevProgram& dp, size_t& total) {
+int upload_program(const Program& pg, DevProgram& dp, size_t& total, int smem_optin) {
   dp.cfg = pg.cfg;
   dp.bilinear = pg.bilinear;
   dp.n_items = (int)pg.items.size();
@@ -408,7 +460,9 @@ int upload_program(const Program& pg, DevProgram& dp, size_t& total) {
     set_error("no kernel instantiation for this tiling");
     return BFQ_EINVAL;
   }
-  BFQ_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, pg.cfg.smem));
+  // Kernel attributes are global per instantiation: always allow the device
+  // maximum so plans of different sizes sharing a kernel never shrink it.
+  BFQ_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin));
   return BFQ_OK;
 }
 
@@ -453,7 +507,7 @@ int launch_q(const bfq_plan* plan, const DevProgram& dp, const double* f2, const
     return BFQ_EINVAL;
   }
   QKernel k = dp.bilinear ? pick_kernel<true>(dp.cfg.mt, dp.cfg.cg) : pick_kernel<false>(dp.cfg.mt, dp.cfg.cg);
-  k<<<(unsigned)blocks, (dp.cfg.nw + 1) * 32, dp.cfg.smem, st>>>(p);
+  k<<<(unsigned)blocks, (dp.cfg.nw + 2) * 32, dp.cfg.smem, st>>>(p);
   BFQ_CUDA_TRY(cudaGetLastError());
   return BFQ_OK;
 }
@@ -497,8 +551,8 @@ int plan_from_desc(const bfq_desc* desc, int device, bfq_plan** out) {
   size_t total = 0;
   if ((rc = upload(plan->hp.rblocks, &plan->R, total)) || (rc = upload(plan->hp.rows, &plan->rows, total)) ||
       (rc = upload(plan->hp.sstart, &plan->sstart, total)) ||
-      (rc = upload_program(plan->hp.sym, plan->sym, total)) ||
-      (rc = upload_program(plan->hp.full, plan->full, total))) {
+      (rc = upload_program(plan->hp.sym, plan->sym, total, smem_optin)) ||
+      (rc = upload_program(plan->hp.full, plan->full, total, smem_optin))) {
     bfq_plan_destroy(plan.release());
     return rc;
   }

@@ -32,12 +32,15 @@ struct alignas(16) Group {
   int32_t l1;
 };
 
-// One CTA's work inside a cell tile: a run of m1-units of one l1 group.
+// One CTA's work inside a cell tile: up to two "teams" of compute warps, each
+// walking the channel list of one l1 group in lockstep behind its own R ring.
+// Team t owns units [ubase[t], ubase[t] + nunits[t]) of group l1[t]; warps
+// 0..nunits[0]-1 form team 0, the next nunits[1] warps team 1.
 struct alignas(16) Item {
-  int32_t l1;
-  int32_t unit_base;
-  int32_t n_units;  // = active compute warps
-  int32_t pad;
+  int32_t l1[2];
+  int32_t ubase[2];
+  int32_t nunits[2];
+  int32_t pad[2];
 };
 
 // Kernel shape chosen at plan time for one program (folded or full).
@@ -47,7 +50,7 @@ struct KernelConfig {
   int cells = 0;   // cells per CTA tile
   int m1t = 0;     // output m1 values per warp unit (cells * m1t == 8 DMMA rows)
   int nw = 0;      // compute warps per CTA
-  int nstage = 0;  // R-block ring depth
+  int nstage = 0;  // R-block ring depth (per team; two teams per CTA)
   int nf = 1;      // f arrays staged per cell (2 for bilinear Q(f2,f3))
   int smem = 0;    // dynamic shared memory bytes
 };

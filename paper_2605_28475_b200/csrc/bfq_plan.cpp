@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <unordered_map>
 
@@ -44,65 +45,97 @@ static int conflict_free_stride(int n) {
   return s;
 }
 
+// Shared memory of one CTA: two R rings (one per team) | Phi per warp | f of the tile.
+static long smem_bytes(int nk, int qs, int k2s, int nf, int cells, int nw, int nstage) {
+  return 128 + 2L * nstage * nk * k2s * 8 + (long)nw * 8 * k2s * 8 + (long)nf * cells * nk * qs * 8;
+}
+
+// DMMA.8x8x4 issues with a ~15-cycle stall on its warp, so a scheduler needs
+// at least two compute warps to keep the FP64 tensor pipe fed while the other
+// warp issues gathers: prefer 8 compute warps, then fewer cells per tile.
 static bool choose_config(int nk, int qs, int k2s, int nf, int smem_limit, KernelConfig& c) {
   c.mt = (nk + 7) / 8;
   c.nf = nf;
-  static const int cells_opts[] = {8, 4, 2, 1};
-  static const int ws[][2] = {{4, 2}, {4, 1}, {2, 2}, {2, 1}, {1, 1}};
-  for (int cells : cells_opts) {
-    for (auto& w : ws) {
-      long smem = 128 + (long)w[1] * nk * k2s * 8 + (long)w[0] * 8 * k2s * 8 +
-                  (long)nf * cells * nk * qs * 8;
-      if (smem <= smem_limit) {
-        c.cells = cells;
-        c.m1t = 8 / cells;
-        c.nw = w[0];
-        c.nstage = w[1];
-        c.smem = (int)smem;
-        c.cg = c.mt == 1 ? std::min(cells, 8) : (c.mt == 2 ? std::min(cells, 2) : 1);
-        return true;
-      }
+  static const int opts[][3] = {  // cells, compute warps, ring stages
+      {4, 8, 2}, {4, 8, 1}, {2, 8, 2}, {2, 8, 1}, {8, 4, 2}, {4, 4, 2}, {4, 4, 1},
+      {2, 4, 2}, {2, 4, 1}, {1, 8, 1}, {1, 4, 1}, {1, 2, 1}, {1, 1, 1}};
+  int force_cells = 0;
+  if (const char* e = std::getenv("BFQ_CELLS")) force_cells = std::atoi(e);
+  for (auto& o : opts) {
+    if (force_cells && o[0] != force_cells) continue;
+    const long smem = smem_bytes(nk, qs, k2s, nf, o[0], o[1], o[2]);
+    if (smem > smem_limit) continue;
+    c.cells = o[0];
+    c.m1t = 8 / o[0];
+    c.nw = o[1];
+    c.nstage = o[2];
+    c.smem = (int)smem;
+    c.cg = std::min(c.cells, c.mt == 1 ? 8 : (c.mt == 2 ? 4 : 2));
+    if (const char* e = std::getenv("BFQ_CG")) {  // tuning override (benchmark sweeps only)
+      const int v = std::atoi(e);
+      if (v == 1 || v == 2 || v == 4 || v == 8) c.cg = std::min(c.cells, c.mt == 3 ? std::min(v, 4) : v);
     }
+    return true;
   }
   return false;
 }
 
-// Build the CTA schedule of one program: per l1 group, units of m1t output
-// columns, packed nw units per CTA; ordered heavy-first.
+// Build the CTA schedule of one program.  Units (m1t output columns x the
+// tile's cells) of all l1 groups are laid out group by group (descending l1,
+// whose per-unit work is nearly uniform) and packed nw at a time into CTAs;
+// a CTA spans at most two groups (two teams, two R rings).  Heavy CTAs first.
 static void build_items(const HostPlan& hp, Program& pg) {
   const KernelConfig& c = pg.cfg;
+  const double stage2 = (double)c.mt * 256.0 * (hp.k2p / 4);
+  auto unit_work = [&](const Group& gr, int u) {
+    double work = 0.0;
+    for (int e = 0; e < gr.n_chan; ++e) {
+      const ChanEntry& ce = pg.chans[gr.chan_off + e];
+      for (int ml = 0; ml < c.m1t; ++ml) {
+        const int m1 = u * c.m1t + ml;
+        if (m1 >= gr.d1) continue;
+        const int rows = hp.sstart[ce.slice_base + m1 + 1] - hp.sstart[ce.slice_base + m1];
+        work += (double)c.cells * c.mt * c.mt * 256.0 * ((rows + 3) / 4);
+      }
+      work += stage2;
+    }
+    return work;
+  };
   struct W {
     Item it;
     double work;
   };
   std::vector<W> all;
   double total = 0.0;
-  const double stage2 = (double)c.mt * 256.0 * (hp.k2p / 4);
-  for (const Group& gr : pg.groups) {
+  W cur{Item{{0, 0}, {0, 0}, {0, 0}, {0, 0}}, 0.0};
+  int nteams = 0, used = 0;
+  auto flush = [&]() {
+    if (used > 0) all.push_back(cur);
+    cur = W{Item{{0, 0}, {0, 0}, {0, 0}, {0, 0}}, 0.0};
+    nteams = 0;
+    used = 0;
+  };
+  for (int l1 = (int)pg.groups.size() - 1; l1 >= 0; --l1) {
+    const Group& gr = pg.groups[l1];
     if (gr.n_chan == 0) continue;
     const int units = (gr.d1 + c.m1t - 1) / c.m1t;
-    const int n_items = (units + c.nw - 1) / c.nw;
     int u = 0;
-    for (int i = 0; i < n_items; ++i) {
-      const int n = units / n_items + (i < units % n_items ? 1 : 0);
-      double work = 0.0;
-      for (int uu = u; uu < u + n; ++uu) {
-        for (int e = 0; e < gr.n_chan; ++e) {
-          const ChanEntry& ce = pg.chans[gr.chan_off + e];
-          for (int ml = 0; ml < c.m1t; ++ml) {
-            const int m1 = uu * c.m1t + ml;
-            if (m1 >= gr.d1) continue;
-            const int rows = hp.sstart[ce.slice_base + m1 + 1] - hp.sstart[ce.slice_base + m1];
-            work += (double)c.cells * c.mt * c.mt * 256.0 * ((rows + 3) / 4);
-          }
-          work += stage2;
-        }
-      }
-      all.push_back({Item{gr.l1, u, n, 0}, work});
-      total += work;
-      u += n;
+    while (u < units) {
+      if (used == c.nw || nteams == 2) flush();
+      const int take = std::min(units - u, c.nw - used);
+      double w = 0.0;
+      for (int uu = u; uu < u + take; ++uu) w += unit_work(gr, uu);
+      cur.it.l1[nteams] = l1;
+      cur.it.ubase[nteams] = u;
+      cur.it.nunits[nteams] = take;
+      cur.work = std::max(cur.work, w / take);  // CTA time ~ slowest warp
+      total += w;
+      ++nteams;
+      used += take;
+      u += take;
     }
   }
+  flush();
   std::stable_sort(all.begin(), all.end(), [](const W& a, const W& b) { return a.work > b.work; });
   pg.items.clear();
   for (auto& w : all) pg.items.push_back(w.it);

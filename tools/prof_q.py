@@ -1,0 +1,36 @@
+"""Minimal driver for ncu: a few Q(f,f) launches on one config (no CPU legs)."""
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from paper_2605_28475_b200 import engine, inputs  # noqa: E402
+from paper_2605_28475_b200.operator import load_cache  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--op", default="hs_n8")
+ap.add_argument("--cells", type=int, default=8192)
+ap.add_argument("--iters", type=int, default=4)
+ap.add_argument("--bilinear", action="store_true")
+a = ap.parse_args()
+op = load_cache(os.path.join(ROOT, "operators", a.op + ".bfct"))
+cells = inputs.perturbed_maxwellians(op.cfg.n_k, op.cfg.l_max, a.cells, seed=1)
+f = torch.from_numpy(cells).cuda()
+f3 = f.clone() if a.bilinear else None
+plan = engine.plan_for(op)
+print(plan.info)
+q = torch.empty_like(f)
+ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+for i in range(a.iters):
+    ev0.record()
+    engine.evaluate_batch(plan, f, f3, out=q)
+    ev1.record()
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    print(f"iter {i}: {ms:.3f} ms  {a.cells / ms * 1e3:.0f} cells/s  "
+          f"{plan.flops_per_cell * a.cells / ms / 1e9:.2f} alg TFLOP/s  "
+          f"{2 * plan.info['exec_macs_per_cell'] * a.cells / ms / 1e9:.2f} exec TFLOP/s")
