@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -47,9 +48,11 @@ struct DevProgram {
   bool bilinear = false;
   ChanEntry* chans = nullptr;
   Group* groups = nullptr;
+  int16_t* unit_m1 = nullptr;
   Item* items = nullptr;
   int n_items = 0;
   double exec_macs_per_cell = 0.0;
+  void (*kernel)(const struct KParams) = nullptr;
 };
 
 struct KParams {
@@ -63,6 +66,7 @@ struct KParams {
   const int* sstart;
   const ChanEntry* chans;
   const Group* groups;
+  const int16_t* unit_m1;
   const Item* items;
   int nk, nq, qs, k2s, k2p;
   int cells, m1t, nw, nstage;
@@ -117,16 +121,33 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned by
                : "memory");
 }
 
+// try_wait with a suspend-time hint: the waiting warp sleeps in hardware
+// until the phase flips (or the hint expires) instead of spinning on issue slots.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
   asm volatile(
       "{\n"
       " .reg .pred p;\n"
       "WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n"
       " @!p bra WAIT_%=;\n"
       "}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+}
+
+// Non-blocking probe of an mbarrier phase.
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, unsigned parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      " mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
 }
 
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
@@ -155,220 +176,61 @@ __device__ __forceinline__ Row fetch_row(const Row* rows, int z, int ze) {
   return r;
 }
 
-// ------------------------------------------------------------ the Q kernel
-// Block = nw compute warps + 2 producer warps (one per team).
-template <int MT, int CG, bool BILIN>
-__global__ void __launch_bounds__(320, 1) bfq_q_kernel(const KParams p) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int r0 = lane >> 2, kq = lane & 3;
-  const int NK = p.nk, QS = p.qs, K2S = p.k2s, CELLS = p.cells, NST = p.nstage;
-
-  const long long item_idx = (long long)blockIdx.x / p.n_tiles;
-  const long long tile = (long long)blockIdx.x - item_idx * p.n_tiles;
-  const Item item = p.items[item_idx];
-
-  // shared layout: barriers | R rings (team, stage) | Phi (per warp, 8 pairs) | f (cells)
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);  // [team*4 + stage]
-  uint64_t* empty = full + 8;
-  double* rs = reinterpret_cast<double*>(smem_raw + 128);
-  const size_t rblk = (size_t)NK * K2S;
-  double* phis = rs + 2 * (size_t)NST * rblk;
-  double* fs = phis + (size_t)p.nw * 8 * K2S;
-  const int cell_elems = NK * QS;
-  const int nf = BILIN ? 2 : 1;
-
-  if (threadIdx.x == 0) {
-    for (int t = 0; t < 2; ++t)
-      for (int s = 0; s < NST; ++s) {
-        mbar_init(&full[t * 4 + s], 1);
-        mbar_init(&empty[t * 4 + s], (unsigned)max(item.nunits[t], 1));
-      }
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  // Phi padding columns (n_k^2 .. k2p) are read by stage 2 and must be 0.
-  for (int i = threadIdx.x; i < p.nw * 8 * K2S; i += blockDim.x) phis[i] = 0.0;
-  // stage the tile's cells: global (cell, k, q) -> shared (cell, k, q padded to QS);
-  // one warp per (array, cell, k) row, lanes over q
-  {
-    const int rows_total = nf * CELLS * NK;
-    const int nwarps = blockDim.x >> 5;
-    for (int row = warp; row < rows_total; row += nwarps) {
-      const int arr = row / (CELLS * NK);
-      const int rem = row - arr * CELLS * NK;
-      const int c = rem / NK, k = rem - c * NK;
-      const long long cell = tile * CELLS + c;
-      const double* src = (arr == 0 ? p.f2 : p.f3) + (cell < p.n_cells ? cell : 0) * (long long)NK * p.nq +
-                          (long long)k * p.nq;
-      double* dst = fs + (size_t)(arr * CELLS + c) * cell_elems + (size_t)k * QS;
-      const bool ok = cell < p.n_cells;
-      for (int q = lane; q < p.nq; q += 32) dst[q] = ok ? __ldg(src + q) : 0.0;
-    }
-  }
-  __syncthreads();
-
-  const unsigned rbytes = (unsigned)(rblk * sizeof(double));
-  if (warp >= p.nw) {
-    // ---------------- producers: producer warp t streams team t's R_tau blocks
-    const int t = warp - p.nw;
-    if (lane == 0 && item.nunits[t] > 0) {
-      const Group grp = p.groups[item.l1[t]];
-      double* ring = rs + (size_t)t * NST * rblk;
-      for (int i = 0; i < grp.n_chan; ++i) {
-        const int s = i % NST;
-        if (i >= NST) mbar_wait(&empty[t * 4 + s], (unsigned)((i / NST) - 1) & 1u);
-        const ChanEntry ce = p.chans[grp.chan_off + i];
-        mbar_arrive_expect_tx(&full[t * 4 + s], rbytes);
-        bulk_g2s(ring + (size_t)s * rblk, p.R + (size_t)ce.tau * rblk, rbytes, &full[t * 4 + s]);
-      }
-    }
-    return;
-  }
-  const int team = warp < item.nunits[0] ? 0 : 1;
-  const int twarp = team == 0 ? warp : warp - item.nunits[0];
-  if (team == 1 && twarp >= item.nunits[1]) return;
-
-  // ---------------- compute warp
-  const Group grp = p.groups[item.l1[team]];
-  const int unit = item.ubase[team] + twarp;
-  uint64_t* tfull = full + team * 4;
-  uint64_t* tempty = empty + team * 4;
-  const uint32_t ring_u32 = smem_u32(rs + (size_t)team * NST * rblk);
-  const uint32_t phw_u32 = smem_u32(phis + (size_t)warp * 8 * K2S);
-  const uint32_t fs_u32 = smem_u32(fs);
-  const uint32_t cell_bytes = (uint32_t)cell_elems * 8u;
-  // Operand rows beyond n_k (DMMA padding) read a clamped valid row: their
-  // products only reach accumulator entries (a or b >= n_k, k1 >= n_k) that
-  // are never stored, so no zero padding or predication is needed.
-  uint32_t frow[MT], rrow[MT];
-#pragma unroll
-  for (int i = 0; i < MT; ++i) {
-    const int r = min(r0 + 8 * i, NK - 1);
-    frow[i] = (uint32_t)(r * QS) * 8u;
-    rrow[i] = (uint32_t)(r * K2S + kq) * 8u;
-  }
-  double acc2[MT][2];
-#pragma unroll
-  for (int j = 0; j < MT; ++j) acc2[j][0] = acc2[j][1] = 0.0;
-
-  for (int i = 0; i < grp.n_chan; ++i) {
-    const ChanEntry ce = p.chans[grp.chan_off + i];
-    const double wgt = ce.weight2 ? 2.0 : 1.0;
-    // ---- stage 1: Phi for this warp's 8 (m1, cell) pairs
-    for (int ml = 0; ml < p.m1t; ++ml) {
-      const int m1 = unit * p.m1t + ml;
-      int zs = 0, ze = 0;
-      if (m1 < grp.d1) {
-        zs = __ldg(p.sstart + ce.slice_base + m1);
-        ze = __ldg(p.sstart + ce.slice_base + m1 + 1);
-      }
-      for (int cg = 0; cg < CELLS; cg += CG) {
-        double acc[CG][MT][MT][2];
-#pragma unroll
-        for (int cc = 0; cc < CG; ++cc)
-#pragma unroll
-          for (int a = 0; a < MT; ++a)
-#pragma unroll
-            for (int b = 0; b < MT; ++b) acc[cc][a][b][0] = acc[cc][a][b][1] = 0.0;
-        const uint32_t fa0 = fs_u32 + (uint32_t)cg * cell_bytes;
-        const uint32_t fb0 = fs_u32 + (uint32_t)((BILIN ? CELLS : 0) + cg) * cell_bytes;
-        // software-pipelined over k-steps: the CG-table row of step s+1 is in
-        // flight while step s issues its gathers and DMMAs
-        Row nxt = fetch_row(p.rows, zs + kq, ze);
-        for (int z0 = zs; z0 < ze; z0 += 4) {
-          const Row rw = nxt;
-          nxt = fetch_row(p.rows, z0 + 4 + kq, ze);
-          const uint32_t qa = fa0 + (uint32_t)rw.q2 * 8u, qb = fb0 + (uint32_t)rw.q3 * 8u;
-#pragma unroll
-          for (int cc = 0; cc < CG; ++cc) {
-            double av[MT], bv[MT];
-#pragma unroll
-            for (int t = 0; t < MT; ++t) {
-              av[t] = rw.g * lds_ro(qa + cc * cell_bytes + frow[t]);
-              bv[t] = lds_ro(qb + cc * cell_bytes + frow[t]);
-            }
-#pragma unroll
-            for (int a = 0; a < MT; ++a)
-#pragma unroll
-              for (int b = 0; b < MT; ++b) dmma884(acc[cc][a][b][0], acc[cc][a][b][1], av[a], bv[b]);
-          }
-        }
-        // accumulator (a = 8A + r0, b = 8B + 2kq + e) -> Phi row of the pair
-#pragma unroll
-        for (int cc = 0; cc < CG; ++cc) {
-          const uint32_t ph = phw_u32 + (uint32_t)((ml * CELLS + cg + cc) * K2S) * 8u;
-#pragma unroll
-          for (int a = 0; a < MT; ++a)
-#pragma unroll
-            for (int b = 0; b < MT; ++b)
-#pragma unroll
-              for (int e = 0; e < 2; ++e) {
-                const int ia = 8 * a + r0, ib = 8 * b + 2 * kq + e;
-                if (ia < NK && ib < NK) sts_v(ph + (uint32_t)(ia * NK + ib) * 8u, wgt * acc[cc][a][b][e]);
-              }
-        }
-      }
-    }
-    __syncwarp();
-    // ---- stage 2: out[pair, k1] += Phi[pair, :] . R_tau[k1, :]
-    const int s = i % NST;
-    mbar_wait(&tfull[s], (unsigned)(i / NST) & 1u);
-    const uint32_t rb = ring_u32 + (uint32_t)(s * rblk) * 8u;
-    const uint32_t pa = phw_u32 + (uint32_t)(r0 * K2S + kq) * 8u;
-#pragma unroll 4
-    for (int k0 = 0; k0 < p.k2p; k0 += 4) {
-      const double av = lds_v(pa + k0 * 8);
-      double bv[MT];
-#pragma unroll
-      for (int j = 0; j < MT; ++j) bv[j] = lds_v(rb + rrow[j] + k0 * 8);
-#pragma unroll
-      for (int j = 0; j < MT; ++j) dmma884(acc2[j][0], acc2[j][1], av, bv[j]);
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&tempty[s]);
-  }
-
-  // ---------------- epilogue: pair r0 = (m1 = unit*m1t + r0/CELLS, cell = r0%CELLS)
-  const int ml = r0 / CELLS, c = r0 - ml * CELLS;
-  const int m1 = unit * p.m1t + ml;
-  const long long cell = tile * CELLS + c;
-  if (m1 < grp.d1 && cell < p.n_cells) {
-    const int l1 = grp.l1, q1 = l1 * l1 + m1;
-    double* qc = p.q + cell * (long long)NK * p.nq + q1;
-#pragma unroll
-    for (int j = 0; j < MT; ++j)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int k1 = 8 * j + 2 * kq + e;
-        if (k1 < NK) {
-          double v = acc2[j][e];
-          if (p.conservation && ((k1 == 0 && l1 <= 1) || (k1 == 1 && l1 == 0))) v = 0.0;
-          qc[(size_t)k1 * p.nq] = v;
-        }
-      }
-  }
+__device__ __forceinline__ Row fetch_row_clamped(const Row* rows, int z, int ze) {
+  Row r = load_row(rows, min(z, ze - 1));
+  if (z >= ze) r.g = 0.0;  // padding lane of the last k-step: contributes 0
+  return r;
 }
+
+// ------------------------------------------------------------ the Q kernel
+#include "bfq_qkernel.cuh"
 
 typedef void (*QKernel)(const KParams);
 
+// Compile-time-size instantiations for the BASELINE configurations (all
+// gathers then use immediate offsets); anything else runs the generic kernel.
+template <bool BILIN, int NK, int QS>
+QKernel pick_fixed(int mt, int cells) {
+  constexpr int MT = (NK + 7) / 8;
+  if (mt != MT) return nullptr;
+  if constexpr (MT == 1) {
+    if (cells == 8) return bfq_q_kernel<1, 8, BILIN, NK, QS>;
+    if (cells == 4) return bfq_q_kernel<1, 4, BILIN, NK, QS>;
+  } else if constexpr (MT == 2) {
+    if (cells == 4) return bfq_q_kernel<2, 4, BILIN, NK, QS>;
+    if (cells == 2) return bfq_q_kernel<2, 2, BILIN, NK, QS>;
+  } else {
+    if (cells == 2) return bfq_q_kernel<MT, 2, BILIN, NK, QS>;
+    if (cells == 1) return bfq_q_kernel<MT, 1, BILIN, NK, QS>;
+  }
+  return nullptr;
+}
+
 template <bool BILIN>
-QKernel pick_kernel(int mt, int cg) {
+QKernel pick_kernel(int mt, int cells, int nk, int qs) {
+  QKernel k = nullptr;
+  if (!std::getenv("BFQ_GENERIC")) {
+    if (nk == 13 && qs == 172) k = pick_fixed<BILIN, 13, 172>(mt, cells);
+    else if (nk == 9 && qs == 84) k = pick_fixed<BILIN, 9, 84>(mt, cells);
+    else if (nk == 11 && qs == 124) k = pick_fixed<BILIN, 11, 124>(mt, cells);
+    else if (nk == 5 && qs == 28) k = pick_fixed<BILIN, 5, 28>(mt, cells);
+    else if (nk == 17 && qs == 292) k = pick_fixed<BILIN, 17, 292>(mt, cells);
+    if (k) return k;
+  }
   if (mt == 1) {
-    if (cg == 8) return bfq_q_kernel<1, 8, BILIN>;
-    if (cg == 4) return bfq_q_kernel<1, 4, BILIN>;
-    if (cg == 2) return bfq_q_kernel<1, 2, BILIN>;
-    return bfq_q_kernel<1, 1, BILIN>;
+    if (cells == 8) return bfq_q_kernel<1, 8, BILIN, 0, 0>;
+    if (cells == 4) return bfq_q_kernel<1, 4, BILIN, 0, 0>;
+    if (cells == 2) return bfq_q_kernel<1, 2, BILIN, 0, 0>;
+    if (cells == 1) return bfq_q_kernel<1, 1, BILIN, 0, 0>;
   }
   if (mt == 2) {
-    if (cg == 8) return bfq_q_kernel<2, 8, BILIN>;
-    if (cg == 4) return bfq_q_kernel<2, 4, BILIN>;
-    if (cg == 2) return bfq_q_kernel<2, 2, BILIN>;
-    return bfq_q_kernel<2, 1, BILIN>;
+    if (cells == 4) return bfq_q_kernel<2, 4, BILIN, 0, 0>;
+    if (cells == 2) return bfq_q_kernel<2, 2, BILIN, 0, 0>;
+    if (cells == 1) return bfq_q_kernel<2, 1, BILIN, 0, 0>;
   }
   if (mt == 3) {
-    if (cg == 4) return bfq_q_kernel<3, 4, BILIN>;
-    if (cg == 2) return bfq_q_kernel<3, 2, BILIN>;
-    return bfq_q_kernel<3, 1, BILIN>;
+    if (cells == 2) return bfq_q_kernel<3, 2, BILIN, 0, 0>;
+    if (cells == 1) return bfq_q_kernel<3, 1, BILIN, 0, 0>;
   }
   return nullptr;
 }
@@ -446,7 +308,7 @@ int upload(const std::vector<T>& v, T** out, size_t& total) {
   return BFQ_OK;
 }
 
-int upload_program(const Program& pg, DevProgram& dp, size_t& total, int smem_optin) {
+int upload_program(const Program& pg, DevProgram& dp, size_t& total, int smem_optin, int nk, int qs) {
   dp.cfg = pg.cfg;
   dp.bilinear = pg.bilinear;
   dp.n_items = (int)pg.items.size();
@@ -454,12 +316,14 @@ int upload_program(const Program& pg, DevProgram& dp, size_t& total, int smem_op
   int rc;
   if ((rc = upload(pg.chans, &dp.chans, total))) return rc;
   if ((rc = upload(pg.groups, &dp.groups, total))) return rc;
+  if ((rc = upload(pg.unit_m1, &dp.unit_m1, total))) return rc;
   if ((rc = upload(pg.items, &dp.items, total))) return rc;
-  QKernel k = pg.bilinear ? pick_kernel<true>(pg.cfg.mt, pg.cfg.cg) : pick_kernel<false>(pg.cfg.mt, pg.cfg.cg);
+  QKernel k = pg.bilinear ? pick_kernel<true>(pg.cfg.mt, pg.cfg.cells, nk, qs) : pick_kernel<false>(pg.cfg.mt, pg.cfg.cells, nk, qs);
   if (!k) {
     set_error("no kernel instantiation for this tiling");
     return BFQ_EINVAL;
   }
+  dp.kernel = k;
   // Kernel attributes are global per instantiation: always allow the device
   // maximum so plans of different sizes sharing a kernel never shrink it.
   BFQ_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin));
@@ -469,6 +333,8 @@ int upload_program(const Program& pg, DevProgram& dp, size_t& total, int smem_op
 void free_program(DevProgram& dp) {
   cudaFree(dp.chans);
   cudaFree(dp.groups);
+  cudaFree(dp.unit_m1);
+  dp.unit_m1 = nullptr;
   cudaFree(dp.items);
   dp.chans = nullptr;
   dp.groups = nullptr;
@@ -490,6 +356,7 @@ int launch_q(const bfq_plan* plan, const DevProgram& dp, const double* f2, const
   p.sstart = plan->sstart;
   p.chans = dp.chans;
   p.groups = dp.groups;
+  p.unit_m1 = dp.unit_m1;
   p.items = dp.items;
   p.nk = hp.n_k;
   p.nq = hp.n_q;
@@ -506,8 +373,8 @@ int launch_q(const bfq_plan* plan, const DevProgram& dp, const double* f2, const
     set_error("too many cells for one launch");
     return BFQ_EINVAL;
   }
-  QKernel k = dp.bilinear ? pick_kernel<true>(dp.cfg.mt, dp.cfg.cg) : pick_kernel<false>(dp.cfg.mt, dp.cfg.cg);
-  k<<<(unsigned)blocks, (dp.cfg.nw + 2) * 32, dp.cfg.smem, st>>>(p);
+  QKernel k = dp.kernel;
+  k<<<(unsigned)blocks, (dp.cfg.nw + 1) * 32, dp.cfg.smem, st>>>(p);
   BFQ_CUDA_TRY(cudaGetLastError());
   return BFQ_OK;
 }
@@ -551,8 +418,8 @@ int plan_from_desc(const bfq_desc* desc, int device, bfq_plan** out) {
   size_t total = 0;
   if ((rc = upload(plan->hp.rblocks, &plan->R, total)) || (rc = upload(plan->hp.rows, &plan->rows, total)) ||
       (rc = upload(plan->hp.sstart, &plan->sstart, total)) ||
-      (rc = upload_program(plan->hp.sym, plan->sym, total, smem_optin)) ||
-      (rc = upload_program(plan->hp.full, plan->full, total, smem_optin))) {
+      (rc = upload_program(plan->hp.sym, plan->sym, total, smem_optin, plan->hp.n_k, plan->hp.qs)) ||
+      (rc = upload_program(plan->hp.full, plan->full, total, smem_optin, plan->hp.n_k, plan->hp.qs))) {
     bfq_plan_destroy(plan.release());
     return rc;
   }

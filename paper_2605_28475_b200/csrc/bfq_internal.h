@@ -9,6 +9,22 @@
 
 namespace bfq {
 
+#ifdef __CUDACC__
+#define BFQ_HD __host__ __device__
+#else
+#define BFQ_HD
+#endif
+
+// Stride rule for fp64 fragment gathers: lanes 0-15 of a DMMA operand load
+// touch rows r0 in 0..3 at columns c in 0..3 (row*stride + c).  With
+// stride = +-4 (mod 16) doubles those 16 addresses fall in 16 distinct
+// 8-byte bank pairs, i.e. one wavefront per 16 lanes.
+BFQ_HD constexpr int conflict_free_stride_dev(int n) {
+  int s = (n + 3) / 4 * 4;
+  while (s % 16 != 4 && s % 16 != 12) s += 4;
+  return s;
+}
+
 // One COO row as the kernel reads it: 16 bytes, one LDG.128 per row.
 struct alignas(16) Row {
   int32_t q2;
@@ -30,6 +46,9 @@ struct alignas(16) Group {
   int32_t n_chan;
   int32_t d1;        // 2*l1 + 1
   int32_t l1;
+  int32_t unit_off;  // first entry of this group's units in Program::unit_m1 (x m1t)
+  int32_t n_units;
+  int32_t pad[2];
 };
 
 // One CTA's work inside a cell tile: up to two "teams" of compute warps, each
@@ -61,6 +80,7 @@ struct Program {
   KernelConfig cfg;
   std::vector<ChanEntry> chans;
   std::vector<Group> groups;  // indexed by l1
+  std::vector<int16_t> unit_m1;  // [unit][m1t] output column m1 of each DMMA row group, -1 = none
   std::vector<Item> items;    // heavy first
   double exec_macs_per_cell = 0.0;
 };

@@ -35,15 +35,7 @@ static inline int isqrt_floor(int x) {
   return r;
 }
 
-// Stride rule for fp64 fragment gathers: lanes 0-15 of a DMMA operand load
-// touch rows r0 in 0..3 at columns c in 0..3 (row*stride + c).  With
-// stride = +-4 (mod 16) doubles those 16 addresses fall in 16 distinct
-// 8-byte bank pairs, i.e. one wavefront per 16 lanes.
-static int conflict_free_stride(int n) {
-  int s = (n + 3) / 4 * 4;
-  while (s % 16 != 4 && s % 16 != 12) s += 4;
-  return s;
-}
+static int conflict_free_stride(int n) { return conflict_free_stride_dev(n); }
 
 // Shared memory of one CTA: two R rings (one per team) | Phi per warp | f of the tile.
 static long smem_bytes(int nk, int qs, int k2s, int nf, int cells, int nw, int nstage) {
@@ -57,12 +49,14 @@ static bool choose_config(int nk, int qs, int k2s, int nf, int smem_limit, Kerne
   c.mt = (nk + 7) / 8;
   c.nf = nf;
   static const int opts[][3] = {  // cells, compute warps, ring stages
-      {4, 8, 2}, {4, 8, 1}, {2, 8, 2}, {2, 8, 1}, {8, 4, 2}, {4, 4, 2}, {4, 4, 1},
+      {8, 8, 2}, {4, 8, 2}, {4, 8, 1}, {2, 8, 2}, {2, 8, 1}, {8, 4, 2}, {4, 4, 2}, {4, 4, 1},
       {2, 4, 2}, {2, 4, 1}, {1, 8, 1}, {1, 4, 1}, {1, 2, 1}, {1, 1, 1}};
   int force_cells = 0;
   if (const char* e = std::getenv("BFQ_CELLS")) force_cells = std::atoi(e);
+  const int max_cells = c.mt == 1 ? 8 : (c.mt == 2 ? 4 : 2);  // stage-1 accumulators in registers
   for (auto& o : opts) {
     if (force_cells && o[0] != force_cells) continue;
+    if (o[0] > max_cells) continue;
     const long smem = smem_bytes(nk, qs, k2s, nf, o[0], o[1], o[2]);
     if (smem > smem_limit) continue;
     c.cells = o[0];
@@ -70,11 +64,7 @@ static bool choose_config(int nk, int qs, int k2s, int nf, int smem_limit, Kerne
     c.nw = o[1];
     c.nstage = o[2];
     c.smem = (int)smem;
-    c.cg = std::min(c.cells, c.mt == 1 ? 8 : (c.mt == 2 ? 4 : 2));
-    if (const char* e = std::getenv("BFQ_CG")) {  // tuning override (benchmark sweeps only)
-      const int v = std::atoi(e);
-      if (v == 1 || v == 2 || v == 4 || v == 8) c.cg = std::min(c.cells, c.mt == 3 ? std::min(v, 4) : v);
-    }
+    c.cg = c.cells;
     return true;
   }
   return false;
@@ -85,15 +75,50 @@ static bool choose_config(int nk, int qs, int k2s, int nf, int smem_limit, Kerne
 // whose per-unit work is nearly uniform) and packed nw at a time into CTAs;
 // a CTA spans at most two groups (two teams, two R rings).  Heavy CTAs first.
 static void build_items(const HostPlan& hp, Program& pg) {
+  // (groups are modified: unit_off / n_units)
   const KernelConfig& c = pg.cfg;
   const double stage2 = (double)c.mt * 256.0 * (hp.k2p / 4);
+  // Stage-1 k-steps of output column m1 summed over the group's channels.
+  auto m1_steps = [&](const Group& gr, int m1) {
+    double st = 0.0;
+    for (int e = 0; e < gr.n_chan; ++e) {
+      const ChanEntry& ce = pg.chans[gr.chan_off + e];
+      st += (hp.sstart[ce.slice_base + m1 + 1] - hp.sstart[ce.slice_base + m1] + 3) / 4;
+    }
+    return st;
+  };
+  // Balanced units: the d1 columns are dealt to ceil(d1/m1t) units of m1t
+  // slots, heaviest column first into the lightest unit with a free slot
+  // (rows per column vary ~2x with |m1|; consecutive columns would leave the
+  // warps of a CTA ~20% imbalanced).
+  pg.unit_m1.clear();
+  for (Group& gr : pg.groups) {
+    const int units = gr.n_chan ? (gr.d1 + c.m1t - 1) / c.m1t : 0;
+    gr.unit_off = (int)(pg.unit_m1.size() / c.m1t);
+    gr.n_units = units;
+    if (!units) continue;
+    std::vector<std::pair<double, int>> cols;
+    for (int m1 = 0; m1 < gr.d1; ++m1) cols.push_back({m1_steps(gr, m1), m1});
+    std::stable_sort(cols.begin(), cols.end(), [](auto& x, auto& y) { return x.first > y.first; });
+    std::vector<double> load(units, 0.0);
+    std::vector<int> fill(units, 0);
+    std::vector<int16_t> slots((size_t)units * c.m1t, (int16_t)-1);
+    for (auto& col : cols) {
+      int best = -1;
+      for (int u = 0; u < units; ++u)
+        if (fill[u] < c.m1t && (best < 0 || load[u] < load[best])) best = u;
+      slots[(size_t)best * c.m1t + fill[best]++] = (int16_t)col.second;
+      load[best] += col.first;
+    }
+    pg.unit_m1.insert(pg.unit_m1.end(), slots.begin(), slots.end());
+  }
   auto unit_work = [&](const Group& gr, int u) {
     double work = 0.0;
     for (int e = 0; e < gr.n_chan; ++e) {
       const ChanEntry& ce = pg.chans[gr.chan_off + e];
       for (int ml = 0; ml < c.m1t; ++ml) {
-        const int m1 = u * c.m1t + ml;
-        if (m1 >= gr.d1) continue;
+        const int m1 = pg.unit_m1[(size_t)(gr.unit_off + u) * c.m1t + ml];
+        if (m1 < 0) continue;
         const int rows = hp.sstart[ce.slice_base + m1 + 1] - hp.sstart[ce.slice_base + m1];
         work += (double)c.cells * c.mt * c.mt * 256.0 * ((rows + 3) / 4);
       }
@@ -118,7 +143,7 @@ static void build_items(const HostPlan& hp, Program& pg) {
   for (int l1 = (int)pg.groups.size() - 1; l1 >= 0; --l1) {
     const Group& gr = pg.groups[l1];
     if (gr.n_chan == 0) continue;
-    const int units = (gr.d1 + c.m1t - 1) / c.m1t;
+    const int units = gr.n_units;
     int u = 0;
     while (u < units) {
       if (used == c.nw || nteams == 2) flush();
@@ -140,6 +165,62 @@ static void build_items(const HostPlan& hp, Program& pg) {
   pg.items.clear();
   for (auto& w : all) pg.items.push_back(w.it);
   pg.exec_macs_per_cell = total / c.cells;
+}
+
+// Shared-memory wavefronts of one stage-1 gather instruction for a group of
+// up to 4 table rows (lane kq reads row kq; lanes r0 = 0..3 of a half-warp read
+// operand row r0 at word r0*qs + q).  Distinct words on the same 8-byte bank
+// pair serialise; equal words broadcast.
+static int group_wavefronts(const int* q, int n, int qs) {
+  int words[16], nw = 0;
+  for (int r0 = 0; r0 < 4; ++r0)
+    for (int j = 0; j < 4; ++j) {
+      const int w = r0 * qs + (j < n ? q[j] : 0);
+      bool dup = false;
+      for (int t = 0; t < nw; ++t) dup |= words[t] == w;
+      if (!dup) words[nw++] = w;
+    }
+  int per_bank[16] = {0}, worst = 0;
+  for (int t = 0; t < nw; ++t) worst = std::max(worst, ++per_bank[words[t] & 15]);
+  return worst;
+}
+
+// Reorder the rows inside every (tau, q1) slice so that each k-step's four
+// rows gather conflict-free (greedy, per slice).  Only the summation order
+// inside a slice changes.
+static void reorder_rows_for_banks(HostPlan& hp, const int64_t* slice_starts, int64_t n_s) {
+  std::vector<Row> tmp;
+  for (int64_t s = 0; s < n_s; ++s) {
+    const int64_t a = slice_starts[s], b = slice_starts[s + 1];
+    const int n = (int)(b - a);
+    if (n <= 1) continue;
+    tmp.assign(hp.rows.begin() + a, hp.rows.begin() + b);
+    std::vector<char> used(n, 0);
+    int64_t out = a;
+    for (int g0 = 0; g0 < n; g0 += 4) {
+      int q2[4], q3[4], m = 0;
+      const int gsz = std::min(4, n - g0);
+      for (int j = 0; j < gsz; ++j) {
+        int best = -1, best_cost = 1 << 30;
+        for (int r = 0; r < n; ++r) {
+          if (used[r]) continue;
+          q2[m] = tmp[r].q2;
+          q3[m] = tmp[r].q3;
+          // cost of the group if completed with this row (missing lanes read q = 0)
+          const int cost = group_wavefronts(q2, m + 1, hp.qs) + group_wavefronts(q3, m + 1, hp.qs);
+          if (cost < best_cost) {
+            best_cost = cost;
+            best = r;
+          }
+        }
+        used[best] = 1;
+        q2[m] = tmp[best].q2;
+        q3[m] = tmp[best].q3;
+        ++m;
+        hp.rows[out++] = tmp[best];
+      }
+    }
+  }
 }
 
 int build_host_plan(const bfq_desc& d, int smem_limit, HostPlan& hp) {
@@ -204,6 +285,8 @@ int build_host_plan(const bfq_desc& d, int smem_limit, HostPlan& hp) {
     if (s > 0 && d.slice_tau[s] == d.slice_tau[s - 1] && d.slice_q1[s] == d.slice_q1[s - 1])
       return fail(BFQ_EINVAL, "duplicate (tau, q1) slice");
   }
+
+  if (!std::getenv("BFQ_NO_ROW_REORDER")) reorder_rows_for_banks(hp, d.slice_starts, d.n_s);
 
   // expanded slice table: every (tau, m1) gets a (possibly empty) row range
   hp.chan_sbase.resize(d.n_t);
@@ -274,7 +357,7 @@ int build_host_plan(const bfq_desc& d, int smem_limit, HostPlan& hp) {
   auto make_program = [&](Program& pg, bool bilinear, bool use_fold) -> bool {
     pg.bilinear = bilinear;
     pg.chans.clear();
-    pg.groups.assign(L + 1, Group{0, 0, 0, 0});
+    pg.groups.assign(L + 1, Group{0, 0, 0, 0, 0, 0, {0, 0}});
     for (int l1 = 0; l1 <= L; ++l1) {
       pg.groups[l1].chan_off = (int)pg.chans.size();
       pg.groups[l1].d1 = 2 * l1 + 1;

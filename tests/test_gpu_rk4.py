@@ -1,0 +1,75 @@
+"""GPU-resident RK4 (config 5 driver) against an oracle RK4 on the CPU.
+
+Reference semantics: harness.rk4_integrate (harness.py:79-120), invariants
+exactly conserved (moment_drift() == 0.0, test_harness.py:22-26), divergence
+raises RuntimeError (harness.py:103-107).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import load_op
+from oracle import q_oracle
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_2605_28475_b200 import harness, inputs  # noqa: E402
+from paper_2605_28475_b200.operator import CoefficientField  # noqa: E402
+
+
+def oracle_rk4(op, y, dt, n):
+    oop = q_oracle.OracleOperator.from_operator(op)
+    rhs = lambda v: q_oracle.q_angular_first(oop, v)  # noqa: E731
+    for _ in range(n):
+        k1 = rhs(y)
+        k2 = rhs(y + 0.5 * dt * k1)
+        k3 = rhs(y + 0.5 * dt * k2)
+        k4 = rhs(y + dt * k3)
+        y = y + (dt / 6.0) * (k1 + 2.0 * k2 + 2.0 * k3 + k4)
+    return y
+
+
+@pytest.mark.parametrize("name,n_steps", [("mm_n4", 20), ("mm_k4l6", 10)])
+def test_rk4_matches_oracle_and_conserves(name, n_steps):
+    op = load_op(name)
+    cfg = op.cfg
+    c0 = inputs.bimodal(cfg.n_k, cfg.l_max, 6, seed=5)
+    tr = harness.rk4_integrate_batch(op, c0, 0.01, n_steps, record_every=5, watch=[0, 5])
+    assert tr.moment_drift() == 0.0
+    for j, cell in enumerate([0, 5]):
+        ref = oracle_rk4(op, c0[cell], 0.01, n_steps)
+        assert q_oracle.rel_err(tr.snapshots[-1, j], ref) <= 1e-12
+    fin = tr.final.cpu().numpy()
+    assert np.array_equal(fin[[0, 5]], tr.snapshots[-1])
+
+
+def test_rk4_single_cell_dropin():
+    op = load_op("mm_n4")
+    c = CoefficientField(inputs.bimodal(op.cfg.n_k, op.cfg.l_max, 1, seed=2)[0], op.cfg)
+    tr = harness.rk4_integrate(op, c, 0.01, 6, record_every=2)
+    assert tr.coeffs.shape == (4, op.cfg.n_k, op.cfg.n_q) and np.allclose(tr.times, [0, 0.02, 0.04, 0.06])
+    assert tr.moment_drift() == 0.0
+    assert q_oracle.rel_err(tr.coeffs[-1], oracle_rk4(op, c.values, 0.01, 6)) <= 1e-12
+    with pytest.raises(ValueError):
+        harness.rk4_integrate(op, c, -1.0, 3)
+
+
+def test_rk4_divergence_raises():
+    op = load_op("hs_n4")
+    c0 = inputs.perturbed_maxwellians(op.cfg.n_k, op.cfg.l_max, 4, seed=1)
+    c0[2] *= 1e150
+    with pytest.raises(RuntimeError, match="diverged"):
+        harness.rk4_integrate_batch(op, c0, 1.0, 3)
+
+
+def test_rk4_config5_operator():
+    """Config 5 (Maxwell N=L=10, bimodal): a short GPU trajectory vs the oracle."""
+    op = load_op("mm_n10")
+    cfg = op.cfg
+    c0 = inputs.bimodal(cfg.n_k, cfg.l_max, 64, seed=7)
+    tr = harness.rk4_integrate_batch(op, c0, 0.01, 3, record_every=3, watch=[17])
+    assert tr.moment_drift() == 0.0
+    assert q_oracle.rel_err(tr.snapshots[-1, 0], oracle_rk4(op, c0[17], 0.01, 3)) <= 1e-12
