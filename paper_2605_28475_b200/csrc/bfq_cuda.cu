@@ -71,6 +71,7 @@ struct KParams {
   int nk, nq, qs, k2s, k2p;
   int cells, m1t, nw, nstage;
   int conservation;
+  int debug;  // timing experiments only (BFQ_DEBUG): bit0 skip stage 1, bit1 skip stage 2
 };
 
 // ------------------------------------------------------------ PTX helpers
@@ -189,50 +190,58 @@ typedef void (*QKernel)(const KParams);
 
 // Compile-time-size instantiations for the BASELINE configurations (all
 // gathers then use immediate offsets); anything else runs the generic kernel.
-template <bool BILIN, int NK, int QS>
+template <bool BILIN, bool PIPE, int NK, int QS>
 QKernel pick_fixed(int mt, int cells) {
   constexpr int MT = (NK + 7) / 8;
   if (mt != MT) return nullptr;
   if constexpr (MT == 1) {
-    if (cells == 8) return bfq_q_kernel<1, 8, BILIN, NK, QS>;
-    if (cells == 4) return bfq_q_kernel<1, 4, BILIN, NK, QS>;
+    if (cells == 8) return bfq_q_kernel<1, 8, BILIN, NK, QS, PIPE>;
+    if (cells == 4) return bfq_q_kernel<1, 4, BILIN, NK, QS, PIPE>;
   } else if constexpr (MT == 2) {
-    if (cells == 4) return bfq_q_kernel<2, 4, BILIN, NK, QS>;
-    if (cells == 2) return bfq_q_kernel<2, 2, BILIN, NK, QS>;
+    if (cells == 4) return bfq_q_kernel<2, 4, BILIN, NK, QS, PIPE>;
+    if (cells == 2) return bfq_q_kernel<2, 2, BILIN, NK, QS, PIPE>;
   } else {
-    if (cells == 2) return bfq_q_kernel<MT, 2, BILIN, NK, QS>;
-    if (cells == 1) return bfq_q_kernel<MT, 1, BILIN, NK, QS>;
+    if (cells == 2) return bfq_q_kernel<MT, 2, BILIN, NK, QS, PIPE>;
+    if (cells == 1) return bfq_q_kernel<MT, 1, BILIN, NK, QS, PIPE>;
   }
   return nullptr;
 }
 
-template <bool BILIN>
-QKernel pick_kernel(int mt, int cells, int nk, int qs) {
+template <bool BILIN, bool PIPE>
+QKernel pick_kernel_p(int mt, int cells, int nk, int qs) {
   QKernel k = nullptr;
   if (!std::getenv("BFQ_GENERIC")) {
-    if (nk == 13 && qs == 172) k = pick_fixed<BILIN, 13, 172>(mt, cells);
-    else if (nk == 9 && qs == 84) k = pick_fixed<BILIN, 9, 84>(mt, cells);
-    else if (nk == 11 && qs == 124) k = pick_fixed<BILIN, 11, 124>(mt, cells);
-    else if (nk == 5 && qs == 28) k = pick_fixed<BILIN, 5, 28>(mt, cells);
-    else if (nk == 17 && qs == 292) k = pick_fixed<BILIN, 17, 292>(mt, cells);
+    if (nk == 13 && qs == 172) k = pick_fixed<BILIN, PIPE, 13, 172>(mt, cells);
+    else if (nk == 9 && qs == 84) k = pick_fixed<BILIN, PIPE, 9, 84>(mt, cells);
+    else if (nk == 11 && qs == 124) k = pick_fixed<BILIN, PIPE, 11, 124>(mt, cells);
+    else if (nk == 5 && qs == 28) k = pick_fixed<BILIN, PIPE, 5, 28>(mt, cells);
+    else if (nk == 17 && qs == 292) k = pick_fixed<BILIN, PIPE, 17, 292>(mt, cells);
     if (k) return k;
   }
   if (mt == 1) {
-    if (cells == 8) return bfq_q_kernel<1, 8, BILIN, 0, 0>;
-    if (cells == 4) return bfq_q_kernel<1, 4, BILIN, 0, 0>;
-    if (cells == 2) return bfq_q_kernel<1, 2, BILIN, 0, 0>;
-    if (cells == 1) return bfq_q_kernel<1, 1, BILIN, 0, 0>;
+    if (cells == 8) return bfq_q_kernel<1, 8, BILIN, 0, 0, PIPE>;
+    if (cells == 4) return bfq_q_kernel<1, 4, BILIN, 0, 0, PIPE>;
+    if (cells == 2) return bfq_q_kernel<1, 2, BILIN, 0, 0, PIPE>;
+    if (cells == 1) return bfq_q_kernel<1, 1, BILIN, 0, 0, PIPE>;
   }
   if (mt == 2) {
-    if (cells == 4) return bfq_q_kernel<2, 4, BILIN, 0, 0>;
-    if (cells == 2) return bfq_q_kernel<2, 2, BILIN, 0, 0>;
-    if (cells == 1) return bfq_q_kernel<2, 1, BILIN, 0, 0>;
+    if (cells == 4) return bfq_q_kernel<2, 4, BILIN, 0, 0, PIPE>;
+    if (cells == 2) return bfq_q_kernel<2, 2, BILIN, 0, 0, PIPE>;
+    if (cells == 1) return bfq_q_kernel<2, 1, BILIN, 0, 0, PIPE>;
   }
   if (mt == 3) {
-    if (cells == 2) return bfq_q_kernel<3, 2, BILIN, 0, 0>;
-    if (cells == 1) return bfq_q_kernel<3, 1, BILIN, 0, 0>;
+    if (cells == 2) return bfq_q_kernel<3, 2, BILIN, 0, 0, PIPE>;
+    if (cells == 1) return bfq_q_kernel<3, 1, BILIN, 0, 0, PIPE>;
   }
   return nullptr;
+}
+
+// BFQ_PIPE=0 selects the non-pipelined stage 1 (A/B timing); default pipelined.
+template <bool BILIN>
+QKernel pick_kernel(int mt, int cells, int nk, int qs) {
+  const char* e = std::getenv("BFQ_PIPE");
+  const bool pipe = !(e && e[0] == '0');
+  return pipe ? pick_kernel_p<BILIN, true>(mt, cells, nk, qs) : pick_kernel_p<BILIN, false>(mt, cells, nk, qs);
 }
 
 // ------------------------------------------------------------ small kernels
@@ -368,13 +377,17 @@ int launch_q(const bfq_plan* plan, const DevProgram& dp, const double* f2, const
   p.nw = dp.cfg.nw;
   p.nstage = dp.cfg.nstage;
   p.conservation = hp.conservation ? 1 : 0;
+  {
+    static const int dbg = std::getenv("BFQ_DEBUG") ? std::atoi(std::getenv("BFQ_DEBUG")) : 0;
+    p.debug = dbg;
+  }
   const long long blocks = p.n_tiles * (long long)dp.n_items;
   if (blocks > 0x7fffffffLL) {
     set_error("too many cells for one launch");
     return BFQ_EINVAL;
   }
   QKernel k = dp.kernel;
-  k<<<(unsigned)blocks, (dp.cfg.nw + 1) * 32, dp.cfg.smem, st>>>(p);
+  k<<<(unsigned)blocks, dp.cfg.nw * 32, dp.cfg.smem, st>>>(p);
   BFQ_CUDA_TRY(cudaGetLastError());
   return BFQ_OK;
 }

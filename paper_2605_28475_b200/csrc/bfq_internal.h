@@ -36,7 +36,7 @@ struct alignas(16) Row {
 struct alignas(16) ChanEntry {
   int32_t tau;         // R block index (0-based channel)
   int32_t slice_base;  // index into the expanded slice-start table; slice of m1 = base + m1
-  int32_t weight2;     // 1: contribution doubled (slot-symmetry fold, l2 < l3)
+  int32_t weight2;     // 1: contribution doubled (fold, l2 < l3); resolved at plan time into a scaled R copy
   int32_t pad;
 };
 

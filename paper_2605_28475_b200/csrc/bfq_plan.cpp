@@ -380,6 +380,16 @@ int build_host_plan(const bfq_desc& d, int smem_limit, HostPlan& hp) {
   };
   if (!make_program(hp.sym, false, fold) || !make_program(hp.full, true, false))
     return fail(BFQ_ESMEM, "no kernel configuration fits in shared memory for this n_k, l_max");
+  // Folded channels with l2 < l3 count twice: give them their own copy of the
+  // R block scaled by 2 (exact in fp64), so the kernel needs no weight.
+  for (ChanEntry& ce : hp.sym.chans) {
+    if (!ce.weight2) continue;
+    const size_t nb = hp.rblocks.size() / blk;
+    hp.rblocks.resize((nb + 1) * blk);
+    for (size_t i = 0; i < blk; ++i) hp.rblocks[nb * blk + i] = 2.0 * hp.rblocks[(size_t)ce.tau * blk + i];
+    ce.tau = (int32_t)nb;
+    ce.weight2 = 0;
+  }
 
   hp.alg_flops_per_cell = 2.0 * ((double)d.n_g * nk * nk + (double)d.n_s * nk * nk * nk);
   hp.alg_bytes_per_cell = 16.0 * nk * nq;

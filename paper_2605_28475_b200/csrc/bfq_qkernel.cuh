@@ -5,8 +5,9 @@
 // (the reference's angular-first order, contraction.py:293-317).
 //
 // CTA = one tile of CELLS cells (staged in shared memory) x up to two teams of
-// compute warps + one producer warp.  A team walks the channel list of one l1 group in lockstep
-// behind its own R ring (cp.async.bulk + mbarrier, fed by a producer warp).
+// compute warps.  A team walks the channel list of one l1 group in lockstep
+// behind its own R ring (cp.async.bulk + mbarrier; the last warp of the team
+// to release a slot refills it).
 // Each compute warp owns 8 DMMA rows "pairs" = (m1, cell), M1T = 8/CELLS
 // output columns for all CELLS cells, and for every channel runs
 //   stage 1  Phi_pair = A B^T over the slice rows: DMMA.8x8x4, M=a, N=b,
@@ -24,8 +25,8 @@
 // (f3 != f2: two staged arrays, no folding), NKT/QST = compile-time n_k and f
 // row stride (0 = runtime) so every gather uses an immediate offset.
 
-template <int MT, int CELLS, bool BILIN, int NKT, int QST>
-__global__ void __launch_bounds__(288, 1) bfq_q_kernel(const KParams p) {
+template <int MT, int CELLS, bool BILIN, int NKT, int QST, bool PIPE>
+__global__ void __launch_bounds__(256, 1) bfq_q_kernel(const KParams p) {
   constexpr int M1T = 8 / CELLS;
   constexpr bool FIXED = NKT > 0;
   constexpr int NF = BILIN ? 2 : 1;
@@ -42,22 +43,38 @@ __global__ void __launch_bounds__(288, 1) bfq_q_kernel(const KParams p) {
   const long long tile = (long long)blockIdx.x - item_idx * p.n_tiles;
   const Item item = p.items[item_idx];
 
-  // shared layout: barriers | R rings (team, stage) | Phi (per warp, 8 pairs) | f (cells)
+  // shared layout: barriers + arrival counters | R rings (team, stage) | Phi (per warp, 8 pairs) | f (cells)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);  // [team*4 + stage]
-  uint64_t* empty = full + 8;
+  int* arrivals = reinterpret_cast<int*>(full + 8);         // [team*4 + stage]
   double* rs = reinterpret_cast<double*>(smem_raw + 128);
   const int rblk = NK * K2S;
   double* phis = rs + 2 * NST * rblk;
   double* fs = phis + p.nw * 8 * K2S;
   const int cell_elems = NK * QS;
 
+  const unsigned rbytes = (unsigned)rblk * 8u;
+  // R ring protocol (no producer warp): thread 0 issues the first NST
+  // cp.async.bulk loads of each team; afterwards the last warp of a team to
+  // finish with a slot (smem arrival counter) issues the refill of that slot.
+  auto issue_r = [&](int t, int i) {
+    const Group g = p.groups[item.l1[t]];
+    const int s = i % NST;
+    const ChanEntry ce = p.chans[g.chan_off + i];
+    mbar_arrive_expect_tx(&full[t * 4 + s], rbytes);
+    bulk_g2s(rs + (t * NST + s) * rblk, p.R + (size_t)ce.tau * rblk, rbytes, &full[t * 4 + s]);
+  };
   if (threadIdx.x == 0) {
     for (int t = 0; t < 2; ++t)
       for (int s = 0; s < NST; ++s) {
         mbar_init(&full[t * 4 + s], 1);
-        mbar_init(&empty[t * 4 + s], (unsigned)max(item.nunits[t], 1));
+        arrivals[t * 4 + s] = 0;
       }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    for (int t = 0; t < 2; ++t)
+      if (item.nunits[t] > 0) {
+        const int n = p.groups[item.l1[t]].n_chan;
+        for (int i = 0; i < NST && i < n; ++i) issue_r(t, i);
+      }
   }
   // Phi padding columns (n_k^2 .. k2p) are read by stage 2 and must be 0.
   for (int i = threadIdx.x; i < p.nw * 8 * K2S; i += blockDim.x) phis[i] = 0.0;
@@ -79,35 +96,6 @@ __global__ void __launch_bounds__(288, 1) bfq_q_kernel(const KParams p) {
   }
   __syncthreads();
 
-  const unsigned rbytes = (unsigned)rblk * 8u;
-  if (warp >= p.nw) {
-    // ---------------- producer: one thread streams both teams' R_tau blocks,
-    // polling the two rings so neither team waits behind the other
-    if (lane == 0) {
-      int nch_t[2], off_t[2], next[2] = {0, 0};
-      for (int t = 0; t < 2; ++t) {
-        const Group grp = p.groups[item.l1[t]];
-        nch_t[t] = item.nunits[t] > 0 ? grp.n_chan : 0;
-        off_t[t] = grp.chan_off;
-      }
-      while (next[0] < nch_t[0] || next[1] < nch_t[1]) {
-        bool issued = false;
-        for (int t = 0; t < 2; ++t) {
-          const int i = next[t];
-          if (i >= nch_t[t]) continue;
-          const int s = i % NST;
-          if (i >= NST && !mbar_test(&empty[t * 4 + s], (unsigned)((i / NST) - 1) & 1u)) continue;
-          const ChanEntry ce = p.chans[off_t[t] + i];
-          mbar_arrive_expect_tx(&full[t * 4 + s], rbytes);
-          bulk_g2s(rs + (t * NST + s) * rblk, p.R + (size_t)ce.tau * rblk, rbytes, &full[t * 4 + s]);
-          next[t] = i + 1;
-          issued = true;
-        }
-        if (!issued) __nanosleep(256);
-      }
-    }
-    return;
-  }
   const int team = warp < item.nunits[0] ? 0 : 1;
   const int twarp = team == 0 ? warp : warp - item.nunits[0];
   if (team == 1 && twarp >= item.nunits[1]) return;
@@ -119,7 +107,7 @@ __global__ void __launch_bounds__(288, 1) bfq_q_kernel(const KParams p) {
 #pragma unroll
   for (int ml = 0; ml < M1T; ++ml) m1s[ml] = p.unit_m1[(grp.unit_off + unit) * M1T + ml];
   uint64_t* tfull = full + team * 4;
-  uint64_t* tempty = empty + team * 4;
+  int* tarr = arrivals + team * 4;
   const uint32_t ring_u32 = smem_u32(rs + team * NST * rblk);
   const uint32_t phw_u32 = smem_u32(phis + warp * 8 * K2S);
   const uint32_t cell_bytes = (uint32_t)cell_elems * 8u;
@@ -142,11 +130,6 @@ __global__ void __launch_bounds__(288, 1) bfq_q_kernel(const KParams p) {
 #pragma unroll
   for (int j = 0; j < MT; ++j) acc2[j][0] = acc2[j][1] = accb[j][0] = accb[j][1] = 0.0;
 
-  // Channel metadata is prefetched one channel ahead.  A warp's M1T slices
-  // are contiguous in the table and read by this warp only (L2, not L1), so
-  // (a) the next channel's row range is prefetched into L1 while the current
-  // channel computes and (b) the row stream runs one k-step ahead across
-  // slice and channel boundaries.
   const int nch = grp.n_chan;
   auto slice_bounds = [&](int ci, int* zs, int* ze) {
     const ChanEntry ce = p.chans[grp.chan_off + ci];
@@ -165,13 +148,147 @@ __global__ void __launch_bounds__(288, 1) bfq_q_kernel(const KParams p) {
       for (int z = (zs[ml] & ~7) + lane * 8; z < ze[ml]; z += 256)
         asm volatile("prefetch.global.L1 [%0];\n" ::"l"(p.rows + z));
   };
+  // Stage-1 operands of one k-step for all cells: A pre-scaled by g.
+  struct Ops {
+    double a[CELLS][MT], b[CELLS][MT];
+  };
+  auto gather = [&](const Row& rw, Ops& o) {
+    const uint32_t qa = (uint32_t)rw.q2 * 8u, qb = (uint32_t)rw.q3 * 8u;
+#pragma unroll
+    for (int cc = 0; cc < CELLS; ++cc)
+#pragma unroll
+      for (int t = 0; t < MT; ++t) {
+        o.a[cc][t] = rw.g * lds_ro(fa[t] + qa + cc * cell_bytes);
+        o.b[cc][t] = lds_ro(fb[t] + qb + cc * cell_bytes);
+      }
+  };
+  auto store_phi = [&](int ml, double (&acc)[CELLS][MT][MT][2]) {
+#pragma unroll
+    for (int cc = 0; cc < CELLS; ++cc) {
+      const uint32_t ph = phw_u32 + (uint32_t)((ml * CELLS + cc) * K2S) * 8u;
+#pragma unroll
+      for (int a = 0; a < MT; ++a)
+#pragma unroll
+        for (int b = 0; b < MT; ++b)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int ia = 8 * a + r0, ib = 8 * b + 2 * kq + e;
+            if (ia < NK && ib < NK) sts_v(ph + (uint32_t)(ia * NK + ib) * 8u, acc[cc][a][b][e]);
+          }
+    }
+  };
+
+  // ---- PIPE state: the warp's k-step stream over (current | next channel)
+  // slices v = 0..2*M1T-1; a cursor (v, z) names one k-step, v == 2*M1T = end.
+  constexpr int NV = 2 * M1T;
+  int zsv[NV], zev[NV];
+  struct Cur {
+    int v, z;
+  };
+  auto norm = [&](Cur c) {  // skip exhausted / empty slices
+#pragma unroll
+    for (int it = 0; it < NV; ++it)
+      if (c.v < NV && c.z >= zev[c.v]) {
+        ++c.v;
+        c.z = c.v < NV ? zsv[c.v] : 0;
+      }
+    return c;
+  };
+  auto adv = [&](Cur c) {
+    c.z += 4;
+    return norm(c);
+  };
+  auto row_at = [&](Cur c) {
+    Row r;
+    if (c.v < NV) {
+      r = load_row(p.rows, min(c.z + kq, zev[c.v] - 1));
+      if (c.z + kq >= zev[c.v]) r.g = 0.0;
+    } else {
+      r.q2 = 0;
+      r.q3 = 0;
+      r.g = 0.0;
+    }
+    return r;
+  };
+  Cur P0{0, 0}, P1{0, 0}, P2{0, 0};
+  Row r1, r2;
+  Ops cur;
+  double acc[CELLS][MT][MT][2];
   int zs_n[M1T], ze_n[M1T];
-  slice_bounds(0, zs_n, ze_n);
-  prefetch_rows_l1(zs_n, ze_n);
-  Row nxt = fetch_row(p.rows, zs_n[0] + kq, ze_n[0]);
+  Row nxt_row;
+  if constexpr (PIPE) {
+    slice_bounds(0, zsv, zev);
+    if (nch > 1) slice_bounds(1, zsv + M1T, zev + M1T);
+    else
+#pragma unroll
+      for (int v = M1T; v < NV; ++v) zsv[v] = zev[v] = 0;
+    prefetch_rows_l1(zsv, zev);
+    prefetch_rows_l1(zsv + M1T, zev + M1T);
+    P0 = norm(Cur{0, zsv[0]});
+    P1 = adv(P0);
+    P2 = adv(P1);
+    r1 = row_at(P1);
+    r2 = row_at(P2);
+    gather(row_at(P0), cur);
+#pragma unroll
+    for (int cc = 0; cc < CELLS; ++cc)
+#pragma unroll
+      for (int a = 0; a < MT; ++a)
+#pragma unroll
+        for (int b = 0; b < MT; ++b) acc[cc][a][b][0] = acc[cc][a][b][1] = 0.0;
+  } else {
+    slice_bounds(0, zs_n, ze_n);
+    prefetch_rows_l1(zs_n, ze_n);
+    nxt_row = fetch_row(p.rows, zs_n[0] + kq, ze_n[0]);
+  }
 
   for (int i = 0; i < nch; ++i) {
-    const int w2 = p.chans[grp.chan_off + i].weight2;
+    if constexpr (PIPE) {
+      // ---- stage 1 (pipelined): gathers one k-step ahead, rows two ahead
+      // valid output columns without rows in this channel: Phi = 0
+#pragma unroll
+      for (int ml = 0; ml < M1T; ++ml)
+        if (m1s[ml] >= 0 && zsv[ml] >= zev[ml]) {
+          double z0[CELLS][MT][MT][2];
+#pragma unroll
+          for (int cc = 0; cc < CELLS; ++cc)
+#pragma unroll
+            for (int a = 0; a < MT; ++a)
+#pragma unroll
+              for (int b = 0; b < MT; ++b) z0[cc][a][b][0] = z0[cc][a][b][1] = 0.0;
+          store_phi(ml, z0);
+        }
+      const int zstop = (p.debug & 1) ? 0 : 1;
+      while (P0.v < M1T && zstop) {
+        Ops nxt;
+        if (P1.v < NV) gather(r1, nxt);
+        const Cur P3 = adv(P2);
+        const Row r3 = row_at(P3);
+#pragma unroll
+        for (int cc = 0; cc < CELLS; ++cc)
+#pragma unroll
+          for (int a = 0; a < MT; ++a)
+#pragma unroll
+            for (int b = 0; b < MT; ++b) dmma884(acc[cc][a][b][0], acc[cc][a][b][1], cur.a[cc][a], cur.b[cc][b]);
+        if (P1.v != P0.v) {  // last k-step of this slice
+          store_phi(P0.v, acc);
+#pragma unroll
+          for (int cc = 0; cc < CELLS; ++cc)
+#pragma unroll
+            for (int a = 0; a < MT; ++a)
+#pragma unroll
+              for (int b = 0; b < MT; ++b) acc[cc][a][b][0] = acc[cc][a][b][1] = 0.0;
+        }
+        P0 = P1;
+        P1 = P2;
+        P2 = P3;
+        r1 = r2;
+        r2 = r3;
+        cur = nxt;
+      }
+    } else {
+    const int zs_dummy = 0;
+    (void)zs_dummy;
     int zs[M1T], ze[M1T];
 #pragma unroll
     for (int ml = 0; ml < M1T; ++ml) {
@@ -182,7 +299,6 @@ __global__ void __launch_bounds__(288, 1) bfq_q_kernel(const KParams p) {
       slice_bounds(i + 1, zs_n, ze_n);
       prefetch_rows_l1(zs_n, ze_n);
     }
-    const double wgt = w2 ? 2.0 : 1.0;
     // ---- stage 1: Phi for this warp's 8 (m1, cell) pairs
 #pragma unroll
     for (int ml = 0; ml < M1T; ++ml) {
@@ -193,13 +309,14 @@ __global__ void __launch_bounds__(288, 1) bfq_q_kernel(const KParams p) {
         for (int a = 0; a < MT; ++a)
 #pragma unroll
           for (int b = 0; b < MT; ++b) acc[cc][a][b][0] = acc[cc][a][b][1] = 0.0;
-      for (int z0 = zs[ml]; z0 < ze[ml]; z0 += 4) {
-        const Row rw = nxt;
+      const int zend = (p.debug & 1) ? zs[ml] : ze[ml];
+      for (int z0 = zs[ml]; z0 < zend; z0 += 4) {
+        const Row rw = nxt_row;
         // next row of the stream: this slice, else the next slice, else the
         // first slice of the next channel
-        if (z0 + 4 < ze[ml]) nxt = fetch_row(p.rows, z0 + 4 + kq, ze[ml]);
-        else if (ml + 1 < M1T) nxt = fetch_row(p.rows, zs[ml + 1 < M1T ? ml + 1 : ml] + kq, ze[ml + 1 < M1T ? ml + 1 : ml]);
-        else nxt = fetch_row(p.rows, zs_n[0] + kq, i + 1 < nch ? ze_n[0] : 0);
+        if (z0 + 4 < ze[ml]) nxt_row = fetch_row(p.rows, z0 + 4 + kq, ze[ml]);
+        else if (ml + 1 < M1T) nxt_row = fetch_row(p.rows, zs[ml + 1 < M1T ? ml + 1 : ml] + kq, ze[ml + 1 < M1T ? ml + 1 : ml]);
+        else nxt_row = fetch_row(p.rows, zs_n[0] + kq, i + 1 < nch ? ze_n[0] : 0);
         const uint32_t qa = (uint32_t)rw.q2 * 8u, qb = (uint32_t)rw.q3 * 8u;
 #pragma unroll
         for (int cc = 0; cc < CELLS; ++cc) {
@@ -217,8 +334,8 @@ __global__ void __launch_bounds__(288, 1) bfq_q_kernel(const KParams p) {
       }
       // empty slice: the stream skips it, keep the prefetch pointing at the next one
       if (zs[ml] >= ze[ml]) {
-        if (ml + 1 < M1T) nxt = fetch_row(p.rows, zs[ml + 1 < M1T ? ml + 1 : ml] + kq, ze[ml + 1 < M1T ? ml + 1 : ml]);
-        else nxt = fetch_row(p.rows, zs_n[0] + kq, i + 1 < nch ? ze_n[0] : 0);
+        if (ml + 1 < M1T) nxt_row = fetch_row(p.rows, zs[ml + 1 < M1T ? ml + 1 : ml] + kq, ze[ml + 1 < M1T ? ml + 1 : ml]);
+        else nxt_row = fetch_row(p.rows, zs_n[0] + kq, i + 1 < nch ? ze_n[0] : 0);
       }
       // accumulator (a = 8A + r0, b = 8B + 2kq + e) -> Phi row of the pair
 #pragma unroll
@@ -231,9 +348,10 @@ __global__ void __launch_bounds__(288, 1) bfq_q_kernel(const KParams p) {
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
               const int ia = 8 * a + r0, ib = 8 * b + 2 * kq + e;
-              if (ia < NK && ib < NK) sts_v(ph + (uint32_t)(ia * NK + ib) * 8u, wgt * acc[cc][a][b][e]);
+              if (ia < NK && ib < NK) sts_v(ph + (uint32_t)(ia * NK + ib) * 8u, acc[cc][a][b][e]);
             }
       }
+    }
     }
     __syncwarp();
     // ---- stage 2: out[pair, k1] += Phi[pair, :] . R_tau[k1, :]
@@ -241,9 +359,7 @@ __global__ void __launch_bounds__(288, 1) bfq_q_kernel(const KParams p) {
     mbar_wait(&tfull[s], (unsigned)(i / NST) & 1u);
     const uint32_t rb = ring_u32 + (uint32_t)(s * rblk) * 8u;
     const uint32_t pa = phw_u32 + (uint32_t)(r0 * K2S + kq) * 8u;
-    int k0 = 0;
-#pragma unroll 2
-    for (; k0 + 8 <= K2P; k0 += 8) {
+    auto step2 = [&](int k0) {
       const double av0 = lds_v(pa + k0 * 8), av1 = lds_v(pa + (k0 + 4) * 8);
       double bv0[MT], bv1[MT];
 #pragma unroll
@@ -256,6 +372,19 @@ __global__ void __launch_bounds__(288, 1) bfq_q_kernel(const KParams p) {
         dmma884(acc2[j][0], acc2[j][1], av0, bv0[j]);
         dmma884(accb[j][0], accb[j][1], av1, bv1[j]);
       }
+    };
+    int k0 = 0;
+    if (p.debug & 2) {
+      k0 = K2P;
+    } else if (FIXED && !(p.debug & 4)) {
+      // compile-time K: fully unrolled, no loop back-edge (whose register
+      // reuse forces NOP padding behind the DMMAs)
+#pragma unroll
+      for (int kk = 0; kk + 8 <= (FIXED ? (NKT * NKT + 3) / 4 * 4 : 0); kk += 8) step2(kk);
+      k0 = FIXED ? (NKT * NKT + 3) / 4 * 4 / 8 * 8 : 0;
+    } else {
+#pragma unroll 2
+      for (; k0 + 8 <= K2P; k0 += 8) step2(k0);
     }
     if (k0 < K2P) {  // K2P is a multiple of 4: at most one step left
       const double av = lds_v(pa + k0 * 8);
@@ -263,7 +392,48 @@ __global__ void __launch_bounds__(288, 1) bfq_q_kernel(const KParams p) {
       for (int j = 0; j < MT; ++j) dmma884(acc2[j][0], acc2[j][1], av, lds_v(rb + rrow[j] + k0 * 8));
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&tempty[s]);
+    if (lane == 0) {
+      // every lane's reads of slot s are complete (consumed by its DMMAs)
+      __threadfence_block();
+      if (atomicAdd(&tarr[s], 1) == item.nunits[team] - 1) {
+        tarr[s] = 0;
+        if (i + NST < nch) issue_r(team, i + NST);
+      }
+    }
+    if constexpr (PIPE) {
+      if (i + 1 < nch) {
+        // slide the stream window: next channel becomes current
+        bool p0_end = P0.v >= NV, p1_end = P1.v >= NV, p2_end = P2.v >= NV;
+        if (P0.v < M1T) p0_end = p1_end = p2_end = true;  // stage 1 skipped (BFQ_DEBUG timing runs)
+#pragma unroll
+        for (int v = 0; v < M1T; ++v) {
+          zsv[v] = zsv[v + M1T];
+          zev[v] = zev[v + M1T];
+        }
+        if (i + 2 < nch) {
+          slice_bounds(i + 2, zsv + M1T, zev + M1T);
+          prefetch_rows_l1(zsv + M1T, zev + M1T);
+        } else {
+#pragma unroll
+          for (int v = M1T; v < NV; ++v) zsv[v] = zev[v] = 0;
+        }
+        if (!p0_end) P0.v -= M1T;
+        if (!p1_end) P1.v -= M1T;
+        if (!p2_end) P2.v -= M1T;
+        if (p0_end) {
+          P0 = norm(Cur{0, zsv[0]});
+          gather(row_at(P0), cur);
+        }
+        if (p1_end) {
+          P1 = adv(P0);
+          r1 = row_at(P1);
+        }
+        if (p2_end) {
+          P2 = adv(P1);
+          r2 = row_at(P2);
+        }
+      }
+    }
   }
 
   // ---------------- epilogue: pair r0 = (m1 = m1s[r0/CELLS], cell = r0%CELLS)
