@@ -29,6 +29,9 @@ CONFIGS = {
     "hs8": ("hs_n8", 4096, "pm", "config2: hard spheres N=L=8, perturbed Maxwellians"),
     "mm10": ("mm_n10", 32768, "bimodal", "config5 operator: Maxwell N=L=10, bimodal cells (single Q eval)"),
     "hs4": ("hs_n4", 65536, "pm", "hard spheres N=L=4 (small)"),
+    "hs16": ("hs_n16", 16384, "pm", "config4: hard spheres N=L=16, perturbed Maxwellians"),
+    "rk4": ("mm_n10", 32768, "bimodal", "config5: Maxwell N=L=10, bimodal cells, GPU-resident RK4 dt=0.01 "
+                                         "(one step = one RK4 step = 4 Q(f,f) per cell)"),
 }
 METRIC = "Q(f,f) cell-evals/s (fp64, hard spheres L=N=12) and FP64/HBM roofline frac"
 FP64_PEAK_TFLOPS = 37.1  # DMMA.8x8x4 sustained, measured on this pool (profiles/fp64_peak.txt)
@@ -159,18 +162,22 @@ def run_reference(args, rank, world):
 
     op = load_cache(os.path.join(ROOT, "operators", opfile + ".bfct"))
     cells = make_cells(args.config, op.cfg.n_k, op.cfg.l_max, 256, seed=args.seed, start=0)
-    rates = []
+    rates, walls = [], []
     for _ in range(args.warmup):
         cpu_port_rate(args.config, cells, budget_s=2.0)
     for _ in range(args.steps):
-        rates.append(cpu_port_rate(args.config, cells, budget_s=args.cpu_budget)["value"])
-    last = cpu_port_rate(args.config, cells[:64], budget_s=1.0)
+        r = cpu_port_rate(args.config, cells, budget_s=args.cpu_budget)
+        rates.append(r["value"])
+        walls.append(r["wall_s"])
+        last = r
     v = statistics.median(rates)
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "cells/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(walls),
+        "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.json distributions)",
-        "config": {"workload": desc, "cells_per_gpu": n_cells, "operator": opfile},
+        "config": {"workload": desc, "cells_per_gpu": n_cells, "operator": opfile,
+                   "step": "one bounded sample of the workload on all host cores (multiprocessing pool)"},
         "cpu_baseline": {"value": v, "unit": "cells/s", "cores": last["cores"], "kind": "port",
                          "sample": f"~{args.cpu_budget:.0f} s of per-core work per step, cells of {desc}"},
         "e2e": {"value": v, "unit": "cells/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -208,8 +215,19 @@ def run_ours(args, rank, world, local_rank):
             dist.barrier()
         torch.cuda.synchronize(dev)
 
+    rk4 = args.config == "rk4"
+    if rk4:
+        y = f.clone()
+        work = torch.empty((3,) + tuple(f.shape), dtype=torch.float64, device=dev)
+        flag = torch.zeros(1, dtype=torch.int32, device=dev)
+
+        def one_step():
+            plan.rk4_step_device(y.data_ptr(), work.data_ptr(), n_cells, 0.01, flag.data_ptr(), stream.cuda_stream)
+    else:
+        def one_step():
+            engine.evaluate_batch(plan, f, out=q)
     for _ in range(max(args.warmup, 0)):
-        engine.evaluate_batch(plan, f, out=q)
+        one_step()
     barrier()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -218,7 +236,7 @@ def run_ours(args, rank, world, local_rank):
         t0 = time.perf_counter()
         for i in range(args.steps):
             starts[i].record(stream)
-            engine.evaluate_batch(plan, f, out=q)
+            one_step()
             ends[i].record(stream)
         barrier()
         wall = time.perf_counter() - t0
@@ -229,11 +247,21 @@ def run_ours(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
-    value = n_cells * world * args.steps / (total_ms / 1e3)
+    q_per_step = 4 if rk4 else 1
+    value = n_cells * world * args.steps * q_per_step / (total_ms / 1e3)
 
-    # conservation diagnostics of the last step, all-reduced (max |production|)
+    # conservation diagnostics of the last step, all-reduced (max |production|,
+    # or for RK4 the max drift of the invariants from the initial state)
     mom = torch.empty((n_cells, 5), dtype=torch.float64, device=dev)
-    plan.moments_device(q.data_ptr(), mom.data_ptr(), n_cells, stream.cuda_stream)
+    if rk4:
+        mom0 = torch.empty_like(mom)
+        plan.moments_device(f.data_ptr(), mom0.data_ptr(), n_cells, stream.cuda_stream)
+        plan.moments_device(y.data_ptr(), mom.data_ptr(), n_cells, stream.cuda_stream)
+        mom = mom - mom0
+        if int(flag.item()):
+            raise RuntimeError("RK4 diverged")
+    else:
+        plan.moments_device(q.data_ptr(), mom.data_ptr(), n_cells, stream.cuda_stream)
     diag = mom.abs().amax(dim=0)
     if dist is not None:
         dist.all_reduce(diag, op=dist.ReduceOp.MAX)
@@ -241,7 +269,7 @@ def run_ours(args, rank, world, local_rank):
 
     # end-to-end through the C ABI with host buffers (pinned), copies timed
     e2e = None
-    if args.e2e_steps > 0:
+    if args.e2e_steps > 0 and not rk4:
         hin = torch.from_numpy(host).pin_memory()
         hout = torch.empty_like(hin).pin_memory()
         from paper_2605_28475_b200 import _lib
@@ -265,7 +293,7 @@ def run_ours(args, rank, world, local_rank):
             dist.destroy_process_group()
         return
     flops_cell, bytes_cell = plan.flops_per_cell, plan.bytes_per_cell
-    achieved = flops_cell * n_cells / (statistics.mean(step_ms) / 1e3) / 1e12
+    achieved = flops_cell * n_cells * q_per_step / (statistics.mean(step_ms) / 1e3) / 1e12
     traffic = None
     tpath = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
     if os.path.exists(tpath):
@@ -289,11 +317,15 @@ def run_ours(args, rank, world, local_rank):
                      "hbm_frac": bytes_cell * n_cells / (statistics.mean(step_ms) / 1e3) / 1e9
                      / measured_peaks().get("hbm_gbs", 6456.5)},
         "e2e": e2e,
-        "gpu_launches": args.steps,
+        "gpu_launches": args.steps * (7 if rk4 else 1),
         "clocks": clk.summary(),
         "conservation_max_abs": conservation_max,
         "wall_s": wall,
     }
+    if rk4:
+        line["rk4"] = {"dt": 0.01, "steps_per_s": args.steps / (total_ms / 1e3),
+                       "full_run_estimate_s": 1000 * ms_per_step / 1e3,
+                       "moment_drift_max": conservation_max}
     if world == 1 and not args.no_cpu:
         cpu = cpu_port_rate(args.config, host[:256], budget_s=args.cpu_budget)
         line["cpu_baseline"] = {"value": cpu["value"], "unit": "cells/s", "cores": cpu["cores"], "kind": "port",
@@ -314,7 +346,7 @@ def main():
     ap.add_argument("--cells", type=int, default=0, help="override cells per GPU")
     ap.add_argument("--seed", type=int, default=20260520)
     ap.add_argument("--e2e-steps", type=int, default=2)
-    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--cpu-budget", type=float, default=10.0, help="seconds of per-core CPU work per sample")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     world = env_int("WORLD_SIZE", 1)

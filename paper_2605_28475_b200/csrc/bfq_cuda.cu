@@ -55,6 +55,8 @@ struct DevProgram {
   void (*kernel)(const struct KParams) = nullptr;
 };
 
+unsigned long long* bfq_dbg_clk_ptr = nullptr;  // BFQ_DEBUG bit 3 only
+
 struct KParams {
   const double* f2;
   const double* f3;
@@ -71,7 +73,9 @@ struct KParams {
   int nk, nq, qs, k2s, k2p;
   int cells, m1t, nw, nstage;
   int conservation;
-  int debug;  // timing experiments only (BFQ_DEBUG): bit0 skip stage 1, bit1 skip stage 2
+  int hdr, max_chan;
+  int debug;  // timing experiments only (BFQ_DEBUG): bit0 skip stage 1, bit1 skip stage 2, bit3 phase clocks
+  unsigned long long* dbg_clk;  // [8] phase cycle totals when bit3 set
 };
 
 // ------------------------------------------------------------ PTX helpers
@@ -159,8 +163,13 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       : "memory");
 }
 
+// volatile: the compiler must issue the table-row load where it is written
+// (early, as a prefetch), not sink it next to its first use.
 __device__ __forceinline__ Row load_row(const Row* rows, int z) {
-  const int4 v = __ldg(reinterpret_cast<const int4*>(rows) + z);
+  int4 v;
+  asm volatile("ld.global.nc.v4.s32 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(reinterpret_cast<const int4*>(rows) + z));
   Row r;
   r.q2 = v.x;
   r.q3 = v.y;
@@ -177,6 +186,15 @@ __device__ __forceinline__ Row fetch_row(const Row* rows, int z, int ze) {
   return r;
 }
 
+// Branch-free fetch of row z of a range ending at ze: always loads a valid
+// row (clamped into [0, ze-1], row 0 for an empty range) and zeroes g when z
+// is past the end, so padding lanes and exhausted streams contribute 0.
+__device__ __forceinline__ Row fetch_row_bf(const Row* rows, int z, int ze) {
+  Row r = load_row(rows, max(min(z, ze - 1), 0));
+  r.g = z < ze ? r.g : 0.0;
+  return r;
+}
+
 __device__ __forceinline__ Row fetch_row_clamped(const Row* rows, int z, int ze) {
   Row r = load_row(rows, min(z, ze - 1));
   if (z >= ze) r.g = 0.0;  // padding lane of the last k-step: contributes 0
@@ -190,58 +208,50 @@ typedef void (*QKernel)(const KParams);
 
 // Compile-time-size instantiations for the BASELINE configurations (all
 // gathers then use immediate offsets); anything else runs the generic kernel.
-template <bool BILIN, bool PIPE, int NK, int QS>
+template <bool BILIN, int NK, int QS>
 QKernel pick_fixed(int mt, int cells) {
   constexpr int MT = (NK + 7) / 8;
   if (mt != MT) return nullptr;
   if constexpr (MT == 1) {
-    if (cells == 8) return bfq_q_kernel<1, 8, BILIN, NK, QS, PIPE>;
-    if (cells == 4) return bfq_q_kernel<1, 4, BILIN, NK, QS, PIPE>;
+    if (cells == 8) return bfq_q_kernel<1, 8, BILIN, NK, QS>;
+    if (cells == 4) return bfq_q_kernel<1, 4, BILIN, NK, QS>;
   } else if constexpr (MT == 2) {
-    if (cells == 4) return bfq_q_kernel<2, 4, BILIN, NK, QS, PIPE>;
-    if (cells == 2) return bfq_q_kernel<2, 2, BILIN, NK, QS, PIPE>;
+    if (cells == 4) return bfq_q_kernel<2, 4, BILIN, NK, QS>;
+    if (cells == 2) return bfq_q_kernel<2, 2, BILIN, NK, QS>;
   } else {
-    if (cells == 2) return bfq_q_kernel<MT, 2, BILIN, NK, QS, PIPE>;
-    if (cells == 1) return bfq_q_kernel<MT, 1, BILIN, NK, QS, PIPE>;
+    if (cells == 2) return bfq_q_kernel<MT, 2, BILIN, NK, QS>;
+    if (cells == 1) return bfq_q_kernel<MT, 1, BILIN, NK, QS>;
   }
   return nullptr;
 }
 
-template <bool BILIN, bool PIPE>
-QKernel pick_kernel_p(int mt, int cells, int nk, int qs) {
+template <bool BILIN>
+QKernel pick_kernel(int mt, int cells, int nk, int qs) {
   QKernel k = nullptr;
   if (!std::getenv("BFQ_GENERIC")) {
-    if (nk == 13 && qs == 172) k = pick_fixed<BILIN, PIPE, 13, 172>(mt, cells);
-    else if (nk == 9 && qs == 84) k = pick_fixed<BILIN, PIPE, 9, 84>(mt, cells);
-    else if (nk == 11 && qs == 124) k = pick_fixed<BILIN, PIPE, 11, 124>(mt, cells);
-    else if (nk == 5 && qs == 28) k = pick_fixed<BILIN, PIPE, 5, 28>(mt, cells);
-    else if (nk == 17 && qs == 292) k = pick_fixed<BILIN, PIPE, 17, 292>(mt, cells);
+    if (nk == 13 && qs == 172) k = pick_fixed<BILIN, 13, 172>(mt, cells);
+    else if (nk == 9 && qs == 84) k = pick_fixed<BILIN, 9, 84>(mt, cells);
+    else if (nk == 11 && qs == 124) k = pick_fixed<BILIN, 11, 124>(mt, cells);
+    else if (nk == 5 && qs == 28) k = pick_fixed<BILIN, 5, 28>(mt, cells);
+    else if (nk == 17 && qs == 292) k = pick_fixed<BILIN, 17, 292>(mt, cells);
     if (k) return k;
   }
   if (mt == 1) {
-    if (cells == 8) return bfq_q_kernel<1, 8, BILIN, 0, 0, PIPE>;
-    if (cells == 4) return bfq_q_kernel<1, 4, BILIN, 0, 0, PIPE>;
-    if (cells == 2) return bfq_q_kernel<1, 2, BILIN, 0, 0, PIPE>;
-    if (cells == 1) return bfq_q_kernel<1, 1, BILIN, 0, 0, PIPE>;
+    if (cells == 8) return bfq_q_kernel<1, 8, BILIN, 0, 0>;
+    if (cells == 4) return bfq_q_kernel<1, 4, BILIN, 0, 0>;
+    if (cells == 2) return bfq_q_kernel<1, 2, BILIN, 0, 0>;
+    if (cells == 1) return bfq_q_kernel<1, 1, BILIN, 0, 0>;
   }
   if (mt == 2) {
-    if (cells == 4) return bfq_q_kernel<2, 4, BILIN, 0, 0, PIPE>;
-    if (cells == 2) return bfq_q_kernel<2, 2, BILIN, 0, 0, PIPE>;
-    if (cells == 1) return bfq_q_kernel<2, 1, BILIN, 0, 0, PIPE>;
+    if (cells == 4) return bfq_q_kernel<2, 4, BILIN, 0, 0>;
+    if (cells == 2) return bfq_q_kernel<2, 2, BILIN, 0, 0>;
+    if (cells == 1) return bfq_q_kernel<2, 1, BILIN, 0, 0>;
   }
   if (mt == 3) {
-    if (cells == 2) return bfq_q_kernel<3, 2, BILIN, 0, 0, PIPE>;
-    if (cells == 1) return bfq_q_kernel<3, 1, BILIN, 0, 0, PIPE>;
+    if (cells == 2) return bfq_q_kernel<3, 2, BILIN, 0, 0>;
+    if (cells == 1) return bfq_q_kernel<3, 1, BILIN, 0, 0>;
   }
   return nullptr;
-}
-
-// BFQ_PIPE=0 selects the non-pipelined stage 1 (A/B timing); default pipelined.
-template <bool BILIN>
-QKernel pick_kernel(int mt, int cells, int nk, int qs) {
-  const char* e = std::getenv("BFQ_PIPE");
-  const bool pipe = !(e && e[0] == '0');
-  return pipe ? pick_kernel_p<BILIN, true>(mt, cells, nk, qs) : pick_kernel_p<BILIN, false>(mt, cells, nk, qs);
 }
 
 // ------------------------------------------------------------ small kernels
@@ -377,9 +387,18 @@ int launch_q(const bfq_plan* plan, const DevProgram& dp, const double* f2, const
   p.nw = dp.cfg.nw;
   p.nstage = dp.cfg.nstage;
   p.conservation = hp.conservation ? 1 : 0;
+  p.hdr = dp.cfg.hdr;
+  p.max_chan = dp.cfg.max_chan;
   {
     static const int dbg = std::getenv("BFQ_DEBUG") ? std::atoi(std::getenv("BFQ_DEBUG")) : 0;
     p.debug = dbg;
+    static unsigned long long* clk = nullptr;
+    if ((dbg & 8) && !clk) {
+      cudaMalloc(&clk, 8 * sizeof(unsigned long long));
+      cudaMemset(clk, 0, 8 * sizeof(unsigned long long));
+    }
+    p.dbg_clk = clk;
+    if (dbg & 8) bfq_dbg_clk_ptr = clk;
   }
   const long long blocks = p.n_tiles * (long long)dp.n_items;
   if (blocks > 0x7fffffffLL) {
@@ -670,5 +689,15 @@ const char* bfq_strerror(int code) {
 }
 
 const char* bfq_last_error(void) { return get_error().c_str(); }
+
+// Debug only (BFQ_DEBUG bit 3): copy out and reset the per-phase cycle totals.
+extern "C" int bfq_debug_phase_clocks(unsigned long long* out8);
+int bfq_debug_phase_clocks(unsigned long long* out8) {
+  if (!bfq_dbg_clk_ptr) return BFQ_EINVAL;
+  cudaDeviceSynchronize();
+  cudaMemcpy(out8, bfq_dbg_clk_ptr, 64, cudaMemcpyDeviceToHost);
+  cudaMemset(bfq_dbg_clk_ptr, 0, 64);
+  return BFQ_OK;
+}
 
 }  // extern "C"

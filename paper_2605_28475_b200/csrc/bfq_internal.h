@@ -72,6 +72,8 @@ struct KernelConfig {
   int nstage = 0;  // R-block ring depth (per team; two teams per CTA)
   int nf = 1;      // f arrays staged per cell (2 for bilinear Q(f2,f3))
   int smem = 0;    // dynamic shared memory bytes
+  int hdr = 0;     // bytes of the barrier/counter/channel-index header
+  int max_chan = 0;
 };
 
 // Host image of one channel program (everything the kernel needs besides f and R).

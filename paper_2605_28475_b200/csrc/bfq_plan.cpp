@@ -38,14 +38,18 @@ static inline int isqrt_floor(int x) {
 static int conflict_free_stride(int n) { return conflict_free_stride_dev(n); }
 
 // Shared memory of one CTA: two R rings (one per team) | Phi per warp | f of the tile.
-static long smem_bytes(int nk, int qs, int k2s, int nf, int cells, int nw, int nstage) {
-  return 128 + 2L * nstage * nk * k2s * 8 + (long)nw * 8 * k2s * 8 + (long)nf * cells * nk * qs * 8;
+static long smem_bytes(int nk, int qs, int k2s, int nf, int cells, int nw, int nstage, int hdr) {
+  return hdr + 2L * nstage * nk * k2s * 8 + (long)nw * 8 * k2s * 8 + (long)nf * cells * nk * qs * 8;
 }
+
+// Header region: 8 mbarriers, 8 arrival counters, then the R-block index of
+// every channel of both teams (the refill path reads it from shared memory).
+static int header_bytes(int max_chan) { return 96 + (2 * max_chan * 4 + 31) / 32 * 32; }
 
 // DMMA.8x8x4 issues with a ~15-cycle stall on its warp, so a scheduler needs
 // at least two compute warps to keep the FP64 tensor pipe fed while the other
 // warp issues gathers: prefer 8 compute warps, then fewer cells per tile.
-static bool choose_config(int nk, int qs, int k2s, int nf, int smem_limit, KernelConfig& c) {
+static bool choose_config(int nk, int qs, int k2s, int nf, int smem_limit, int max_chan, KernelConfig& c) {
   c.mt = (nk + 7) / 8;
   c.nf = nf;
   static const int opts[][3] = {  // cells, compute warps, ring stages
@@ -57,7 +61,9 @@ static bool choose_config(int nk, int qs, int k2s, int nf, int smem_limit, Kerne
   for (auto& o : opts) {
     if (force_cells && o[0] != force_cells) continue;
     if (o[0] > max_cells) continue;
-    const long smem = smem_bytes(nk, qs, k2s, nf, o[0], o[1], o[2]);
+    c.hdr = header_bytes(max_chan);
+    c.max_chan = max_chan;
+    const long smem = smem_bytes(nk, qs, k2s, nf, o[0], o[1], o[2], c.hdr);
     if (smem > smem_limit) continue;
     c.cells = o[0];
     c.m1t = 8 / o[0];
@@ -374,7 +380,9 @@ int build_host_plan(const bfq_desc& d, int smem_limit, HostPlan& hp) {
       }
       pg.groups[l1].n_chan = (int)pg.chans.size() - pg.groups[l1].chan_off;
     }
-    if (!choose_config(nk, hp.qs, hp.k2s, bilinear ? 2 : 1, smem_limit, pg.cfg)) return false;
+    int max_chan = 1;
+    for (const Group& g : pg.groups) max_chan = std::max(max_chan, g.n_chan);
+    if (!choose_config(nk, hp.qs, hp.k2s, bilinear ? 2 : 1, smem_limit, max_chan, pg.cfg)) return false;
     build_items(hp, pg);
     return true;
   };

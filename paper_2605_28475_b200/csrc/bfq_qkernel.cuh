@@ -25,7 +25,7 @@
 // (f3 != f2: two staged arrays, no folding), NKT/QST = compile-time n_k and f
 // row stride (0 = runtime) so every gather uses an immediate offset.
 
-template <int MT, int CELLS, bool BILIN, int NKT, int QST, bool PIPE>
+template <int MT, int CELLS, bool BILIN, int NKT, int QST>
 __global__ void __launch_bounds__(256, 1) bfq_q_kernel(const KParams p) {
   constexpr int M1T = 8 / CELLS;
   constexpr bool FIXED = NKT > 0;
@@ -46,7 +46,8 @@ __global__ void __launch_bounds__(256, 1) bfq_q_kernel(const KParams p) {
   // shared layout: barriers + arrival counters | R rings (team, stage) | Phi (per warp, 8 pairs) | f (cells)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);  // [team*4 + stage]
   int* arrivals = reinterpret_cast<int*>(full + 8);         // [team*4 + stage]
-  double* rs = reinterpret_cast<double*>(smem_raw + 128);
+  int* ctau = arrivals + 8;                                   // [team][max_chan] R block index
+  double* rs = reinterpret_cast<double*>(smem_raw + p.hdr);
   const int rblk = NK * K2S;
   double* phis = rs + 2 * NST * rblk;
   double* fs = phis + p.nw * 8 * K2S;
@@ -56,12 +57,10 @@ __global__ void __launch_bounds__(256, 1) bfq_q_kernel(const KParams p) {
   // R ring protocol (no producer warp): thread 0 issues the first NST
   // cp.async.bulk loads of each team; afterwards the last warp of a team to
   // finish with a slot (smem arrival counter) issues the refill of that slot.
-  auto issue_r = [&](int t, int i) {
-    const Group g = p.groups[item.l1[t]];
+  auto issue_r = [&](int t, int i, int tau) {
     const int s = i % NST;
-    const ChanEntry ce = p.chans[g.chan_off + i];
     mbar_arrive_expect_tx(&full[t * 4 + s], rbytes);
-    bulk_g2s(rs + (t * NST + s) * rblk, p.R + (size_t)ce.tau * rblk, rbytes, &full[t * 4 + s]);
+    bulk_g2s(rs + (t * NST + s) * rblk, p.R + (size_t)tau * rblk, rbytes, &full[t * 4 + s]);
   };
   if (threadIdx.x == 0) {
     for (int t = 0; t < 2; ++t)
@@ -72,10 +71,16 @@ __global__ void __launch_bounds__(256, 1) bfq_q_kernel(const KParams p) {
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     for (int t = 0; t < 2; ++t)
       if (item.nunits[t] > 0) {
-        const int n = p.groups[item.l1[t]].n_chan;
-        for (int i = 0; i < NST && i < n; ++i) issue_r(t, i);
+        const Group g = p.groups[item.l1[t]];
+        for (int i = 0; i < NST && i < g.n_chan; ++i) issue_r(t, i, p.chans[g.chan_off + i].tau);
       }
   }
+  // channel R-block indices of both teams, for the refills
+  for (int t = 0; t < 2; ++t)
+    if (item.nunits[t] > 0) {
+      const Group g = p.groups[item.l1[t]];
+      for (int i = threadIdx.x; i < g.n_chan; i += blockDim.x) ctau[t * p.max_chan + i] = p.chans[g.chan_off + i].tau;
+    }
   // Phi padding columns (n_k^2 .. k2p) are read by stage 2 and must be 0.
   for (int i = threadIdx.x; i < p.nw * 8 * K2S; i += blockDim.x) phis[i] = 0.0;
   // stage the tile's cells: global (cell, k, q) -> shared (cell, k, q padded to QS);
@@ -99,10 +104,16 @@ __global__ void __launch_bounds__(256, 1) bfq_q_kernel(const KParams p) {
   const int team = warp < item.nunits[0] ? 0 : 1;
   const int twarp = team == 0 ? warp : warp - item.nunits[0];
   if (team == 1 && twarp >= item.nunits[1]) return;
+  // team fields as scalars (a dynamically indexed Item would live in local memory)
+  const int t_l1 = team ? item.l1[1] : item.l1[0];
+  const int t_ubase = team ? item.ubase[1] : item.ubase[0];
+  const int t_nunits = team ? item.nunits[1] : item.nunits[0];
 
   // ---------------- compute warp
-  const Group grp = p.groups[item.l1[team]];
-  const int unit = item.ubase[team] + twarp;
+  const bool clk_on = (p.debug & 8) != 0;
+  long long ck_s1 = 0, ck_w = 0, ck_s2 = 0, ck_rf = 0, ck0 = clock64(), ckt = ck0;
+  const Group grp = p.groups[t_l1];
+  const int unit = t_ubase + twarp;
   int m1s[M1T];  // this warp's output columns (plan-balanced), -1 = empty slot
 #pragma unroll
   for (int ml = 0; ml < M1T; ++ml) m1s[ml] = p.unit_m1[(grp.unit_off + unit) * M1T + ml];
@@ -148,20 +159,7 @@ __global__ void __launch_bounds__(256, 1) bfq_q_kernel(const KParams p) {
       for (int z = (zs[ml] & ~7) + lane * 8; z < ze[ml]; z += 256)
         asm volatile("prefetch.global.L1 [%0];\n" ::"l"(p.rows + z));
   };
-  // Stage-1 operands of one k-step for all cells: A pre-scaled by g.
-  struct Ops {
-    double a[CELLS][MT], b[CELLS][MT];
-  };
-  auto gather = [&](const Row& rw, Ops& o) {
-    const uint32_t qa = (uint32_t)rw.q2 * 8u, qb = (uint32_t)rw.q3 * 8u;
-#pragma unroll
-    for (int cc = 0; cc < CELLS; ++cc)
-#pragma unroll
-      for (int t = 0; t < MT; ++t) {
-        o.a[cc][t] = rw.g * lds_ro(fa[t] + qa + cc * cell_bytes);
-        o.b[cc][t] = lds_ro(fb[t] + qb + cc * cell_bytes);
-      }
-  };
+  // accumulator (a = 8A + r0, b = 8B + 2kq + e) -> Phi row of pair (ml, cc)
   auto store_phi = [&](int ml, double (&acc)[CELLS][MT][MT][2]) {
 #pragma unroll
     for (int cc = 0; cc < CELLS; ++cc) {
@@ -178,117 +176,15 @@ __global__ void __launch_bounds__(256, 1) bfq_q_kernel(const KParams p) {
     }
   };
 
-  // ---- PIPE state: the warp's k-step stream over (current | next channel)
-  // slices v = 0..2*M1T-1; a cursor (v, z) names one k-step, v == 2*M1T = end.
-  constexpr int NV = 2 * M1T;
-  int zsv[NV], zev[NV];
-  struct Cur {
-    int v, z;
-  };
-  auto norm = [&](Cur c) {  // skip exhausted / empty slices
-#pragma unroll
-    for (int it = 0; it < NV; ++it)
-      if (c.v < NV && c.z >= zev[c.v]) {
-        ++c.v;
-        c.z = c.v < NV ? zsv[c.v] : 0;
-      }
-    return c;
-  };
-  auto adv = [&](Cur c) {
-    c.z += 4;
-    return norm(c);
-  };
-  auto row_at = [&](Cur c) {
-    Row r;
-    if (c.v < NV) {
-      r = load_row(p.rows, min(c.z + kq, zev[c.v] - 1));
-      if (c.z + kq >= zev[c.v]) r.g = 0.0;
-    } else {
-      r.q2 = 0;
-      r.q3 = 0;
-      r.g = 0.0;
-    }
-    return r;
-  };
-  Cur P0{0, 0}, P1{0, 0}, P2{0, 0};
-  Row r1, r2;
-  Ops cur;
-  double acc[CELLS][MT][MT][2];
-  int zs_n[M1T], ze_n[M1T];
-  Row nxt_row;
-  if constexpr (PIPE) {
-    slice_bounds(0, zsv, zev);
-    if (nch > 1) slice_bounds(1, zsv + M1T, zev + M1T);
-    else
-#pragma unroll
-      for (int v = M1T; v < NV; ++v) zsv[v] = zev[v] = 0;
-    prefetch_rows_l1(zsv, zev);
-    prefetch_rows_l1(zsv + M1T, zev + M1T);
-    P0 = norm(Cur{0, zsv[0]});
-    P1 = adv(P0);
-    P2 = adv(P1);
-    r1 = row_at(P1);
-    r2 = row_at(P2);
-    gather(row_at(P0), cur);
-#pragma unroll
-    for (int cc = 0; cc < CELLS; ++cc)
-#pragma unroll
-      for (int a = 0; a < MT; ++a)
-#pragma unroll
-        for (int b = 0; b < MT; ++b) acc[cc][a][b][0] = acc[cc][a][b][1] = 0.0;
-  } else {
-    slice_bounds(0, zs_n, ze_n);
-    prefetch_rows_l1(zs_n, ze_n);
-    nxt_row = fetch_row(p.rows, zs_n[0] + kq, ze_n[0]);
-  }
+  // slice bounds run two channels ahead (their sstart loads come from L2),
+  // the L1 row prefetch one channel ahead
+  int zs_n[M1T], ze_n[M1T], zs_nn[M1T], ze_nn[M1T];
+  slice_bounds(0, zs_n, ze_n);
+  if (nch > 1) slice_bounds(1, zs_nn, ze_nn);
+  prefetch_rows_l1(zs_n, ze_n);
+  Row nxt_row = fetch_row_bf(p.rows, zs_n[0] + kq, ze_n[0]);
 
   for (int i = 0; i < nch; ++i) {
-    if constexpr (PIPE) {
-      // ---- stage 1 (pipelined): gathers one k-step ahead, rows two ahead
-      // valid output columns without rows in this channel: Phi = 0
-#pragma unroll
-      for (int ml = 0; ml < M1T; ++ml)
-        if (m1s[ml] >= 0 && zsv[ml] >= zev[ml]) {
-          double z0[CELLS][MT][MT][2];
-#pragma unroll
-          for (int cc = 0; cc < CELLS; ++cc)
-#pragma unroll
-            for (int a = 0; a < MT; ++a)
-#pragma unroll
-              for (int b = 0; b < MT; ++b) z0[cc][a][b][0] = z0[cc][a][b][1] = 0.0;
-          store_phi(ml, z0);
-        }
-      const int zstop = (p.debug & 1) ? 0 : 1;
-      while (P0.v < M1T && zstop) {
-        Ops nxt;
-        if (P1.v < NV) gather(r1, nxt);
-        const Cur P3 = adv(P2);
-        const Row r3 = row_at(P3);
-#pragma unroll
-        for (int cc = 0; cc < CELLS; ++cc)
-#pragma unroll
-          for (int a = 0; a < MT; ++a)
-#pragma unroll
-            for (int b = 0; b < MT; ++b) dmma884(acc[cc][a][b][0], acc[cc][a][b][1], cur.a[cc][a], cur.b[cc][b]);
-        if (P1.v != P0.v) {  // last k-step of this slice
-          store_phi(P0.v, acc);
-#pragma unroll
-          for (int cc = 0; cc < CELLS; ++cc)
-#pragma unroll
-            for (int a = 0; a < MT; ++a)
-#pragma unroll
-              for (int b = 0; b < MT; ++b) acc[cc][a][b][0] = acc[cc][a][b][1] = 0.0;
-        }
-        P0 = P1;
-        P1 = P2;
-        P2 = P3;
-        r1 = r2;
-        r2 = r3;
-        cur = nxt;
-      }
-    } else {
-    const int zs_dummy = 0;
-    (void)zs_dummy;
     int zs[M1T], ze[M1T];
 #pragma unroll
     for (int ml = 0; ml < M1T; ++ml) {
@@ -296,7 +192,12 @@ __global__ void __launch_bounds__(256, 1) bfq_q_kernel(const KParams p) {
       ze[ml] = ze_n[ml];
     }
     if (i + 1 < nch) {
-      slice_bounds(i + 1, zs_n, ze_n);
+#pragma unroll
+      for (int ml = 0; ml < M1T; ++ml) {
+        zs_n[ml] = zs_nn[ml];
+        ze_n[ml] = ze_nn[ml];
+      }
+      if (i + 2 < nch) slice_bounds(i + 2, zs_nn, ze_nn);
       prefetch_rows_l1(zs_n, ze_n);
     }
     // ---- stage 1: Phi for this warp's 8 (m1, cell) pairs
@@ -314,9 +215,12 @@ __global__ void __launch_bounds__(256, 1) bfq_q_kernel(const KParams p) {
         const Row rw = nxt_row;
         // next row of the stream: this slice, else the next slice, else the
         // first slice of the next channel
-        if (z0 + 4 < ze[ml]) nxt_row = fetch_row(p.rows, z0 + 4 + kq, ze[ml]);
-        else if (ml + 1 < M1T) nxt_row = fetch_row(p.rows, zs[ml + 1 < M1T ? ml + 1 : ml] + kq, ze[ml + 1 < M1T ? ml + 1 : ml]);
-        else nxt_row = fetch_row(p.rows, zs_n[0] + kq, i + 1 < nch ? ze_n[0] : 0);
+        {  // branch-free: select the position, then one unconditional load
+          const bool same = z0 + 4 < ze[ml];
+          const int zn = ml + 1 < M1T ? zs[ml + 1 < M1T ? ml + 1 : ml] : zs_n[0];
+          const int en = ml + 1 < M1T ? ze[ml + 1 < M1T ? ml + 1 : ml] : (i + 1 < nch ? ze_n[0] : 0);
+          nxt_row = fetch_row_bf(p.rows, (same ? z0 + 4 : zn) + kq, same ? ze[ml] : en);
+        }
         const uint32_t qa = (uint32_t)rw.q2 * 8u, qb = (uint32_t)rw.q3 * 8u;
 #pragma unroll
         for (int cc = 0; cc < CELLS; ++cc) {
@@ -334,29 +238,17 @@ __global__ void __launch_bounds__(256, 1) bfq_q_kernel(const KParams p) {
       }
       // empty slice: the stream skips it, keep the prefetch pointing at the next one
       if (zs[ml] >= ze[ml]) {
-        if (ml + 1 < M1T) nxt_row = fetch_row(p.rows, zs[ml + 1 < M1T ? ml + 1 : ml] + kq, ze[ml + 1 < M1T ? ml + 1 : ml]);
-        else nxt_row = fetch_row(p.rows, zs_n[0] + kq, i + 1 < nch ? ze_n[0] : 0);
+        if (ml + 1 < M1T) nxt_row = fetch_row_bf(p.rows, zs[ml + 1 < M1T ? ml + 1 : ml] + kq, ze[ml + 1 < M1T ? ml + 1 : ml]);
+        else nxt_row = fetch_row_bf(p.rows, zs_n[0] + kq, i + 1 < nch ? ze_n[0] : 0);
       }
-      // accumulator (a = 8A + r0, b = 8B + 2kq + e) -> Phi row of the pair
-#pragma unroll
-      for (int cc = 0; cc < CELLS; ++cc) {
-        const uint32_t ph = phw_u32 + (uint32_t)((ml * CELLS + cc) * K2S) * 8u;
-#pragma unroll
-        for (int a = 0; a < MT; ++a)
-#pragma unroll
-          for (int b = 0; b < MT; ++b)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int ia = 8 * a + r0, ib = 8 * b + 2 * kq + e;
-              if (ia < NK && ib < NK) sts_v(ph + (uint32_t)(ia * NK + ib) * 8u, acc[cc][a][b][e]);
-            }
-      }
-    }
+      if (!(p.debug & 32)) store_phi(ml, acc);
     }
     __syncwarp();
+    if (clk_on) { const long long t = clock64(); ck_s1 += t - ckt; ckt = t; }
     // ---- stage 2: out[pair, k1] += Phi[pair, :] . R_tau[k1, :]
     const int s = i % NST;
     mbar_wait(&tfull[s], (unsigned)(i / NST) & 1u);
+    if (clk_on) { const long long t = clock64(); ck_w += t - ckt; ckt = t; }
     const uint32_t rb = ring_u32 + (uint32_t)(s * rblk) * 8u;
     const uint32_t pa = phw_u32 + (uint32_t)(r0 * K2S + kq) * 8u;
     auto step2 = [&](int k0) {
@@ -376,13 +268,9 @@ __global__ void __launch_bounds__(256, 1) bfq_q_kernel(const KParams p) {
     int k0 = 0;
     if (p.debug & 2) {
       k0 = K2P;
-    } else if (FIXED && !(p.debug & 4)) {
-      // compile-time K: fully unrolled, no loop back-edge (whose register
-      // reuse forces NOP padding behind the DMMAs)
-#pragma unroll
-      for (int kk = 0; kk + 8 <= (FIXED ? (NKT * NKT + 3) / 4 * 4 : 0); kk += 8) step2(kk);
-      k0 = FIXED ? (NKT * NKT + 3) / 4 * 4 / 8 * 8 : 0;
     } else {
+      // kept as a loop: a fully unrolled stage 2 lets the compiler sink the
+      // next channel's table-row load below it (exposing its L2 latency)
 #pragma unroll 2
       for (; k0 + 8 <= K2P; k0 += 8) step2(k0);
     }
@@ -392,48 +280,24 @@ __global__ void __launch_bounds__(256, 1) bfq_q_kernel(const KParams p) {
       for (int j = 0; j < MT; ++j) dmma884(acc2[j][0], acc2[j][1], av, lds_v(rb + rrow[j] + k0 * 8));
     }
     __syncwarp();
+    if (clk_on) { const long long t = clock64(); ck_s2 += t - ckt; ckt = t; }
     if (lane == 0) {
       // every lane's reads of slot s are complete (consumed by its DMMAs)
       __threadfence_block();
-      if (atomicAdd(&tarr[s], 1) == item.nunits[team] - 1) {
+      if (atomicAdd(&tarr[s], 1) == t_nunits - 1) {
         tarr[s] = 0;
-        if (i + NST < nch) issue_r(team, i + NST);
+        if (i + NST < nch) issue_r(team, i + NST, ctau[team * p.max_chan + i + NST]);
       }
     }
-    if constexpr (PIPE) {
-      if (i + 1 < nch) {
-        // slide the stream window: next channel becomes current
-        bool p0_end = P0.v >= NV, p1_end = P1.v >= NV, p2_end = P2.v >= NV;
-        if (P0.v < M1T) p0_end = p1_end = p2_end = true;  // stage 1 skipped (BFQ_DEBUG timing runs)
-#pragma unroll
-        for (int v = 0; v < M1T; ++v) {
-          zsv[v] = zsv[v + M1T];
-          zev[v] = zev[v + M1T];
-        }
-        if (i + 2 < nch) {
-          slice_bounds(i + 2, zsv + M1T, zev + M1T);
-          prefetch_rows_l1(zsv + M1T, zev + M1T);
-        } else {
-#pragma unroll
-          for (int v = M1T; v < NV; ++v) zsv[v] = zev[v] = 0;
-        }
-        if (!p0_end) P0.v -= M1T;
-        if (!p1_end) P1.v -= M1T;
-        if (!p2_end) P2.v -= M1T;
-        if (p0_end) {
-          P0 = norm(Cur{0, zsv[0]});
-          gather(row_at(P0), cur);
-        }
-        if (p1_end) {
-          P1 = adv(P0);
-          r1 = row_at(P1);
-        }
-        if (p2_end) {
-          P2 = adv(P1);
-          r2 = row_at(P2);
-        }
-      }
-    }
+    if (clk_on) { const long long t = clock64(); ck_rf += t - ckt; ckt = t; }
+  }
+  if (clk_on && lane == 0) {
+    atomicAdd(p.dbg_clk + 0, (unsigned long long)ck_s1);
+    atomicAdd(p.dbg_clk + 1, (unsigned long long)ck_w);
+    atomicAdd(p.dbg_clk + 2, (unsigned long long)ck_s2);
+    atomicAdd(p.dbg_clk + 3, (unsigned long long)ck_rf);
+    atomicAdd(p.dbg_clk + 4, (unsigned long long)(clock64() - ck0));
+    atomicAdd(p.dbg_clk + 5, 1ull);
   }
 
   // ---------------- epilogue: pair r0 = (m1 = m1s[r0/CELLS], cell = r0%CELLS)

@@ -34,3 +34,15 @@ for i in range(a.iters):
     print(f"iter {i}: {ms:.3f} ms  {a.cells / ms * 1e3:.0f} cells/s  "
           f"{plan.flops_per_cell * a.cells / ms / 1e9:.2f} alg TFLOP/s  "
           f"{2 * plan.info['exec_macs_per_cell'] * a.cells / ms / 1e9:.2f} exec TFLOP/s")
+
+if os.environ.get("BFQ_DEBUG", "0") != "0" and int(os.environ["BFQ_DEBUG"]) & 8:
+    import ctypes
+    from paper_2605_28475_b200 import _lib
+    lib = _lib.lib()
+    buf = (ctypes.c_ulonglong * 8)()
+    lib.bfq_debug_phase_clocks(buf)
+    n = max(buf[5], 1)
+    tot = buf[4]
+    names = ["stage1+flush", "wait R", "stage2", "refill", "total"]
+    print("phase cycles per warp (avg over %d warps):" % n, {k: round(buf[j] / n) for j, k in enumerate(names)})
+    print("shares:", {k: round(100.0 * buf[j] / tot, 1) for j, k in enumerate(names[:4])})
