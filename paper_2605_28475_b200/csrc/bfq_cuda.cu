@@ -102,6 +102,10 @@ __device__ __forceinline__ double lds_v(uint32_t addr) {
   return v;
 }
 
+__device__ __forceinline__ void named_bar_sync(unsigned id, unsigned count) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+
 __device__ __forceinline__ void sts_v(uint32_t addr, double v) {
   asm volatile("st.shared.f64 [%0], %1;\n" ::"r"(addr), "d"(v) : "memory");
 }
@@ -203,6 +207,7 @@ __device__ __forceinline__ Row fetch_row_clamped(const Row* rows, int z, int ze)
 
 // ------------------------------------------------------------ the Q kernel
 #include "bfq_qkernel.cuh"
+#include "bfq_qkernel2.cuh"
 
 typedef void (*QKernel)(const KParams);
 
@@ -251,6 +256,46 @@ QKernel pick_kernel(int mt, int cells, int nk, int qs) {
     if (cells == 2) return bfq_q_kernel<3, 2, BILIN, 0, 0>;
     if (cells == 1) return bfq_q_kernel<3, 1, BILIN, 0, 0>;
   }
+  return nullptr;
+}
+
+template <bool BILIN, int NK, int QS>
+QKernel pick_fixed2(int mt, int cells) {
+  constexpr int MT = (NK + 7) / 8;
+  if (mt != MT) return nullptr;
+  if constexpr (MT == 1) {
+    if (cells == 8) return bfq_q_kernel2<1, 8, BILIN, NK, QS>;
+    if (cells == 4) return bfq_q_kernel2<1, 4, BILIN, NK, QS>;
+  } else if constexpr (MT == 2) {
+    if (cells == 4) return bfq_q_kernel2<2, 4, BILIN, NK, QS>;
+    if (cells == 2) return bfq_q_kernel2<2, 2, BILIN, NK, QS>;
+  } else {
+    if (cells == 2) return bfq_q_kernel2<MT, 2, BILIN, NK, QS>;
+  }
+  return nullptr;
+}
+
+template <bool BILIN>
+QKernel pick_kernel2(int mt, int cells, int nk, int qs) {
+  QKernel k = nullptr;
+  if (!std::getenv("BFQ_GENERIC")) {
+    if (nk == 13 && qs == 172) k = pick_fixed2<BILIN, 13, 172>(mt, cells);
+    else if (nk == 9 && qs == 84) k = pick_fixed2<BILIN, 9, 84>(mt, cells);
+    else if (nk == 11 && qs == 124) k = pick_fixed2<BILIN, 11, 124>(mt, cells);
+    else if (nk == 5 && qs == 28) k = pick_fixed2<BILIN, 5, 28>(mt, cells);
+    else if (nk == 17 && qs == 292) k = pick_fixed2<BILIN, 17, 292>(mt, cells);
+    if (k) return k;
+  }
+  if (mt == 1) {
+    if (cells == 8) return bfq_q_kernel2<1, 8, BILIN, 0, 0>;
+    if (cells == 4) return bfq_q_kernel2<1, 4, BILIN, 0, 0>;
+    if (cells == 2) return bfq_q_kernel2<1, 2, BILIN, 0, 0>;
+  }
+  if (mt == 2) {
+    if (cells == 4) return bfq_q_kernel2<2, 4, BILIN, 0, 0>;
+    if (cells == 2) return bfq_q_kernel2<2, 2, BILIN, 0, 0>;
+  }
+  if (mt == 3 && cells == 2) return bfq_q_kernel2<3, 2, BILIN, 0, 0>;
   return nullptr;
 }
 
@@ -337,7 +382,11 @@ int upload_program(const Program& pg, DevProgram& dp, size_t& total, int smem_op
   if ((rc = upload(pg.groups, &dp.groups, total))) return rc;
   if ((rc = upload(pg.unit_m1, &dp.unit_m1, total))) return rc;
   if ((rc = upload(pg.items, &dp.items, total))) return rc;
-  QKernel k = pg.bilinear ? pick_kernel<true>(pg.cfg.mt, pg.cfg.cells, nk, qs) : pick_kernel<false>(pg.cfg.mt, pg.cfg.cells, nk, qs);
+  QKernel k = pg.cfg.pairsplit
+                  ? (pg.bilinear ? pick_kernel2<true>(pg.cfg.mt, pg.cfg.cells, nk, qs)
+                                 : pick_kernel2<false>(pg.cfg.mt, pg.cfg.cells, nk, qs))
+                  : (pg.bilinear ? pick_kernel<true>(pg.cfg.mt, pg.cfg.cells, nk, qs)
+                                 : pick_kernel<false>(pg.cfg.mt, pg.cfg.cells, nk, qs));
   if (!k) {
     set_error("no kernel instantiation for this tiling");
     return BFQ_EINVAL;

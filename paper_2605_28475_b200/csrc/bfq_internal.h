@@ -73,6 +73,8 @@ struct KernelConfig {
   int nf = 1;      // f arrays staged per cell (2 for bilinear Q(f2,f3))
   int smem = 0;    // dynamic shared memory bytes
   int hdr = 0;     // bytes of the barrier/counter/channel-index header
+  int pairsplit = 0;  // 1: two warps per unit (bfq_qkernel2), nw = 2 * units per CTA
+  int upc = 0;        // units per CTA
   int max_chan = 0;
 };
 

@@ -38,8 +38,8 @@ static inline int isqrt_floor(int x) {
 static int conflict_free_stride(int n) { return conflict_free_stride_dev(n); }
 
 // Shared memory of one CTA: two R rings (one per team) | Phi per warp | f of the tile.
-static long smem_bytes(int nk, int qs, int k2s, int nf, int cells, int nw, int nstage, int hdr) {
-  return hdr + 2L * nstage * nk * k2s * 8 + (long)nw * 8 * k2s * 8 + (long)nf * cells * nk * qs * 8;
+static long smem_bytes(int nk, int qs, int k2s, int nf, int cells, int units, int nstage, int hdr) {
+  return hdr + 2L * nstage * nk * k2s * 8 + (long)units * 8 * k2s * 8 + (long)nf * cells * nk * qs * 8;
 }
 
 // Header region: 8 mbarriers, 8 arrival counters, then the R-block index of
@@ -52,25 +52,48 @@ static int header_bytes(int max_chan) { return 96 + (2 * max_chan * 4 + 31) / 32
 static bool choose_config(int nk, int qs, int k2s, int nf, int smem_limit, int max_chan, KernelConfig& c) {
   c.mt = (nk + 7) / 8;
   c.nf = nf;
-  static const int opts[][3] = {  // cells, compute warps, ring stages
+  const int max_cells = c.mt == 1 ? 8 : (c.mt == 2 ? 4 : 2);  // stage-1 accumulators in registers
+  int force_cells = 0, kernel = 2;
+  if (const char* e = std::getenv("BFQ_CELLS")) force_cells = std::atoi(e);
+  if (const char* e = std::getenv("BFQ_KERNEL")) kernel = std::atoi(e);
+  c.hdr = header_bytes(max_chan);
+  c.max_chan = max_chan;
+  // Pair-split kernel first: 8 units x 2 warps (4 compute warps per
+  // scheduler) in the shared memory of 8 Phi buffers.
+  static const int popts[][3] = {{8, 8, 2}, {4, 8, 2}, {4, 8, 1}, {2, 8, 2}, {2, 8, 1}};  // cells, units, stages
+  if (kernel == 2) {
+    for (auto& o : popts) {
+      if (force_cells && o[0] != force_cells) continue;
+      if (o[0] > max_cells || o[0] < 2) continue;
+      const long smem = smem_bytes(nk, qs, k2s, nf, o[0], o[1], o[2], c.hdr);
+      if (smem > smem_limit) continue;
+      c.cells = o[0];
+      c.m1t = 8 / o[0];
+      c.upc = o[1];
+      c.nw = 2 * o[1];
+      c.nstage = o[2];
+      c.smem = (int)smem;
+      c.cg = c.cells;
+      c.pairsplit = 1;
+      return true;
+    }
+  }
+  static const int opts[][3] = {  // cells, compute warps (= units), ring stages
       {8, 8, 2}, {4, 8, 2}, {4, 8, 1}, {2, 8, 2}, {2, 8, 1}, {8, 4, 2}, {4, 4, 2}, {4, 4, 1},
       {2, 4, 2}, {2, 4, 1}, {1, 8, 1}, {1, 4, 1}, {1, 2, 1}, {1, 1, 1}};
-  int force_cells = 0;
-  if (const char* e = std::getenv("BFQ_CELLS")) force_cells = std::atoi(e);
-  const int max_cells = c.mt == 1 ? 8 : (c.mt == 2 ? 4 : 2);  // stage-1 accumulators in registers
   for (auto& o : opts) {
     if (force_cells && o[0] != force_cells) continue;
     if (o[0] > max_cells) continue;
-    c.hdr = header_bytes(max_chan);
-    c.max_chan = max_chan;
     const long smem = smem_bytes(nk, qs, k2s, nf, o[0], o[1], o[2], c.hdr);
     if (smem > smem_limit) continue;
     c.cells = o[0];
     c.m1t = 8 / o[0];
     c.nw = o[1];
+    c.upc = o[1];
     c.nstage = o[2];
     c.smem = (int)smem;
     c.cg = c.cells;
+    c.pairsplit = 0;
     return true;
   }
   return false;
@@ -152,8 +175,8 @@ static void build_items(const HostPlan& hp, Program& pg) {
     const int units = gr.n_units;
     int u = 0;
     while (u < units) {
-      if (used == c.nw || nteams == 2) flush();
-      const int take = std::min(units - u, c.nw - used);
+      if (used == c.upc || nteams == 2) flush();
+      const int take = std::min(units - u, c.upc - used);
       double w = 0.0;
       for (int uu = u; uu < u + take; ++uu) w += unit_work(gr, uu);
       cur.it.l1[nteams] = l1;

@@ -1,0 +1,292 @@
+// Pair-split variant of the fused Q(f2, f3) kernel (included by bfq_cuda.cu).
+//
+// Same algorithm, data layout and plan as bfq_qkernel.cuh, but every unit
+// (8 DMMA rows = M1T output columns x CELLS cells) is served by TWO warps:
+//   stage 1  warp h of the unit computes Phi for the cells {h*HC .. h*HC+HC-1}
+//            (HC = CELLS/2), both warps walk the same table rows (the second
+//            read hits L1),
+//   stage 2  warp h contracts its half of K = n_k^2 for all 8 pairs; the two
+//            partial accumulators are added once, in the epilogue (fixed
+//            order, deterministic).
+// With 8 units per CTA this gives 16 compute warps (4 per scheduler) in the
+// shared memory of 8 (the Phi buffer is per unit), so the 15-cycle issue
+// stall of DMMA.8x8x4 and the gather latencies are covered by other warps.
+// The two warps of a unit meet at a named barrier twice per channel (Phi
+// complete; Phi consumed).
+
+template <int MT, int CELLS, bool BILIN, int NKT, int QST>
+__global__ void __launch_bounds__(512, 1) bfq_q_kernel2(const KParams p) {
+  constexpr int M1T = 8 / CELLS;
+  constexpr int HC = CELLS / 2;  // cells per warp in stage 1
+  static_assert(CELLS >= 2, "pair split needs at least two cells per tile");
+  constexpr bool FIXED = NKT > 0;
+  constexpr int NF = BILIN ? 2 : 1;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r0 = lane >> 2, kq = lane & 3;
+  const int NK = FIXED ? NKT : p.nk;
+  const int QS = FIXED ? QST : p.qs;
+  const int K2P = FIXED ? (NKT * NKT + 3) / 4 * 4 : p.k2p;
+  const int K2S = FIXED ? conflict_free_stride_dev((NKT * NKT + 3) / 4 * 4) : p.k2s;
+  const int NST = p.nstage;
+  const int NU = p.nw / 2;  // units (Phi buffers) per CTA
+
+  const long long item_idx = (long long)blockIdx.x / p.n_tiles;
+  const long long tile = (long long)blockIdx.x - item_idx * p.n_tiles;
+  const Item item = p.items[item_idx];
+
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);  // [team*4 + stage]
+  int* arrivals = reinterpret_cast<int*>(full + 8);         // [team*4 + stage]
+  int* ctau = arrivals + 8;                                   // [team][max_chan]
+  double* rs = reinterpret_cast<double*>(smem_raw + p.hdr);
+  const int rblk = NK * K2S;
+  double* phis = rs + 2 * NST * rblk;
+  double* fs = phis + NU * 8 * K2S;
+  const int cell_elems = NK * QS;
+
+  const unsigned rbytes = (unsigned)rblk * 8u;
+  auto issue_r = [&](int t, int i, int tau) {
+    const int s = i % NST;
+    mbar_arrive_expect_tx(&full[t * 4 + s], rbytes);
+    bulk_g2s(rs + (t * NST + s) * rblk, p.R + (size_t)tau * rblk, rbytes, &full[t * 4 + s]);
+  };
+  if (threadIdx.x == 0) {
+    for (int t = 0; t < 2; ++t)
+      for (int s = 0; s < NST; ++s) {
+        mbar_init(&full[t * 4 + s], 1);
+        arrivals[t * 4 + s] = 0;
+      }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    for (int t = 0; t < 2; ++t)
+      if (item.nunits[t] > 0) {
+        const Group g = p.groups[item.l1[t]];
+        for (int i = 0; i < NST && i < g.n_chan; ++i) issue_r(t, i, p.chans[g.chan_off + i].tau);
+      }
+  }
+  for (int t = 0; t < 2; ++t)
+    if (item.nunits[t] > 0) {
+      const Group g = p.groups[item.l1[t]];
+      for (int i = threadIdx.x; i < g.n_chan; i += blockDim.x) ctau[t * p.max_chan + i] = p.chans[g.chan_off + i].tau;
+    }
+  for (int i = threadIdx.x; i < NU * 8 * K2S; i += blockDim.x) phis[i] = 0.0;
+  {
+    const int rows_total = NF * CELLS * NK;
+    const int nwarps = blockDim.x >> 5;
+    for (int row = warp; row < rows_total; row += nwarps) {
+      const int arr = row / (CELLS * NK);
+      const int rem = row - arr * CELLS * NK;
+      const int c = rem / NK, k = rem - c * NK;
+      const long long cell = tile * CELLS + c;
+      const bool ok = cell < p.n_cells;
+      const double* src = (arr == 0 ? p.f2 : p.f3) + (ok ? cell : 0) * (long long)NK * p.nq + (long long)k * p.nq;
+      double* dst = fs + (arr * CELLS + c) * cell_elems + k * QS;
+      for (int q = lane; q < p.nq; q += 32) dst[q] = ok ? __ldg(src + q) : 0.0;
+    }
+  }
+  __syncthreads();
+
+  const int u = warp >> 1, h = warp & 1;
+  const int team = u < item.nunits[0] ? 0 : 1;
+  const int tunit = team == 0 ? u : u - item.nunits[0];
+  const int t_l1 = team ? item.l1[1] : item.l1[0];
+  const int t_ubase = team ? item.ubase[1] : item.ubase[0];
+  const int t_nunits = team ? item.nunits[1] : item.nunits[0];
+  if (tunit >= t_nunits) return;  // both warps of an absent unit leave together
+  const unsigned bar_id = 1u + (unsigned)u;
+
+  const Group grp = p.groups[t_l1];
+  const int unit = t_ubase + tunit;
+  int m1s[M1T];
+#pragma unroll
+  for (int ml = 0; ml < M1T; ++ml) m1s[ml] = p.unit_m1[(grp.unit_off + unit) * M1T + ml];
+  uint64_t* tfull = full + team * 4;
+  int* tarr = arrivals + team * 4;
+  const uint32_t ring_u32 = smem_u32(rs + team * NST * rblk);
+  const uint32_t phu_u32 = smem_u32(phis + u * 8 * K2S);
+  const uint32_t cell_bytes = (uint32_t)cell_elems * 8u;
+  uint32_t fa[MT], fb[MT], rrow[MT];
+  {
+    const uint32_t f0 = smem_u32(fs) + (uint32_t)(h * HC) * cell_bytes;  // this warp's first cell
+    const uint32_t f3off = BILIN ? (uint32_t)(CELLS * cell_elems) * 8u : 0u;
+#pragma unroll
+    for (int t = 0; t < MT; ++t) {
+      const int r = min(r0 + 8 * t, NK - 1);
+      fa[t] = f0 + (uint32_t)(r * QS) * 8u;
+      fb[t] = fa[t] + f3off;
+      rrow[t] = (uint32_t)(r * K2S + kq) * 8u;
+    }
+  }
+  // stage-2 K range of this warp: k-steps [ks0, ks1) of K2P/4
+  const int nks = K2P / 4;
+  const int ks0 = h ? (nks + 1) / 2 : 0, ks1 = h ? nks : (nks + 1) / 2;
+  double acc2[MT][2], accb[MT][2];
+#pragma unroll
+  for (int j = 0; j < MT; ++j) acc2[j][0] = acc2[j][1] = accb[j][0] = accb[j][1] = 0.0;
+
+  const int nch = grp.n_chan;
+  auto slice_bounds = [&](int ci, int* zs, int* ze) {
+    const ChanEntry ce = p.chans[grp.chan_off + ci];
+#pragma unroll
+    for (int ml = 0; ml < M1T; ++ml) {
+      const int m1 = m1s[ml];
+      const bool ok = m1 >= 0;
+      zs[ml] = ok ? __ldg(p.sstart + ce.slice_base + m1) : 0;
+      ze[ml] = ok ? __ldg(p.sstart + ce.slice_base + m1 + 1) : 0;
+    }
+  };
+  auto prefetch_rows_l1 = [&](const int* zs, const int* ze) {
+    if (h) return;  // one warp of the pair is enough
+#pragma unroll
+    for (int ml = 0; ml < M1T; ++ml)
+      for (int z = (zs[ml] & ~7) + lane * 8; z < ze[ml]; z += 256)
+        asm volatile("prefetch.global.L1 [%0];\n" ::"l"(p.rows + z));
+  };
+  auto store_phi = [&](int ml, double (&acc)[HC][MT][MT][2]) {
+#pragma unroll
+    for (int cc = 0; cc < HC; ++cc) {
+      const uint32_t ph = phu_u32 + (uint32_t)((ml * CELLS + h * HC + cc) * K2S) * 8u;
+#pragma unroll
+      for (int a = 0; a < MT; ++a)
+#pragma unroll
+        for (int b = 0; b < MT; ++b)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int ia = 8 * a + r0, ib = 8 * b + 2 * kq + e;
+            if (ia < NK && ib < NK) sts_v(ph + (uint32_t)(ia * NK + ib) * 8u, acc[cc][a][b][e]);
+          }
+    }
+  };
+
+  int zs_n[M1T], ze_n[M1T], zs_nn[M1T], ze_nn[M1T];
+  slice_bounds(0, zs_n, ze_n);
+  if (nch > 1) slice_bounds(1, zs_nn, ze_nn);
+  prefetch_rows_l1(zs_n, ze_n);
+  Row nxt_row = fetch_row_bf(p.rows, zs_n[0] + kq, ze_n[0]);
+
+  for (int i = 0; i < nch; ++i) {
+    int zs[M1T], ze[M1T];
+#pragma unroll
+    for (int ml = 0; ml < M1T; ++ml) {
+      zs[ml] = zs_n[ml];
+      ze[ml] = ze_n[ml];
+    }
+    if (i + 1 < nch) {
+#pragma unroll
+      for (int ml = 0; ml < M1T; ++ml) {
+        zs_n[ml] = zs_nn[ml];
+        ze_n[ml] = ze_nn[ml];
+      }
+      if (i + 2 < nch) slice_bounds(i + 2, zs_nn, ze_nn);
+      prefetch_rows_l1(zs_n, ze_n);
+    }
+    // ---- stage 1: Phi of this warp's HC cells for the unit's M1T columns
+#pragma unroll
+    for (int ml = 0; ml < M1T; ++ml) {
+      double acc[HC][MT][MT][2];
+#pragma unroll
+      for (int cc = 0; cc < HC; ++cc)
+#pragma unroll
+        for (int a = 0; a < MT; ++a)
+#pragma unroll
+          for (int b = 0; b < MT; ++b) acc[cc][a][b][0] = acc[cc][a][b][1] = 0.0;
+      for (int z0 = zs[ml]; z0 < ze[ml]; z0 += 4) {
+        const Row rw = nxt_row;
+        {
+          const bool same = z0 + 4 < ze[ml];
+          const int zn = ml + 1 < M1T ? zs[ml + 1 < M1T ? ml + 1 : ml] : zs_n[0];
+          const int en = ml + 1 < M1T ? ze[ml + 1 < M1T ? ml + 1 : ml] : (i + 1 < nch ? ze_n[0] : 0);
+          nxt_row = fetch_row_bf(p.rows, (same ? z0 + 4 : zn) + kq, same ? ze[ml] : en);
+        }
+        const uint32_t qa = (uint32_t)rw.q2 * 8u, qb = (uint32_t)rw.q3 * 8u;
+#pragma unroll
+        for (int cc = 0; cc < HC; ++cc) {
+          double av[MT], bv[MT];
+#pragma unroll
+          for (int t = 0; t < MT; ++t) {
+            av[t] = rw.g * lds_ro(fa[t] + qa + cc * cell_bytes);
+            bv[t] = lds_ro(fb[t] + qb + cc * cell_bytes);
+          }
+#pragma unroll
+          for (int a = 0; a < MT; ++a)
+#pragma unroll
+            for (int b = 0; b < MT; ++b) dmma884(acc[cc][a][b][0], acc[cc][a][b][1], av[a], bv[b]);
+        }
+      }
+      if (zs[ml] >= ze[ml]) {
+        if (ml + 1 < M1T) nxt_row = fetch_row_bf(p.rows, zs[ml + 1 < M1T ? ml + 1 : ml] + kq, ze[ml + 1 < M1T ? ml + 1 : ml]);
+        else nxt_row = fetch_row_bf(p.rows, zs_n[0] + kq, i + 1 < nch ? ze_n[0] : 0);
+      }
+      store_phi(ml, acc);
+    }
+    named_bar_sync(bar_id, 64);  // Phi of all 8 pairs written
+    // ---- stage 2: this warp's half of K for all 8 pairs
+    const int s = i % NST;
+    mbar_wait(&tfull[s], (unsigned)(i / NST) & 1u);
+    const uint32_t rb = ring_u32 + (uint32_t)(s * rblk) * 8u;
+    const uint32_t pa = phu_u32 + (uint32_t)(r0 * K2S + kq) * 8u;
+    int ks = ks0;
+#pragma unroll 2
+    for (; ks + 2 <= ks1; ks += 2) {
+      const int k0 = ks * 4;
+      const double av0 = lds_v(pa + k0 * 8), av1 = lds_v(pa + (k0 + 4) * 8);
+      double bv0[MT], bv1[MT];
+#pragma unroll
+      for (int j = 0; j < MT; ++j) {
+        bv0[j] = lds_v(rb + rrow[j] + k0 * 8);
+        bv1[j] = lds_v(rb + rrow[j] + (k0 + 4) * 8);
+      }
+#pragma unroll
+      for (int j = 0; j < MT; ++j) {
+        dmma884(acc2[j][0], acc2[j][1], av0, bv0[j]);
+        dmma884(accb[j][0], accb[j][1], av1, bv1[j]);
+      }
+    }
+    if (ks < ks1) {
+      const int k0 = ks * 4;
+      const double av = lds_v(pa + k0 * 8);
+#pragma unroll
+      for (int j = 0; j < MT; ++j) dmma884(acc2[j][0], acc2[j][1], av, lds_v(rb + rrow[j] + k0 * 8));
+    }
+    named_bar_sync(bar_id, 64);  // Phi consumed by both warps
+    if (lane == 0) {
+      __threadfence_block();
+      if (atomicAdd(&tarr[s], 1) == 2 * t_nunits - 1) {
+        tarr[s] = 0;
+        if (i + NST < nch) issue_r(team, i + NST, ctau[team * p.max_chan + i + NST]);
+      }
+    }
+  }
+
+  // ---------------- epilogue: warp 1 hands its K-half partials to warp 0
+  const uint32_t xch = phu_u32 + (uint32_t)(lane * 2 * MT) * 8u;
+  if (h == 1) {
+#pragma unroll
+    for (int j = 0; j < MT; ++j) {
+      sts_v(xch + (uint32_t)(2 * j) * 8u, acc2[j][0] + accb[j][0]);
+      sts_v(xch + (uint32_t)(2 * j + 1) * 8u, acc2[j][1] + accb[j][1]);
+    }
+  }
+  named_bar_sync(bar_id, 64);
+  if (h == 1) return;
+  const int ml = r0 / CELLS, c = r0 - ml * CELLS;
+  int m1 = -1;
+#pragma unroll
+  for (int t = 0; t < M1T; ++t)
+    if (t == ml) m1 = m1s[t];
+  const long long cell = tile * CELLS + c;
+  if (m1 >= 0 && cell < p.n_cells) {
+    const int l1 = grp.l1, q1 = l1 * l1 + m1;
+    double* qc = p.q + cell * (long long)NK * p.nq + q1;
+#pragma unroll
+    for (int j = 0; j < MT; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int k1 = 8 * j + 2 * kq + e;
+        if (k1 < NK) {
+          double v = (acc2[j][e] + accb[j][e]) + lds_v(xch + (uint32_t)(2 * j + e) * 8u);
+          if (p.conservation && ((k1 == 0 && l1 <= 1) || (k1 == 1 && l1 == 0))) v = 0.0;
+          qc[(size_t)k1 * p.nq] = v;
+        }
+      }
+  }
+}
