@@ -297,9 +297,9 @@ def run_ours(args, rank, world, local_rank):
     traffic = None
     tpath = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
     if os.path.exists(tpath):
-        try:
-            traffic = json.load(open(tpath)).get("bytes_per_launch")
-        except (OSError, ValueError):
+        try:  # ncu dram bytes per cell of the same kernel, scaled to this launch
+            traffic = json.load(open(tpath))["dram_bytes_per_cell"] * n_cells
+        except (OSError, ValueError, KeyError):
             traffic = None
     line = {
         "metric": METRIC, "value": value, "unit": "cells/s", "n_gpus": world, "steps": args.steps,

@@ -94,6 +94,15 @@ __global__ void __launch_bounds__(512, 1) bfq_q_kernel2(const KParams p) {
   if (tunit >= t_nunits) return;  // both warps of an absent unit leave together
   const unsigned bar_id = 1u + (unsigned)u;
 
+  const bool clk_on = (p.debug & 8) != 0;
+  long long ck_s1 = 0, ck_b1 = 0, ck_w = 0, ck_s2 = 0, ck_b2 = 0, ck0 = clock64(), ckt = ck0;
+  auto tick = [&](long long& acc) {
+    if (clk_on) {
+      const long long t = clock64();
+      acc += t - ckt;
+      ckt = t;
+    }
+  };
   const Group grp = p.groups[t_l1];
   const int unit = t_ubase + tunit;
   int m1s[M1T];
@@ -218,10 +227,13 @@ __global__ void __launch_bounds__(512, 1) bfq_q_kernel2(const KParams p) {
       }
       store_phi(ml, acc);
     }
+    tick(ck_s1);
     named_bar_sync(bar_id, 64);  // Phi of all 8 pairs written
+    tick(ck_b1);
     // ---- stage 2: this warp's half of K for all 8 pairs
     const int s = i % NST;
     mbar_wait(&tfull[s], (unsigned)(i / NST) & 1u);
+    tick(ck_w);
     const uint32_t rb = ring_u32 + (uint32_t)(s * rblk) * 8u;
     const uint32_t pa = phu_u32 + (uint32_t)(r0 * K2S + kq) * 8u;
     int ks = ks0;
@@ -247,7 +259,9 @@ __global__ void __launch_bounds__(512, 1) bfq_q_kernel2(const KParams p) {
 #pragma unroll
       for (int j = 0; j < MT; ++j) dmma884(acc2[j][0], acc2[j][1], av, lds_v(rb + rrow[j] + k0 * 8));
     }
+    tick(ck_s2);
     named_bar_sync(bar_id, 64);  // Phi consumed by both warps
+    tick(ck_b2);
     if (lane == 0) {
       __threadfence_block();
       if (atomicAdd(&tarr[s], 1) == 2 * t_nunits - 1) {
@@ -257,6 +271,15 @@ __global__ void __launch_bounds__(512, 1) bfq_q_kernel2(const KParams p) {
     }
   }
 
+  if (clk_on && lane == 0) {
+    atomicAdd(p.dbg_clk + 0, (unsigned long long)ck_s1);
+    atomicAdd(p.dbg_clk + 1, (unsigned long long)ck_b1);
+    atomicAdd(p.dbg_clk + 2, (unsigned long long)ck_w);
+    atomicAdd(p.dbg_clk + 3, (unsigned long long)ck_s2);
+    atomicAdd(p.dbg_clk + 4, (unsigned long long)ck_b2);
+    atomicAdd(p.dbg_clk + 5, (unsigned long long)(clock64() - ck0));
+    atomicAdd(p.dbg_clk + 6, 1ull);
+  }
   // ---------------- epilogue: warp 1 hands its K-half partials to warp 0
   const uint32_t xch = phu_u32 + (uint32_t)(lane * 2 * MT) * 8u;
   if (h == 1) {

@@ -41,8 +41,12 @@ if os.environ.get("BFQ_DEBUG", "0") != "0" and int(os.environ["BFQ_DEBUG"]) & 8:
     lib = _lib.lib()
     buf = (ctypes.c_ulonglong * 8)()
     lib.bfq_debug_phase_clocks(buf)
-    n = max(buf[5], 1)
-    tot = buf[4]
-    names = ["stage1+flush", "wait R", "stage2", "refill", "total"]
+    if plan.info["warps_per_cta"] == 16:  # pair-split kernel
+        names = ["stage1", "bar1", "wait R", "stage2", "bar2", "total"]
+        n = max(buf[6], 1)
+    else:
+        names = ["stage1+flush", "wait R", "stage2", "refill", "total"]
+        n = max(buf[5], 1)
+    tot = buf[len(names) - 1]
     print("phase cycles per warp (avg over %d warps):" % n, {k: round(buf[j] / n) for j, k in enumerate(names)})
-    print("shares:", {k: round(100.0 * buf[j] / tot, 1) for j, k in enumerate(names[:4])})
+    print("shares:", {k: round(100.0 * buf[j] / max(tot, 1), 1) for j, k in enumerate(names[:-1])})
