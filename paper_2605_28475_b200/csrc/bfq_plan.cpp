@@ -61,8 +61,11 @@ static bool choose_config(int nk, int qs, int k2s, int nf, int smem_limit, int m
   // Pair-split kernel first: 8 units x 2 warps (4 compute warps per
   // scheduler) in the shared memory of 8 Phi buffers.
   static const int popts[][3] = {{8, 8, 2}, {4, 8, 2}, {4, 8, 1}, {2, 8, 2}, {2, 8, 1}};  // cells, units, stages
+  int force_stages = 0;
+  if (const char* e = std::getenv("BFQ_STAGES")) force_stages = std::atoi(e);
   if (kernel == 2) {
-    for (auto& o : popts) {
+    for (auto o0 : popts) {
+      int o[3] = {o0[0], o0[1], force_stages ? force_stages : o0[2]};
       if (force_cells && o[0] != force_cells) continue;
       if (o[0] > max_cells || o[0] < 2) continue;
       const long smem = smem_bytes(nk, qs, k2s, nf, o[0], o[1], o[2], c.hdr);

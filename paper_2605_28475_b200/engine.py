@@ -41,6 +41,7 @@ __all__ = [
     "evaluate",
     "STRATEGIES",
     "register_with_reference",
+    "linearize",
 ]
 
 
@@ -303,6 +304,37 @@ def q_gpu(op, c, c2=None, stats=None):
     q = evaluate_batch(plan, f, f3)[0].cpu().numpy()
     _record(stats, op, time.perf_counter() - t0)
     return type(c)(q, c.cfg)
+
+
+def linearize(op, c_eq, device: int | None = None, chunk: int = 4096) -> np.ndarray:
+    """Jacobian of Q at ``c_eq`` as a dense (n_dof, n_dof) matrix, on the GPU.
+
+    Same result as the reference's ``linearize`` (contraction.py:343-369):
+    column beta is dQ/dc_beta = Q(c_eq, e_beta) + Q(e_beta, c_eq) (slot-3 and
+    slot-2 derivatives, the t3 / t2 terms of :360-368), evaluated as two
+    batched bilinear launches with one basis vector e_beta per cell.
+    """
+    import torch
+
+    plan = plan_for(op, device)
+    dev = torch.device("cuda", plan.device)
+    cfg = op.cfg
+    n_dof = cfg.n_dof
+    vals = np.ascontiguousarray(c_eq.values if hasattr(c_eq, "values") else c_eq, dtype=np.float64)
+    if vals.shape != (cfg.n_k, cfg.n_q):
+        raise ValueError("coefficient field does not match the operator")
+    base = torch.from_numpy(vals).to(dev)
+    jac_t = torch.empty((n_dof, n_dof), dtype=torch.float64, device=dev)  # row beta = column beta of J
+    for b0 in range(0, n_dof, chunk):
+        nb = min(chunk, n_dof - b0)
+        e = torch.zeros((nb, n_dof), dtype=torch.float64, device=dev)
+        e[torch.arange(nb, device=dev), torch.arange(b0, b0 + nb, device=dev)] = 1.0
+        e = e.view(nb, cfg.n_k, cfg.n_q)
+        c = base.expand(nb, cfg.n_k, cfg.n_q).contiguous()
+        q3 = evaluate_batch(plan, c, e)  # Q(c_eq, e_beta): derivative through slot 3
+        q2 = evaluate_batch(plan, e, c)  # Q(e_beta, c_eq): derivative through slot 2
+        jac_t[b0:b0 + nb] = (q3 + q2).view(nb, n_dof)
+    return jac_t.t().contiguous().cpu().numpy()
 
 
 STRATEGIES = {"gpu": q_gpu}

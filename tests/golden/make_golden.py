@@ -26,7 +26,7 @@ sys.path.insert(0, str(REPO))
 
 from boltzfact import cache as ref_cache  # noqa: E402
 from boltzfact.basis import CoefficientField, SpectralConfig, project  # noqa: E402
-from boltzfact.contraction import evaluate, q_angular_first, q_naive  # noqa: E402
+from boltzfact.contraction import evaluate, linearize, q_angular_first, q_naive  # noqa: E402
 
 sys.path.insert(0, "/root/reference/pkg/tests")
 from oracles import maxwell_eigenvalue_ref  # noqa: E402
@@ -66,8 +66,13 @@ def one(name: str, n_uni: int, n_pm: int) -> None:
     c1 = inputs.uniform_fields(cfg.n_k, cfg.l_max, 1, seed=11)[0]
     c2 = inputs.uniform_fields(cfg.n_k, cfg.l_max, 1, seed=12)[0]
     q12 = q_angular_first(op, CoefficientField(c1, cfg), CoefficientField(c2, cfg)).values
+    extra = {}
+    if cfg.n_dof <= 300:  # reference linearize (contraction.py:343-369) at equilibrium and a perturbed state
+        extra["jac_eq"] = linearize(op, CoefficientField.equilibrium(cfg))
+        extra["jac_c"] = cells[n_uni]
+        extra["jac_pm"] = linearize(op, CoefficientField(cells[n_uni].copy(), cfg))
     np.savez_compressed(OUT / f"{name}.npz", cells=cells, q=q, q_naive0=qn, c1=c1, c2=c2, q12=q12,
-                        k_max=cfg.k_max, l_max=cfg.l_max, gamma=cfg.gamma)
+                        k_max=cfg.k_max, l_max=cfg.l_max, gamma=cfg.gamma, **extra)
     print(f"{name}: {cells.shape[0]} cells, max|Q| {np.abs(q).max():.3e}")
 
 

@@ -260,3 +260,25 @@ def test_hs12_headline_operator():
     for i in (0, 1, 511, 1024, 2047):
         ref = q_oracle.q_angular_first(oop, cells[i], r_slices=rs)
         assert q_oracle.rel_err(q[i], ref) <= TOL, i
+
+
+@pytest.mark.parametrize("name", ["hs_n2", "mm_n4", "mm_k4l6", "hs_k4l6"])
+def test_linearize_matches_reference(name):
+    """Batched GPU Jacobian vs the reference's linearize (contraction.py:343-369)."""
+    op, d = load_op(name), golden(name)
+    if "jac_eq" not in d:
+        pytest.skip("no reference Jacobian in the golden file")
+    cfg = op.cfg
+    eq = CoefficientField.equilibrium(cfg)
+    j_eq = engine.linearize(op, eq)
+    assert q_oracle.rel_err(j_eq, d["jac_eq"]) <= 1e-12
+    j_pm = engine.linearize(op, CoefficientField(d["jac_c"].copy(), cfg))
+    assert q_oracle.rel_err(j_pm, d["jac_pm"]) <= 1e-12
+    # structure at equilibrium (test_contraction.py:133-147): block-diagonal in q, 5 invariants
+    blocks = j_eq.reshape(cfg.n_k, cfg.n_q, cfg.n_k, cfg.n_q).copy()
+    for qq in range(cfg.n_q):
+        blocks[:, qq, :, qq] = 0.0
+    assert np.abs(blocks).max() == 0.0
+    if name == "hs_k4l6":
+        lam = np.linalg.eigvals(j_eq)
+        assert int(np.sum(np.abs(lam) < 1e-12)) == 5
