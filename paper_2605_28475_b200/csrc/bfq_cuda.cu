@@ -27,6 +27,7 @@
 #include <new>
 #include <string>
 #include <vector>
+#include <type_traits>
 
 #include "bfq_internal.h"
 
@@ -70,7 +71,7 @@ struct KParams {
   const Group* groups;
   const int16_t* unit_m1;
   const Item* items;
-  int nk, nq, qs, k2s, k2p;
+  int nk, nq, qs, k2s, k2p, k2sd, k2pd;
   int cells, m1t, nw, nstage;
   int conservation;
   int hdr, max_chan;
@@ -431,6 +432,8 @@ int launch_q(const bfq_plan* plan, const DevProgram& dp, const double* f2, const
   p.qs = hp.qs;
   p.k2s = hp.k2s;
   p.k2p = hp.k2p;
+  p.k2sd = hp.k2sd;
+  p.k2pd = hp.k2pd;
   p.cells = dp.cfg.cells;
   p.m1t = dp.cfg.m1t;
   p.nw = dp.cfg.nw;

@@ -37,7 +37,7 @@ struct alignas(16) ChanEntry {
   int32_t tau;         // R block index (0-based channel)
   int32_t slice_base;  // index into the expanded slice-start table; slice of m1 = base + m1
   int32_t weight2;     // 1: contribution doubled (fold, l2 < l3); resolved at plan time into a scaled R copy
-  int32_t pad;
+  int32_t diag;        // 1: self-symmetric channel (l2 == l3), R block packed as the upper triangle
 };
 
 // Output-degree group: all channels sharing l1, i.e. one set of output columns.
@@ -96,6 +96,8 @@ struct HostPlan {
   int qs = 0;   // smem row stride of f (doubles)
   int k2p = 0;  // n_k^2 rounded up to 4 (stage-2 K extent)
   int k2s = 0;  // row stride of Phi and R blocks (doubles)
+  int k2pd = 0; // packed upper-triangle K of self-symmetric channels, rounded up to 4
+  int k2sd = 0; // its row stride
   bool conservation = false, detailed_balance = false;
   bool folded = false;  // slot symmetry verified -> Q(f,f) uses the folded program
   std::vector<int32_t> triplets;  // [n_t*3]

@@ -277,6 +277,8 @@ int build_host_plan(const bfq_desc& d, int smem_limit, HostPlan& hp) {
   hp.qs = conflict_free_stride(nq);
   hp.k2p = (nk * nk + 3) / 4 * 4;
   hp.k2s = conflict_free_stride(hp.k2p);
+  hp.k2pd = (nk * (nk + 1) / 2 + 3) / 4 * 4;
+  hp.k2sd = conflict_free_stride(hp.k2pd);
 
   // channel table (angular.py:119-135)
   hp.triplets.assign(d.triplets, d.triplets + 3 * (size_t)d.n_t);
@@ -424,7 +426,45 @@ int build_host_plan(const bfq_desc& d, int smem_limit, HostPlan& hp) {
     ce.tau = (int32_t)nb;
     ce.weight2 = 0;
   }
+  // Self-symmetric folded channels (l2 == l3, their own swap partner): Phi and
+  // R are symmetric in (a, b), so the pair-split kernel contracts only the
+  // upper triangle a <= b, with R packed as R'[k1][p(a,b)] = (a<b ? 2 : 1) R.
+  if (hp.folded && hp.sym.cfg.pairsplit && !std::getenv("BFQ_NO_DIAG")) {
+    for (ChanEntry& ce : hp.sym.chans) {
+      const int t = ce.tau < d.n_t ? ce.tau : -1;
+      if (t < 0 || hp.triplets[3 * t + 1] != hp.triplets[3 * t + 2]) continue;
+      const size_t nb = hp.rblocks.size() / blk;
+      hp.rblocks.resize((nb + 1) * blk, 0.0);
+      for (int k1 = 0; k1 < nk; ++k1) {
+        int pidx = 0;
+        for (int a = 0; a < nk; ++a)
+          for (int b = a; b < nk; ++b, ++pidx)
+            hp.rblocks[nb * blk + (size_t)k1 * hp.k2sd + pidx] =
+                (a < b ? 2.0 : 1.0) * hp.rblocks[(size_t)t * blk + (size_t)k1 * hp.k2s + a * nk + b];
+      }
+      ce.tau = (int32_t)nb;
+      ce.diag = 1;
+    }
+  }
 
+  // executed DMMA MACs per cell of the Q(f,f) program (after the diag packing)
+  {
+    const Program& pg = hp.sym;
+    const KernelConfig& c = pg.cfg;
+    double total = 0.0;
+    for (const Group& gr : pg.groups) {
+      for (int e = 0; e < gr.n_chan; ++e) {
+        const ChanEntry& ce = pg.chans[gr.chan_off + e];
+        const double tiles = ce.diag ? c.mt * (c.mt + 1) / 2 : c.mt * c.mt;
+        for (int m1 = 0; m1 < gr.d1; ++m1) {
+          const int rows = hp.sstart[ce.slice_base + m1 + 1] - hp.sstart[ce.slice_base + m1];
+          total += tiles * 256.0 * ((rows + 3) / 4);  // per cell
+        }
+        total += (double)gr.n_units * c.mt * 256.0 * ((ce.diag ? hp.k2pd : hp.k2p) / 4) / c.cells;
+      }
+    }
+    hp.sym.exec_macs_per_cell = total;
+  }
   hp.alg_flops_per_cell = 2.0 * ((double)d.n_g * nk * nk + (double)d.n_s * nk * nk * nk);
   hp.alg_bytes_per_cell = 16.0 * nk * nq;
   return BFQ_OK;

@@ -28,6 +28,9 @@ __global__ void __launch_bounds__(512, 1) bfq_q_kernel2(const KParams p) {
   const int QS = FIXED ? QST : p.qs;
   const int K2P = FIXED ? (NKT * NKT + 3) / 4 * 4 : p.k2p;
   const int K2S = FIXED ? conflict_free_stride_dev((NKT * NKT + 3) / 4 * 4) : p.k2s;
+  // packed upper triangle of self-symmetric (diag) channels
+  const int K2PD = FIXED ? (NKT * (NKT + 1) / 2 + 3) / 4 * 4 : p.k2pd;
+  const int K2SD = FIXED ? conflict_free_stride_dev((NKT * (NKT + 1) / 2 + 3) / 4 * 4) : p.k2sd;
   const int NST = p.nstage;
   const int NU = p.nw / 2;  // units (Phi buffers) per CTA
 
@@ -44,11 +47,12 @@ __global__ void __launch_bounds__(512, 1) bfq_q_kernel2(const KParams p) {
   double* fs = phis + NU * 8 * K2S;
   const int cell_elems = NK * QS;
 
-  const unsigned rbytes = (unsigned)rblk * 8u;
-  auto issue_r = [&](int t, int i, int tau) {
+  // ctau[t][i] = 2 * R-block index + diag; diag blocks are shorter (packed K)
+  auto issue_r = [&](int t, int i, int code) {
     const int s = i % NST;
-    mbar_arrive_expect_tx(&full[t * 4 + s], rbytes);
-    bulk_g2s(rs + (t * NST + s) * rblk, p.R + (size_t)tau * rblk, rbytes, &full[t * 4 + s]);
+    const unsigned bytes = (unsigned)(NK * ((code & 1) ? K2SD : K2S)) * 8u;
+    mbar_arrive_expect_tx(&full[t * 4 + s], bytes);
+    bulk_g2s(rs + (t * NST + s) * rblk, p.R + (size_t)(code >> 1) * rblk, bytes, &full[t * 4 + s]);
   };
   if (threadIdx.x == 0) {
     for (int t = 0; t < 2; ++t)
@@ -60,13 +64,19 @@ __global__ void __launch_bounds__(512, 1) bfq_q_kernel2(const KParams p) {
     for (int t = 0; t < 2; ++t)
       if (item.nunits[t] > 0) {
         const Group g = p.groups[item.l1[t]];
-        for (int i = 0; i < NST && i < g.n_chan; ++i) issue_r(t, i, p.chans[g.chan_off + i].tau);
+        for (int i = 0; i < NST && i < g.n_chan; ++i) {
+          const ChanEntry ce = p.chans[g.chan_off + i];
+          issue_r(t, i, 2 * ce.tau + ce.diag);
+        }
       }
   }
   for (int t = 0; t < 2; ++t)
     if (item.nunits[t] > 0) {
       const Group g = p.groups[item.l1[t]];
-      for (int i = threadIdx.x; i < g.n_chan; i += blockDim.x) ctau[t * p.max_chan + i] = p.chans[g.chan_off + i].tau;
+      for (int i = threadIdx.x; i < g.n_chan; i += blockDim.x) {
+        const ChanEntry ce = p.chans[g.chan_off + i];
+        ctau[t * p.max_chan + i] = 2 * ce.tau + ce.diag;
+      }
     }
   for (int i = threadIdx.x; i < NU * 8 * K2S; i += blockDim.x) phis[i] = 0.0;
   {
@@ -113,7 +123,7 @@ __global__ void __launch_bounds__(512, 1) bfq_q_kernel2(const KParams p) {
   const uint32_t ring_u32 = smem_u32(rs + team * NST * rblk);
   const uint32_t phu_u32 = smem_u32(phis + u * 8 * K2S);
   const uint32_t cell_bytes = (uint32_t)cell_elems * 8u;
-  uint32_t fa[MT], fb[MT], rrow[MT];
+  uint32_t fa[MT], fb[MT], rrow[MT], rrowd[MT];
   {
     const uint32_t f0 = smem_u32(fs) + (uint32_t)(h * HC) * cell_bytes;  // this warp's first cell
     const uint32_t f3off = BILIN ? (uint32_t)(CELLS * cell_elems) * 8u : 0u;
@@ -123,11 +133,9 @@ __global__ void __launch_bounds__(512, 1) bfq_q_kernel2(const KParams p) {
       fa[t] = f0 + (uint32_t)(r * QS) * 8u;
       fb[t] = fa[t] + f3off;
       rrow[t] = (uint32_t)(r * K2S + kq) * 8u;
+      rrowd[t] = (uint32_t)(r * K2SD + kq) * 8u;
     }
   }
-  // stage-2 K range of this warp: k-steps [ks0, ks1) of K2P/4
-  const int nks = K2P / 4;
-  const int ks0 = h ? (nks + 1) / 2 : 0, ks1 = h ? nks : (nks + 1) / 2;
   double acc2[MT][2], accb[MT][2];
 #pragma unroll
   for (int j = 0; j < MT; ++j) acc2[j][0] = acc2[j][1] = accb[j][0] = accb[j][1] = 0.0;
@@ -150,7 +158,7 @@ __global__ void __launch_bounds__(512, 1) bfq_q_kernel2(const KParams p) {
       for (int z = (zs[ml] & ~7) + lane * 8; z < ze[ml]; z += 256)
         asm volatile("prefetch.global.L1 [%0];\n" ::"l"(p.rows + z));
   };
-  auto store_phi = [&](int ml, double (&acc)[HC][MT][MT][2]) {
+  auto store_phi = [&](int ml, double (&acc)[HC][MT][MT][2], bool dg) {
 #pragma unroll
     for (int cc = 0; cc < HC; ++cc) {
       const uint32_t ph = phu_u32 + (uint32_t)((ml * CELLS + h * HC + cc) * K2S) * 8u;
@@ -161,7 +169,13 @@ __global__ void __launch_bounds__(512, 1) bfq_q_kernel2(const KParams p) {
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int ia = 8 * a + r0, ib = 8 * b + 2 * kq + e;
-            if (ia < NK && ib < NK) sts_v(ph + (uint32_t)(ia * NK + ib) * 8u, acc[cc][a][b][e]);
+            if (!dg) {
+              if (ia < NK && ib < NK) sts_v(ph + (uint32_t)(ia * NK + ib) * 8u, acc[cc][a][b][e]);
+            } else if (a <= b && ia <= ib && ib < NK) {
+              // packed upper triangle p(a,b) = a*NK - a(a-1)/2 + (b - a)
+              const int pidx = ia * NK - (ia * (ia - 1)) / 2 + (ib - ia);
+              sts_v(ph + (uint32_t)pidx * 8u, acc[cc][a][b][e]);
+            }
           }
     }
   };
@@ -188,6 +202,9 @@ __global__ void __launch_bounds__(512, 1) bfq_q_kernel2(const KParams p) {
       if (i + 2 < nch) slice_bounds(i + 2, zs_nn, ze_nn);
       prefetch_rows_l1(zs_n, ze_n);
     }
+    const bool dg = (ctau[team * p.max_chan + i] & 1) != 0;
+    auto stage1 = [&](auto dgtag) {
+      constexpr bool DGC = decltype(dgtag)::value;
     // ---- stage 1: Phi of this warp's HC cells for the unit's M1T columns
 #pragma unroll
     for (int ml = 0; ml < M1T; ++ml) {
@@ -218,15 +235,19 @@ __global__ void __launch_bounds__(512, 1) bfq_q_kernel2(const KParams p) {
 #pragma unroll
           for (int a = 0; a < MT; ++a)
 #pragma unroll
-            for (int b = 0; b < MT; ++b) dmma884(acc[cc][a][b][0], acc[cc][a][b][1], av[a], bv[b]);
+            for (int b = 0; b < MT; ++b)
+              if (b >= a || !DGC) dmma884(acc[cc][a][b][0], acc[cc][a][b][1], av[a], bv[b]);
         }
       }
       if (zs[ml] >= ze[ml]) {
         if (ml + 1 < M1T) nxt_row = fetch_row_bf(p.rows, zs[ml + 1 < M1T ? ml + 1 : ml] + kq, ze[ml + 1 < M1T ? ml + 1 : ml]);
         else nxt_row = fetch_row_bf(p.rows, zs_n[0] + kq, i + 1 < nch ? ze_n[0] : 0);
       }
-      store_phi(ml, acc);
+      store_phi(ml, acc, DGC);
     }
+    };
+    if (dg) stage1(std::true_type{});
+    else stage1(std::false_type{});
     tick(ck_s1);
     named_bar_sync(bar_id, 64);  // Phi of all 8 pairs written
     tick(ck_b1);
@@ -236,6 +257,14 @@ __global__ void __launch_bounds__(512, 1) bfq_q_kernel2(const KParams p) {
     tick(ck_w);
     const uint32_t rb = ring_u32 + (uint32_t)(s * rblk) * 8u;
     const uint32_t pa = phu_u32 + (uint32_t)(r0 * K2S + kq) * 8u;
+    auto stage2 = [&](auto dgtag) {
+      constexpr bool DGC = decltype(dgtag)::value;
+    // this warp's half of the k-steps (K = n_k^2, or the packed triangle)
+    const int nks = (DGC ? K2PD : K2P) / 4;
+    const int ks0 = h ? (nks + 1) / 2 : 0, ks1 = h ? nks : (nks + 1) / 2;
+    uint32_t rr[MT];
+#pragma unroll
+    for (int j = 0; j < MT; ++j) rr[j] = DGC ? rrowd[j] : rrow[j];
     int ks = ks0;
 #pragma unroll 2
     for (; ks + 2 <= ks1; ks += 2) {
@@ -244,8 +273,8 @@ __global__ void __launch_bounds__(512, 1) bfq_q_kernel2(const KParams p) {
       double bv0[MT], bv1[MT];
 #pragma unroll
       for (int j = 0; j < MT; ++j) {
-        bv0[j] = lds_v(rb + rrow[j] + k0 * 8);
-        bv1[j] = lds_v(rb + rrow[j] + (k0 + 4) * 8);
+        bv0[j] = lds_v(rb + rr[j] + k0 * 8);
+        bv1[j] = lds_v(rb + rr[j] + (k0 + 4) * 8);
       }
 #pragma unroll
       for (int j = 0; j < MT; ++j) {
@@ -257,8 +286,11 @@ __global__ void __launch_bounds__(512, 1) bfq_q_kernel2(const KParams p) {
       const int k0 = ks * 4;
       const double av = lds_v(pa + k0 * 8);
 #pragma unroll
-      for (int j = 0; j < MT; ++j) dmma884(acc2[j][0], acc2[j][1], av, lds_v(rb + rrow[j] + k0 * 8));
+      for (int j = 0; j < MT; ++j) dmma884(acc2[j][0], acc2[j][1], av, lds_v(rb + rr[j] + k0 * 8));
     }
+    };
+    if (dg) stage2(std::true_type{});
+    else stage2(std::false_type{});
     tick(ck_s2);
     named_bar_sync(bar_id, 64);  // Phi consumed by both warps
     tick(ck_b2);
