@@ -74,7 +74,7 @@ struct KParams {
   int nk, nq, qs, k2s, k2p, k2sd, k2pd;
   int cells, m1t, nw, nstage;
   int conservation;
-  int hdr, max_chan;
+  int hdr, max_chan, nteams;
   int debug;  // timing experiments only (BFQ_DEBUG): bit0 skip stage 1, bit1 skip stage 2, bit3 phase clocks
   unsigned long long* dbg_clk;  // [8] phase cycle totals when bit3 set
 };
@@ -441,6 +441,7 @@ int launch_q(const bfq_plan* plan, const DevProgram& dp, const double* f2, const
   p.conservation = hp.conservation ? 1 : 0;
   p.hdr = dp.cfg.hdr;
   p.max_chan = dp.cfg.max_chan;
+  p.nteams = dp.cfg.nteams;
   {
     static const int dbg = std::getenv("BFQ_DEBUG") ? std::atoi(std::getenv("BFQ_DEBUG")) : 0;
     p.debug = dbg;

@@ -51,15 +51,16 @@ struct alignas(16) Group {
   int32_t pad[2];
 };
 
-// One CTA's work inside a cell tile: up to two "teams" of compute warps, each
-// walking the channel list of one l1 group in lockstep behind its own R ring.
-// Team t owns units [ubase[t], ubase[t] + nunits[t]) of group l1[t]; warps
-// 0..nunits[0]-1 form team 0, the next nunits[1] warps team 1.
+// One CTA's work inside a cell tile: up to MAX_TEAMS "teams" of units, each
+// team walking the channel list of one l1 group in lockstep behind its own R
+// ring.  Team t owns units [ubase[t], ubase[t] + nunits[t]) of group l1[t];
+// the CTA's unit slots are assigned to teams in order.
+constexpr int MAX_TEAMS = 4;
 struct alignas(16) Item {
-  int32_t l1[2];
-  int32_t ubase[2];
-  int32_t nunits[2];
-  int32_t pad[2];
+  int32_t l1[MAX_TEAMS];
+  int32_t ubase[MAX_TEAMS];
+  int32_t nunits[MAX_TEAMS];
+  int32_t pad[MAX_TEAMS];
 };
 
 // Kernel shape chosen at plan time for one program (folded or full).
@@ -74,6 +75,7 @@ struct KernelConfig {
   int smem = 0;    // dynamic shared memory bytes
   int hdr = 0;     // bytes of the barrier/counter/channel-index header
   int pairsplit = 0;  // 1: two warps per unit (bfq_qkernel2), nw = 2 * units per CTA
+  int nteams = 2;     // R rings (l1 groups) per CTA, <= MAX_TEAMS
   int upc = 0;        // units per CTA
   int max_chan = 0;
 };

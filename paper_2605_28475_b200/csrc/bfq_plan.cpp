@@ -38,13 +38,13 @@ static inline int isqrt_floor(int x) {
 static int conflict_free_stride(int n) { return conflict_free_stride_dev(n); }
 
 // Shared memory of one CTA: two R rings (one per team) | Phi per warp | f of the tile.
-static long smem_bytes(int nk, int qs, int k2s, int nf, int cells, int units, int nstage, int hdr) {
-  return hdr + 2L * nstage * nk * k2s * 8 + (long)units * 8 * k2s * 8 + (long)nf * cells * nk * qs * 8;
+static long smem_bytes(int nk, int qs, int k2s, int nf, int cells, int units, int nstage, int hdr, int nteams) {
+  return hdr + (long)nteams * nstage * nk * k2s * 8 + (long)units * 8 * k2s * 8 + (long)nf * cells * nk * qs * 8;
 }
 
 // Header region: 8 mbarriers, 8 arrival counters, then the R-block index of
 // every channel of both teams (the refill path reads it from shared memory).
-static int header_bytes(int max_chan) { return 96 + (2 * max_chan * 4 + 31) / 32 * 32; }
+static int header_bytes(int max_chan) { return 96 + (MAX_TEAMS * max_chan * 4 + 31) / 32 * 32; }
 
 // DMMA.8x8x4 issues with a ~15-cycle stall on its warp, so a scheduler needs
 // at least two compute warps to keep the FP64 tensor pipe fed while the other
@@ -59,22 +59,29 @@ static bool choose_config(int nk, int qs, int k2s, int nf, int smem_limit, int m
   c.hdr = header_bytes(max_chan);
   c.max_chan = max_chan;
   // Pair-split kernel first: 8 units x 2 warps (4 compute warps per
-  // scheduler) in the shared memory of 8 Phi buffers.
-  static const int popts[][3] = {{8, 8, 2}, {4, 8, 2}, {4, 8, 1}, {2, 8, 2}, {2, 8, 1}};  // cells, units, stages
-  int force_stages = 0;
+  // scheduler) in the shared memory of 8 Phi buffers.  R rings: up to 4 teams
+  // with one stage each (measured as fast as two stages: the refill has a
+  // whole stage 1 to land), else 2 teams.
+  static const int popts[][4] = {  // cells, units, stages, teams
+      {8, 8, 1, 4}, {8, 8, 2, 2}, {4, 8, 1, 4}, {4, 8, 2, 2}, {4, 8, 1, 2},
+      {2, 8, 1, 4}, {2, 8, 2, 2}, {2, 8, 1, 2}};
+  int force_stages = 0, force_teams = 0;
   if (const char* e = std::getenv("BFQ_STAGES")) force_stages = std::atoi(e);
+  if (const char* e = std::getenv("BFQ_TEAMS")) force_teams = std::atoi(e);
   if (kernel == 2) {
     for (auto o0 : popts) {
-      int o[3] = {o0[0], o0[1], force_stages ? force_stages : o0[2]};
+      int o[4] = {o0[0], o0[1], force_stages ? force_stages : o0[2], force_teams ? force_teams : o0[3]};
       if (force_cells && o[0] != force_cells) continue;
       if (o[0] > max_cells || o[0] < 2) continue;
-      const long smem = smem_bytes(nk, qs, k2s, nf, o[0], o[1], o[2], c.hdr);
+      if (o[2] * o[3] > 2 * MAX_TEAMS || o[3] > MAX_TEAMS || o[2] > 2) continue;
+      const long smem = smem_bytes(nk, qs, k2s, nf, o[0], o[1], o[2], c.hdr, o[3]);
       if (smem > smem_limit) continue;
       c.cells = o[0];
       c.m1t = 8 / o[0];
       c.upc = o[1];
       c.nw = 2 * o[1];
       c.nstage = o[2];
+      c.nteams = o[3];
       c.smem = (int)smem;
       c.cg = c.cells;
       c.pairsplit = 1;
@@ -87,12 +94,13 @@ static bool choose_config(int nk, int qs, int k2s, int nf, int smem_limit, int m
   for (auto& o : opts) {
     if (force_cells && o[0] != force_cells) continue;
     if (o[0] > max_cells) continue;
-    const long smem = smem_bytes(nk, qs, k2s, nf, o[0], o[1], o[2], c.hdr);
+    const long smem = smem_bytes(nk, qs, k2s, nf, o[0], o[1], o[2], c.hdr, 2);
     if (smem > smem_limit) continue;
     c.cells = o[0];
     c.m1t = 8 / o[0];
     c.nw = o[1];
     c.upc = o[1];
+    c.nteams = 2;
     c.nstage = o[2];
     c.smem = (int)smem;
     c.cg = c.cells;
@@ -158,44 +166,77 @@ static void build_items(const HostPlan& hp, Program& pg) {
     }
     return work;
   };
-  struct W {
-    Item it;
+  // Packing: units sorted by work (heaviest first) fill CTAs of c.upc unit
+  // slots, taking the next units in order whose group fits the CTA's team
+  // budget (<= c.nteams groups), so every CTA holds units of similar work and
+  // few slots idle at its end.  Units are then renumbered inside each group
+  // so that a team's units are contiguous (Item::ubase/nunits).
+  struct U {
     double work;
+    int l1, u;
   };
-  std::vector<W> all;
+  std::vector<U> units_all;
   double total = 0.0;
-  W cur{Item{{0, 0}, {0, 0}, {0, 0}, {0, 0}}, 0.0};
-  int nteams = 0, used = 0;
-  auto flush = [&]() {
-    if (used > 0) all.push_back(cur);
-    cur = W{Item{{0, 0}, {0, 0}, {0, 0}, {0, 0}}, 0.0};
-    nteams = 0;
-    used = 0;
-  };
-  for (int l1 = (int)pg.groups.size() - 1; l1 >= 0; --l1) {
-    const Group& gr = pg.groups[l1];
-    if (gr.n_chan == 0) continue;
-    const int units = gr.n_units;
-    int u = 0;
-    while (u < units) {
-      if (used == c.upc || nteams == 2) flush();
-      const int take = std::min(units - u, c.upc - used);
-      double w = 0.0;
-      for (int uu = u; uu < u + take; ++uu) w += unit_work(gr, uu);
-      cur.it.l1[nteams] = l1;
-      cur.it.ubase[nteams] = u;
-      cur.it.nunits[nteams] = take;
-      cur.work = std::max(cur.work, w / take);  // CTA time ~ slowest warp
+  for (const Group& gr : pg.groups)
+    for (int u = 0; u < gr.n_units; ++u) {
+      const double w = unit_work(gr, u);
+      units_all.push_back({w, gr.l1, u});
       total += w;
-      ++nteams;
-      used += take;
-      u += take;
     }
+  std::stable_sort(units_all.begin(), units_all.end(), [](const U& x, const U& y) { return x.work > y.work; });
+  struct Cta {
+    std::vector<std::vector<int>> team_units;  // per team: old unit ids
+    std::vector<int> team_l1;
+    double work = 0.0;
+  };
+  std::vector<Cta> ctas;
+  std::vector<char> taken(units_all.size(), 0);
+  size_t left = units_all.size();
+  while (left) {
+    Cta cta;
+    int used = 0;
+    for (size_t k = 0; k < units_all.size() && used < c.upc; ++k) {
+      if (taken[k]) continue;
+      const U& un = units_all[k];
+      int t = -1;
+      for (size_t j = 0; j < cta.team_l1.size(); ++j)
+        if (cta.team_l1[j] == un.l1) t = (int)j;
+      if (t < 0) {
+        if ((int)cta.team_l1.size() == c.nteams) continue;
+        cta.team_l1.push_back(un.l1);
+        cta.team_units.emplace_back();
+        t = (int)cta.team_l1.size() - 1;
+      }
+      cta.team_units[t].push_back(un.u);
+      cta.work = std::max(cta.work, un.work);
+      taken[k] = 1;
+      --left;
+      ++used;
+    }
+    ctas.push_back(std::move(cta));
   }
-  flush();
-  std::stable_sort(all.begin(), all.end(), [](const W& a, const W& b) { return a.work > b.work; });
+  // renumber units inside each group in order of appearance
+  std::vector<int16_t> new_m1 = pg.unit_m1;
+  std::vector<int> next_id(pg.groups.size(), 0);
   pg.items.clear();
-  for (auto& w : all) pg.items.push_back(w.it);
+  std::stable_sort(ctas.begin(), ctas.end(), [](const Cta& x, const Cta& y) { return x.work > y.work; });
+  for (const Cta& cta : ctas) {
+    Item it{};
+    for (size_t t = 0; t < cta.team_l1.size(); ++t) {
+      const int l1 = cta.team_l1[t];
+      const Group& gr = pg.groups[l1];
+      it.l1[t] = l1;
+      it.ubase[t] = next_id[l1];
+      it.nunits[t] = (int32_t)cta.team_units[t].size();
+      for (int old : cta.team_units[t]) {
+        const int nu = next_id[l1]++;
+        for (int ml = 0; ml < c.m1t; ++ml)
+          new_m1[(size_t)(gr.unit_off + nu) * c.m1t + ml] = pg.unit_m1[(size_t)(gr.unit_off + old) * c.m1t + ml];
+      }
+    }
+    pg.items.push_back(it);
+  }
+  pg.unit_m1.swap(new_m1);
   pg.exec_macs_per_cell = total / c.cells;
 }
 

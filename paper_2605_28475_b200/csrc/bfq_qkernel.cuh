@@ -44,12 +44,12 @@ __global__ void __launch_bounds__(256, 1) bfq_q_kernel(const KParams p) {
   const Item item = p.items[item_idx];
 
   // shared layout: barriers + arrival counters | R rings (team, stage) | Phi (per warp, 8 pairs) | f (cells)
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);  // [team*4 + stage]
-  int* arrivals = reinterpret_cast<int*>(full + 8);         // [team*4 + stage]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);  // [team*2 + stage]
+  int* arrivals = reinterpret_cast<int*>(full + 8);         // [team*2 + stage]
   int* ctau = arrivals + 8;                                   // [team][max_chan] R block index
   double* rs = reinterpret_cast<double*>(smem_raw + p.hdr);
   const int rblk = NK * K2S;
-  double* phis = rs + 2 * NST * rblk;
+  double* phis = rs + p.nteams * NST * rblk;  // R rings: nteams x NST slots
   double* fs = phis + p.nw * 8 * K2S;
   const int cell_elems = NK * QS;
 
@@ -59,24 +59,24 @@ __global__ void __launch_bounds__(256, 1) bfq_q_kernel(const KParams p) {
   // finish with a slot (smem arrival counter) issues the refill of that slot.
   auto issue_r = [&](int t, int i, int tau) {
     const int s = i % NST;
-    mbar_arrive_expect_tx(&full[t * 4 + s], rbytes);
-    bulk_g2s(rs + (t * NST + s) * rblk, p.R + (size_t)tau * rblk, rbytes, &full[t * 4 + s]);
+    mbar_arrive_expect_tx(&full[t * 2 + s], rbytes);
+    bulk_g2s(rs + (t * NST + s) * rblk, p.R + (size_t)tau * rblk, rbytes, &full[t * 2 + s]);
   };
   if (threadIdx.x == 0) {
-    for (int t = 0; t < 2; ++t)
+    for (int t = 0; t < MAX_TEAMS; ++t)
       for (int s = 0; s < NST; ++s) {
-        mbar_init(&full[t * 4 + s], 1);
-        arrivals[t * 4 + s] = 0;
+        mbar_init(&full[t * 2 + s], 1);
+        arrivals[t * 2 + s] = 0;
       }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    for (int t = 0; t < 2; ++t)
+    for (int t = 0; t < MAX_TEAMS; ++t)
       if (item.nunits[t] > 0) {
         const Group g = p.groups[item.l1[t]];
         for (int i = 0; i < NST && i < g.n_chan; ++i) issue_r(t, i, p.chans[g.chan_off + i].tau);
       }
   }
   // channel R-block indices of both teams, for the refills
-  for (int t = 0; t < 2; ++t)
+  for (int t = 0; t < MAX_TEAMS; ++t)
     if (item.nunits[t] > 0) {
       const Group g = p.groups[item.l1[t]];
       for (int i = threadIdx.x; i < g.n_chan; i += blockDim.x) ctau[t * p.max_chan + i] = p.chans[g.chan_off + i].tau;
@@ -101,14 +101,26 @@ __global__ void __launch_bounds__(256, 1) bfq_q_kernel(const KParams p) {
   }
   __syncthreads();
 
-  const int team = warp < item.nunits[0] ? 0 : 1;
-  const int twarp = team == 0 ? warp : warp - item.nunits[0];
-  if (team == 1 && twarp >= item.nunits[1]) return;
-  // team fields as scalars (a dynamically indexed Item would live in local memory)
-  const int t_l1 = team ? item.l1[1] : item.l1[0];
-  const int t_ubase = team ? item.ubase[1] : item.ubase[0];
-  const int t_nunits = team ? item.nunits[1] : item.nunits[0];
-
+  // team of this unit slot: teams own consecutive slots (scalar selects; a
+  // dynamically indexed Item would live in local memory)
+  int team = -1, tunit = 0, t_l1 = 0, t_ubase = 0, t_nunits = 0;
+  {
+    int cum = 0;
+#pragma unroll
+    for (int t = 0; t < MAX_TEAMS; ++t) {
+      const int n = item.nunits[t];
+      if (team < 0 && warp < cum + n) {
+        team = t;
+        tunit = warp - cum;
+        t_l1 = item.l1[t];
+        t_ubase = item.ubase[t];
+        t_nunits = n;
+      }
+      cum += n;
+    }
+  }
+  if (team < 0) return;
+  const int twarp = tunit;
   // ---------------- compute warp
   const bool clk_on = (p.debug & 8) != 0;
   long long ck_s1 = 0, ck_w = 0, ck_s2 = 0, ck_rf = 0, ck0 = clock64(), ckt = ck0;
@@ -117,8 +129,8 @@ __global__ void __launch_bounds__(256, 1) bfq_q_kernel(const KParams p) {
   int m1s[M1T];  // this warp's output columns (plan-balanced), -1 = empty slot
 #pragma unroll
   for (int ml = 0; ml < M1T; ++ml) m1s[ml] = p.unit_m1[(grp.unit_off + unit) * M1T + ml];
-  uint64_t* tfull = full + team * 4;
-  int* tarr = arrivals + team * 4;
+  uint64_t* tfull = full + team * 2;
+  int* tarr = arrivals + team * 2;
   const uint32_t ring_u32 = smem_u32(rs + team * NST * rblk);
   const uint32_t phw_u32 = smem_u32(phis + warp * 8 * K2S);
   const uint32_t cell_bytes = (uint32_t)cell_elems * 8u;

@@ -38,12 +38,12 @@ __global__ void __launch_bounds__(512, 1) bfq_q_kernel2(const KParams p) {
   const long long tile = (long long)blockIdx.x - item_idx * p.n_tiles;
   const Item item = p.items[item_idx];
 
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);  // [team*4 + stage]
-  int* arrivals = reinterpret_cast<int*>(full + 8);         // [team*4 + stage]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);  // [team*2 + stage]
+  int* arrivals = reinterpret_cast<int*>(full + 8);         // [team*2 + stage]
   int* ctau = arrivals + 8;                                   // [team][max_chan]
   double* rs = reinterpret_cast<double*>(smem_raw + p.hdr);
   const int rblk = NK * K2S;
-  double* phis = rs + 2 * NST * rblk;
+  double* phis = rs + p.nteams * NST * rblk;  // R rings: nteams x NST slots
   double* fs = phis + NU * 8 * K2S;
   const int cell_elems = NK * QS;
 
@@ -51,17 +51,17 @@ __global__ void __launch_bounds__(512, 1) bfq_q_kernel2(const KParams p) {
   auto issue_r = [&](int t, int i, int code) {
     const int s = i % NST;
     const unsigned bytes = (unsigned)(NK * ((code & 1) ? K2SD : K2S)) * 8u;
-    mbar_arrive_expect_tx(&full[t * 4 + s], bytes);
-    bulk_g2s(rs + (t * NST + s) * rblk, p.R + (size_t)(code >> 1) * rblk, bytes, &full[t * 4 + s]);
+    mbar_arrive_expect_tx(&full[t * 2 + s], bytes);
+    bulk_g2s(rs + (t * NST + s) * rblk, p.R + (size_t)(code >> 1) * rblk, bytes, &full[t * 2 + s]);
   };
   if (threadIdx.x == 0) {
-    for (int t = 0; t < 2; ++t)
+    for (int t = 0; t < MAX_TEAMS; ++t)
       for (int s = 0; s < NST; ++s) {
-        mbar_init(&full[t * 4 + s], 1);
-        arrivals[t * 4 + s] = 0;
+        mbar_init(&full[t * 2 + s], 1);
+        arrivals[t * 2 + s] = 0;
       }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    for (int t = 0; t < 2; ++t)
+    for (int t = 0; t < MAX_TEAMS; ++t)
       if (item.nunits[t] > 0) {
         const Group g = p.groups[item.l1[t]];
         for (int i = 0; i < NST && i < g.n_chan; ++i) {
@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(512, 1) bfq_q_kernel2(const KParams p) {
         }
       }
   }
-  for (int t = 0; t < 2; ++t)
+  for (int t = 0; t < MAX_TEAMS; ++t)
     if (item.nunits[t] > 0) {
       const Group g = p.groups[item.l1[t]];
       for (int i = threadIdx.x; i < g.n_chan; i += blockDim.x) {
@@ -96,12 +96,25 @@ __global__ void __launch_bounds__(512, 1) bfq_q_kernel2(const KParams p) {
   __syncthreads();
 
   const int u = warp >> 1, h = warp & 1;
-  const int team = u < item.nunits[0] ? 0 : 1;
-  const int tunit = team == 0 ? u : u - item.nunits[0];
-  const int t_l1 = team ? item.l1[1] : item.l1[0];
-  const int t_ubase = team ? item.ubase[1] : item.ubase[0];
-  const int t_nunits = team ? item.nunits[1] : item.nunits[0];
-  if (tunit >= t_nunits) return;  // both warps of an absent unit leave together
+  // team of this unit slot: teams own consecutive slots (scalar selects; a
+  // dynamically indexed Item would live in local memory)
+  int team = -1, tunit = 0, t_l1 = 0, t_ubase = 0, t_nunits = 0;
+  {
+    int cum = 0;
+#pragma unroll
+    for (int t = 0; t < MAX_TEAMS; ++t) {
+      const int n = item.nunits[t];
+      if (team < 0 && u < cum + n) {
+        team = t;
+        tunit = u - cum;
+        t_l1 = item.l1[t];
+        t_ubase = item.ubase[t];
+        t_nunits = n;
+      }
+      cum += n;
+    }
+  }
+  if (team < 0) return;  // both warps of an absent unit leave together
   const unsigned bar_id = 1u + (unsigned)u;
 
   const bool clk_on = (p.debug & 8) != 0;
@@ -118,8 +131,8 @@ __global__ void __launch_bounds__(512, 1) bfq_q_kernel2(const KParams p) {
   int m1s[M1T];
 #pragma unroll
   for (int ml = 0; ml < M1T; ++ml) m1s[ml] = p.unit_m1[(grp.unit_off + unit) * M1T + ml];
-  uint64_t* tfull = full + team * 4;
-  int* tarr = arrivals + team * 4;
+  uint64_t* tfull = full + team * 2;
+  int* tarr = arrivals + team * 2;
   const uint32_t ring_u32 = smem_u32(rs + team * NST * rblk);
   const uint32_t phu_u32 = smem_u32(phis + u * 8 * K2S);
   const uint32_t cell_bytes = (uint32_t)cell_elems * 8u;
