@@ -349,9 +349,18 @@ __global__ void rk4_final_kernel(double* __restrict__ y, const double* __restric
 }  // namespace
 
 // ------------------------------------------------------------ the plan
+struct HostPathScratch {
+  std::mutex mu;
+  static constexpr int NB = 3;
+  cudaStream_t st[NB] = {nullptr, nullptr, nullptr};
+  double* buf[NB] = {nullptr, nullptr, nullptr};
+  size_t cap = 0;  // doubles per buffer
+};
+
 struct bfq_plan {
   int device = 0;
   HostPlan hp;
+  HostPathScratch* host = nullptr;  // lazily created by bfq_eval_host
   double* R = nullptr;
   Row* rows = nullptr;
   int* sstart = nullptr;
@@ -542,6 +551,13 @@ int bfq_plan_destroy(bfq_plan* plan) {
     cudaFree(plan->sstart);
     free_program(plan->sym);
     free_program(plan->full);
+    if (plan->host) {
+      for (int b = 0; b < HostPathScratch::NB; ++b) {
+        cudaFree(plan->host->buf[b]);
+        if (plan->host->st[b]) cudaStreamDestroy(plan->host->st[b]);
+      }
+      delete plan->host;
+    }
   }
   delete plan;
   return BFQ_OK;
@@ -602,52 +618,67 @@ int bfq_eval_host(const bfq_plan* plan, const double* f2, const double* f3, doub
   DeviceGuard guard(plan->device);
   const bool same = (f3 == nullptr || f3 == f2);
   const size_t ndof = (size_t)plan->hp.n_k * plan->hp.n_q;
-  // chunked, two-stream pipeline: H2D(i+1) and D2H(i-1) overlap Q(i)
-  const int64_t chunk = std::min<int64_t>(n_cells, 4096);
-  const int nbuf = 2;
-  cudaStream_t st[nbuf];
-  double* dbuf[nbuf] = {nullptr, nullptr};
-  int rc = BFQ_OK;
-  for (int b = 0; b < nbuf; ++b) {
-    if (cudaStreamCreateWithFlags(&st[b], cudaStreamNonBlocking) != cudaSuccess) {
+  // chunked pipeline over NB streams: H2D(i+1), Q(i), D2H(i-1) overlap; the
+  // streams and device buffers persist in the plan (serialised by a mutex)
+  const int64_t chunk = std::min<int64_t>(n_cells, std::max<int64_t>(2048, std::min<int64_t>(8192, n_cells / 8)));
+  HostPathScratch*& hs = const_cast<bfq_plan*>(plan)->host;
+  static std::mutex create_mu;
+  {
+    std::lock_guard<std::mutex> lk(create_mu);
+    if (!hs) hs = new (std::nothrow) HostPathScratch();
+    if (!hs) {
+      set_error("host allocation failed");
+      return BFQ_ENOMEM;
+    }
+  }
+  std::lock_guard<std::mutex> lk(hs->mu);
+  const int NB = HostPathScratch::NB;
+  const size_t per = chunk * ndof, need = per * 3;
+  if (hs->cap < need) {
+    for (int b = 0; b < NB; ++b) {
+      cudaFree(hs->buf[b]);
+      hs->buf[b] = nullptr;
+    }
+    hs->cap = 0;
+    for (int b = 0; b < NB; ++b)
+      if (cudaMalloc(&hs->buf[b], need * sizeof(double)) != cudaSuccess) {
+        set_error("device allocation failed");
+        return BFQ_ENOMEM;
+      }
+    hs->cap = need;
+  }
+  for (int b = 0; b < NB; ++b)
+    if (!hs->st[b] && cudaStreamCreateWithFlags(&hs->st[b], cudaStreamNonBlocking) != cudaSuccess) {
       set_error("stream creation failed");
       return BFQ_ECUDA;
     }
-  }
-  const size_t per = chunk * ndof;
-  for (int b = 0; b < nbuf && rc == BFQ_OK; ++b)
-    if (cudaMalloc(&dbuf[b], per * sizeof(double) * (same ? 2 : 3)) != cudaSuccess) {
-      set_error("device allocation failed");
-      rc = BFQ_ENOMEM;
-    }
+  int rc = BFQ_OK;
   for (int64_t c0 = 0, i = 0; c0 < n_cells && rc == BFQ_OK; c0 += chunk, ++i) {
-    const int b = (int)(i % nbuf);
+    const int b = (int)(i % NB);
+    cudaStream_t st = hs->st[b];
     const int64_t n = std::min<int64_t>(chunk, n_cells - c0);
-    double* d2 = dbuf[b];
+    double* d2 = hs->buf[b];
     double* dq = d2 + per;
     double* d3 = same ? d2 : dq + per;
     const size_t bytes = n * ndof * sizeof(double);
-    if (cudaMemcpyAsync(d2, f2 + c0 * ndof, bytes, cudaMemcpyHostToDevice, st[b]) != cudaSuccess ||
-        (!same && cudaMemcpyAsync(d3, f3 + c0 * ndof, bytes, cudaMemcpyHostToDevice, st[b]) != cudaSuccess)) {
+    if (cudaMemcpyAsync(d2, f2 + c0 * ndof, bytes, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+        (!same && cudaMemcpyAsync(d3, f3 + c0 * ndof, bytes, cudaMemcpyHostToDevice, st) != cudaSuccess)) {
       set_error("host-to-device copy failed");
       rc = BFQ_ECUDA;
       break;
     }
-    rc = launch_q(plan, same ? plan->sym : plan->full, d2, d3, dq, n, st[b]);
+    rc = launch_q(plan, same ? plan->sym : plan->full, d2, d3, dq, n, st);
     if (rc) break;
-    if (cudaMemcpyAsync(q + c0 * ndof, dq, bytes, cudaMemcpyDeviceToHost, st[b]) != cudaSuccess) {
+    if (cudaMemcpyAsync(q + c0 * ndof, dq, bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess) {
       set_error("device-to-host copy failed");
       rc = BFQ_ECUDA;
     }
   }
-  for (int b = 0; b < nbuf; ++b) {
-    if (cudaStreamSynchronize(st[b]) != cudaSuccess && rc == BFQ_OK) {
+  for (int b = 0; b < NB; ++b)
+    if (cudaStreamSynchronize(hs->st[b]) != cudaSuccess && rc == BFQ_OK) {
       set_error(cudaGetErrorString(cudaGetLastError()));
       rc = BFQ_ECUDA;
     }
-    cudaFree(dbuf[b]);
-    cudaStreamDestroy(st[b]);
-  }
   return rc;
 }
 

@@ -64,7 +64,7 @@ static bool choose_config(int nk, int qs, int k2s, int nf, int smem_limit, int m
   // whole stage 1 to land), else 2 teams.
   static const int popts[][4] = {  // cells, units, stages, teams
       {8, 8, 1, 4}, {8, 8, 2, 2}, {4, 8, 1, 4}, {4, 8, 2, 2}, {4, 8, 1, 2},
-      {2, 8, 1, 4}, {2, 8, 2, 2}, {2, 8, 1, 2}};
+      {2, 8, 1, 4}, {2, 8, 2, 2}, {2, 8, 1, 2}, {2, 4, 1, 2}, {2, 4, 1, 1}};
   int force_stages = 0, force_teams = 0;
   if (const char* e = std::getenv("BFQ_STAGES")) force_stages = std::atoi(e);
   if (const char* e = std::getenv("BFQ_TEAMS")) force_teams = std::atoi(e);

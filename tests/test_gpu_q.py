@@ -282,3 +282,20 @@ def test_linearize_matches_reference(name):
     if name == "hs_k4l6":
         lam = np.linalg.eigvals(j_eq)
         assert int(np.sum(np.abs(lam) < 1e-12)) == 5
+
+
+def test_n16_path_synthetic_operator():
+    """N=L=16 (config-4 shape: n_k = 17, three 8x8 tiles per axis) on the
+    synthetic-R operator, against the oracle on two cells."""
+    if not os.path.exists(os.path.join(OPERATORS, "synth_n16.bfct")):
+        pytest.skip("synthetic N=L=16 operator not present")
+    op = load_op("synth_n16")
+    cfg = op.cfg
+    cells = inputs.perturbed_maxwellians(cfg.n_k, cfg.l_max, 9, seed=16)
+    q = run(op, cells)
+    assert_invariants_zero(q)
+    oop = q_oracle.OracleOperator.from_operator(op)
+    for i in (0, 8):
+        assert q_oracle.rel_err(q[i], q_oracle.q_angular_first(oop, cells[i])) <= TOL, i
+    q12 = run(op, cells[:3], cells[3:6])  # bilinear path at n_k = 17
+    assert q_oracle.rel_err(q12[1], q_oracle.q_angular_first(oop, cells[1], cells[4])) <= TOL
