@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(512, 1) bfq_q_kernel2(const KParams p) {
 
   // ctau[t][i] = 2 * R-block index + diag; diag blocks are shorter (packed K)
   auto issue_r = [&](int t, int i, int code) {
-    const int s = i % NST;
+    const int s = NST == 1 ? 0 : (i & 1);
     const unsigned bytes = (unsigned)(NK * ((code & 1) ? K2SD : K2S)) * 8u;
     mbar_arrive_expect_tx(&full[t * 2 + s], bytes);
     bulk_g2s(rs + (t * NST + s) * rblk, p.R + (size_t)(code >> 1) * rblk, bytes, &full[t * 2 + s]);
@@ -117,7 +117,11 @@ __global__ void __launch_bounds__(512, 1) bfq_q_kernel2(const KParams p) {
   if (team < 0) return;  // both warps of an absent unit leave together
   const unsigned bar_id = 1u + (unsigned)u;
 
+#ifdef BFQ_PHASE_CLOCKS
   const bool clk_on = (p.debug & 8) != 0;
+#else
+  constexpr bool clk_on = false;  // build with -DBFQ_PHASE_CLOCKS for per-phase cycle counts
+#endif
   long long ck_s1 = 0, ck_b1 = 0, ck_w = 0, ck_s2 = 0, ck_b2 = 0, ck0 = clock64(), ckt = ck0;
   auto tick = [&](long long& acc) {
     if (clk_on) {
@@ -265,8 +269,10 @@ __global__ void __launch_bounds__(512, 1) bfq_q_kernel2(const KParams p) {
     named_bar_sync(bar_id, 64);  // Phi of all 8 pairs written
     tick(ck_b1);
     // ---- stage 2: this warp's half of K for all 8 pairs
-    const int s = i % NST;
-    mbar_wait(&tfull[s], (unsigned)(i / NST) & 1u);
+    // ring slot and phase of channel i (NST is 1 or 2: no integer division)
+    const int s = NST == 1 ? 0 : (i & 1);
+    const unsigned par = NST == 1 ? (unsigned)(i & 1) : (unsigned)((i >> 1) & 1);
+    mbar_wait(&tfull[s], par);
     tick(ck_w);
     const uint32_t rb = ring_u32 + (uint32_t)(s * rblk) * 8u;
     const uint32_t pa = phu_u32 + (uint32_t)(r0 * K2S + kq) * 8u;
