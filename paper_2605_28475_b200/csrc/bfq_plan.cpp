@@ -492,16 +492,21 @@ int build_host_plan(const bfq_desc& d, int smem_limit, HostPlan& hp) {
   {
     const Program& pg = hp.sym;
     const KernelConfig& c = pg.cfg;
+    // n_k = 8k+1 with a fixed-size pair-split kernel: the last k row/column
+    // runs on DFMA (bfq_qkernel2.cuh, X1), so one tile column fewer on DMMA
+    const bool x1 = c.pairsplit && nk % 8 == 1 && c.mt >= 2 && (nk == 9 || nk == 17) &&
+                    !std::getenv("BFQ_GENERIC");
+    const int mte = x1 ? c.mt - 1 : c.mt;
     double total = 0.0;
     for (const Group& gr : pg.groups) {
       for (int e = 0; e < gr.n_chan; ++e) {
         const ChanEntry& ce = pg.chans[gr.chan_off + e];
-        const double tiles = ce.diag ? c.mt * (c.mt + 1) / 2 : c.mt * c.mt;
+        const double tiles = ce.diag ? mte * (mte + 1) / 2 : mte * mte;
         for (int m1 = 0; m1 < gr.d1; ++m1) {
           const int rows = hp.sstart[ce.slice_base + m1 + 1] - hp.sstart[ce.slice_base + m1];
           total += tiles * 256.0 * ((rows + 3) / 4);  // per cell
         }
-        total += (double)gr.n_units * c.mt * 256.0 * ((ce.diag ? hp.k2pd : hp.k2p) / 4) / c.cells;
+        total += (double)gr.n_units * mte * 256.0 * ((ce.diag ? hp.k2pd : hp.k2p) / 4) / c.cells;
       }
     }
     hp.sym.exec_macs_per_cell = total;

@@ -21,6 +21,11 @@ __global__ void __launch_bounds__(512, 1) bfq_q_kernel2(const KParams p) {
   static_assert(CELLS >= 2, "pair split needs at least two cells per tile");
   constexpr bool FIXED = NKT > 0;
   constexpr int NF = BILIN ? 2 : 1;
+  // 8k+1 sizes (n_k = 9, 17): the last radial index is handled by DFMA +
+  // lane reductions instead of a padded DMMA tile row/column (X1); MTM tiles
+  // per axis go through DMMA
+  constexpr bool X1 = FIXED && (NKT % 8 == 1) && MT >= 2;
+  constexpr int MTM = X1 ? MT - 1 : MT;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r0 = lane >> 2, kq = lane & 3;
@@ -140,7 +145,7 @@ __global__ void __launch_bounds__(512, 1) bfq_q_kernel2(const KParams p) {
   const uint32_t ring_u32 = smem_u32(rs + team * NST * rblk);
   const uint32_t phu_u32 = smem_u32(phis + u * 8 * K2S);
   const uint32_t cell_bytes = (uint32_t)cell_elems * 8u;
-  uint32_t fa[MT], fb[MT], rrow[MT], rrowd[MT];
+  uint32_t fa[MT], fb[MT], rrow[MT], rrowd[MT], fx_a = 0, fx_b = 0, rx = 0, rxd = 0;
   {
     const uint32_t f0 = smem_u32(fs) + (uint32_t)(h * HC) * cell_bytes;  // this warp's first cell
     const uint32_t f3off = BILIN ? (uint32_t)(CELLS * cell_elems) * 8u : 0u;
@@ -152,10 +157,15 @@ __global__ void __launch_bounds__(512, 1) bfq_q_kernel2(const KParams p) {
       rrow[t] = (uint32_t)(r * K2S + kq) * 8u;
       rrowd[t] = (uint32_t)(r * K2SD + kq) * 8u;
     }
+    fx_a = f0 + (uint32_t)((NK - 1) * QS) * 8u;
+    fx_b = fx_a + f3off;
+    rx = (uint32_t)((NK - 1) * K2S + kq) * 8u;   // R row k1 = n_k-1 (X1 stage 2)
+    rxd = (uint32_t)((NK - 1) * K2SD + kq) * 8u;
   }
   double acc2[MT][2], accb[MT][2];
 #pragma unroll
   for (int j = 0; j < MT; ++j) acc2[j][0] = acc2[j][1] = accb[j][0] = accb[j][1] = 0.0;
+  double x2 = 0.0;  // X1: partial out[pair r0][k1 = n_k-1] over this lane's k
 
   const int nch = grp.n_chan;
   auto slice_bounds = [&](int ci, int* zs, int* ze) {
@@ -180,9 +190,9 @@ __global__ void __launch_bounds__(512, 1) bfq_q_kernel2(const KParams p) {
     for (int cc = 0; cc < HC; ++cc) {
       const uint32_t ph = phu_u32 + (uint32_t)((ml * CELLS + h * HC + cc) * K2S) * 8u;
 #pragma unroll
-      for (int a = 0; a < MT; ++a)
+      for (int a = 0; a < MTM; ++a)
 #pragma unroll
-        for (int b = 0; b < MT; ++b)
+        for (int b = 0; b < MTM; ++b)
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int ia = 8 * a + r0, ib = 8 * b + 2 * kq + e;
@@ -222,46 +232,95 @@ __global__ void __launch_bounds__(512, 1) bfq_q_kernel2(const KParams p) {
     const bool dg = (ctau[team * p.max_chan + i] & 1) != 0;
     auto stage1 = [&](auto dgtag) {
       constexpr bool DGC = decltype(dgtag)::value;
-    // ---- stage 1: Phi of this warp's HC cells for the unit's M1T columns
+      // ---- stage 1: Phi of this warp's HC cells for the unit's M1T columns
 #pragma unroll
-    for (int ml = 0; ml < M1T; ++ml) {
-      double acc[HC][MT][MT][2];
-#pragma unroll
-      for (int cc = 0; cc < HC; ++cc)
-#pragma unroll
-        for (int a = 0; a < MT; ++a)
-#pragma unroll
-          for (int b = 0; b < MT; ++b) acc[cc][a][b][0] = acc[cc][a][b][1] = 0.0;
-      for (int z0 = zs[ml]; z0 < ze[ml]; z0 += 4) {
-        const Row rw = nxt_row;
-        {
-          const bool same = z0 + 4 < ze[ml];
-          const int zn = ml + 1 < M1T ? zs[ml + 1 < M1T ? ml + 1 : ml] : zs_n[0];
-          const int en = ml + 1 < M1T ? ze[ml + 1 < M1T ? ml + 1 : ml] : (i + 1 < nch ? ze_n[0] : 0);
-          nxt_row = fetch_row_bf(p.rows, (same ? z0 + 4 : zn) + kq, same ? ze[ml] : en);
-        }
-        const uint32_t qa = (uint32_t)rw.q2 * 8u, qb = (uint32_t)rw.q3 * 8u;
+      for (int ml = 0; ml < M1T; ++ml) {
+        double acc[HC][MT][MT][2];
+        double xr[HC][MTM], xc[HC][MTM], xd[HC];  // X1: row / column / corner of index n_k-1
 #pragma unroll
         for (int cc = 0; cc < HC; ++cc) {
-          double av[MT], bv[MT];
-#pragma unroll
-          for (int t = 0; t < MT; ++t) {
-            av[t] = rw.g * lds_ro(fa[t] + qa + cc * cell_bytes);
-            bv[t] = lds_ro(fb[t] + qb + cc * cell_bytes);
-          }
 #pragma unroll
           for (int a = 0; a < MT; ++a)
 #pragma unroll
-            for (int b = 0; b < MT; ++b)
-              if (b >= a || !DGC) dmma884(acc[cc][a][b][0], acc[cc][a][b][1], av[a], bv[b]);
+            for (int b = 0; b < MT; ++b) acc[cc][a][b][0] = acc[cc][a][b][1] = 0.0;
+#pragma unroll
+          for (int t = 0; t < MTM; ++t) xr[cc][t] = xc[cc][t] = 0.0;
+          xd[cc] = 0.0;
+        }
+        for (int z0 = zs[ml]; z0 < ze[ml]; z0 += 4) {
+          const Row rw = nxt_row;
+          {
+            const bool same = z0 + 4 < ze[ml];
+            const int zn = ml + 1 < M1T ? zs[ml + 1 < M1T ? ml + 1 : ml] : zs_n[0];
+            const int en = ml + 1 < M1T ? ze[ml + 1 < M1T ? ml + 1 : ml] : (i + 1 < nch ? ze_n[0] : 0);
+            nxt_row = fetch_row_bf(p.rows, (same ? z0 + 4 : zn) + kq, same ? ze[ml] : en);
+          }
+          const uint32_t qa = (uint32_t)rw.q2 * 8u, qb = (uint32_t)rw.q3 * 8u;
+#pragma unroll
+          for (int cc = 0; cc < HC; ++cc) {
+            double av[MT], bv[MT];
+#pragma unroll
+            for (int t = 0; t < MTM; ++t) {
+              av[t] = rw.g * lds_ro(fa[t] + qa + cc * cell_bytes);
+              bv[t] = lds_ro(fb[t] + qb + cc * cell_bytes);
+            }
+#pragma unroll
+            for (int a = 0; a < MTM; ++a)
+#pragma unroll
+              for (int b = 0; b < MTM; ++b)
+                if (b >= a || !DGC) dmma884(acc[cc][a][b][0], acc[cc][a][b][1], av[a], bv[b]);
+            if constexpr (X1) {
+              const double ea = rw.g * lds_ro(fx_a + qa + cc * cell_bytes);  // g f2[n_k-1, q2]
+              const double eb = lds_ro(fx_b + qb + cc * cell_bytes);         // f3[n_k-1, q3]
+#pragma unroll
+              for (int t = 0; t < MTM; ++t) {
+                if (!DGC) xr[cc][t] = fma(ea, bv[t], xr[cc][t]);
+                xc[cc][t] = fma(av[t], eb, xc[cc][t]);
+              }
+              xd[cc] = fma(ea, eb, xd[cc]);
+            }
+          }
+        }
+        if (zs[ml] >= ze[ml]) {
+          if (ml + 1 < M1T) nxt_row = fetch_row_bf(p.rows, zs[ml + 1 < M1T ? ml + 1 : ml] + kq, ze[ml + 1 < M1T ? ml + 1 : ml]);
+          else nxt_row = fetch_row_bf(p.rows, zs_n[0] + kq, i + 1 < nch ? ze_n[0] : 0);
+        }
+        store_phi(ml, acc, DGC);
+        if constexpr (X1) {
+          // lanes kq = 0..3 hold partial sums over their own rows: reduce, then
+          // the kq == 0 lanes store row / column n_k-1 of Phi
+#pragma unroll
+          for (int cc = 0; cc < HC; ++cc) {
+#pragma unroll
+            for (int t = 0; t < MTM; ++t) {
+              xr[cc][t] += __shfl_xor_sync(0xffffffffu, xr[cc][t], 1);
+              xr[cc][t] += __shfl_xor_sync(0xffffffffu, xr[cc][t], 2);
+              xc[cc][t] += __shfl_xor_sync(0xffffffffu, xc[cc][t], 1);
+              xc[cc][t] += __shfl_xor_sync(0xffffffffu, xc[cc][t], 2);
+            }
+            xd[cc] += __shfl_xor_sync(0xffffffffu, xd[cc], 1);
+            xd[cc] += __shfl_xor_sync(0xffffffffu, xd[cc], 2);
+            const uint32_t ph = phu_u32 + (uint32_t)((ml * CELLS + h * HC + cc) * K2S) * 8u;
+            constexpr int L = NKT - 1;
+            if (kq == 0) {
+#pragma unroll
+              for (int t = 0; t < MTM; ++t) {
+                const int ab = r0 + 8 * t;
+                if (!DGC) {
+                  sts_v(ph + (uint32_t)(L * NKT + ab) * 8u, xr[cc][t]);  // Phi[L][b]
+                  sts_v(ph + (uint32_t)(ab * NKT + L) * 8u, xc[cc][t]);  // Phi[a][L]
+                } else {
+                  sts_v(ph + (uint32_t)(ab * NKT - (ab * (ab - 1)) / 2 + (L - ab)) * 8u, xc[cc][t]);
+                }
+              }
+              if (r0 == 0) {
+                const int pl = DGC ? (L * NKT - (L * (L - 1)) / 2) : (L * NKT + L);
+                sts_v(ph + (uint32_t)pl * 8u, xd[cc]);
+              }
+            }
+          }
         }
       }
-      if (zs[ml] >= ze[ml]) {
-        if (ml + 1 < M1T) nxt_row = fetch_row_bf(p.rows, zs[ml + 1 < M1T ? ml + 1 : ml] + kq, ze[ml + 1 < M1T ? ml + 1 : ml]);
-        else nxt_row = fetch_row_bf(p.rows, zs_n[0] + kq, i + 1 < nch ? ze_n[0] : 0);
-      }
-      store_phi(ml, acc, DGC);
-    }
     };
     if (dg) stage1(std::true_type{});
     else stage1(std::false_type{});
@@ -278,35 +337,41 @@ __global__ void __launch_bounds__(512, 1) bfq_q_kernel2(const KParams p) {
     const uint32_t pa = phu_u32 + (uint32_t)(r0 * K2S + kq) * 8u;
     auto stage2 = [&](auto dgtag) {
       constexpr bool DGC = decltype(dgtag)::value;
-    // this warp's half of the k-steps (K = n_k^2, or the packed triangle)
-    const int nks = (DGC ? K2PD : K2P) / 4;
-    const int ks0 = h ? (nks + 1) / 2 : 0, ks1 = h ? nks : (nks + 1) / 2;
-    uint32_t rr[MT];
+      // this warp's half of the k-steps (K = n_k^2, or the packed triangle)
+      const int nks = (DGC ? K2PD : K2P) / 4;
+      const int ks0 = h ? (nks + 1) / 2 : 0, ks1 = h ? nks : (nks + 1) / 2;
+      uint32_t rr[MT];
 #pragma unroll
-    for (int j = 0; j < MT; ++j) rr[j] = DGC ? rrowd[j] : rrow[j];
-    int ks = ks0;
+      for (int j = 0; j < MT; ++j) rr[j] = DGC ? rrowd[j] : rrow[j];
+      const uint32_t rrx = DGC ? rxd : rx;  // X1: R row k1 = n_k-1 (DFMA)
+      int ks = ks0;
 #pragma unroll 2
-    for (; ks + 2 <= ks1; ks += 2) {
-      const int k0 = ks * 4;
-      const double av0 = lds_v(pa + k0 * 8), av1 = lds_v(pa + (k0 + 4) * 8);
-      double bv0[MT], bv1[MT];
+      for (; ks + 2 <= ks1; ks += 2) {
+        const int k0 = ks * 4;
+        const double av0 = lds_v(pa + k0 * 8), av1 = lds_v(pa + (k0 + 4) * 8);
+        double bv0[MT], bv1[MT];
 #pragma unroll
-      for (int j = 0; j < MT; ++j) {
-        bv0[j] = lds_v(rb + rr[j] + k0 * 8);
-        bv1[j] = lds_v(rb + rr[j] + (k0 + 4) * 8);
+        for (int j = 0; j < MTM; ++j) {
+          bv0[j] = lds_v(rb + rr[j] + k0 * 8);
+          bv1[j] = lds_v(rb + rr[j] + (k0 + 4) * 8);
+        }
+#pragma unroll
+        for (int j = 0; j < MTM; ++j) {
+          dmma884(acc2[j][0], acc2[j][1], av0, bv0[j]);
+          dmma884(accb[j][0], accb[j][1], av1, bv1[j]);
+        }
+        if constexpr (X1) {
+          x2 = fma(av0, lds_v(rb + rrx + k0 * 8), x2);
+          x2 = fma(av1, lds_v(rb + rrx + (k0 + 4) * 8), x2);
+        }
       }
+      if (ks < ks1) {
+        const int k0 = ks * 4;
+        const double av = lds_v(pa + k0 * 8);
 #pragma unroll
-      for (int j = 0; j < MT; ++j) {
-        dmma884(acc2[j][0], acc2[j][1], av0, bv0[j]);
-        dmma884(accb[j][0], accb[j][1], av1, bv1[j]);
+        for (int j = 0; j < MTM; ++j) dmma884(acc2[j][0], acc2[j][1], av, lds_v(rb + rr[j] + k0 * 8));
+        if constexpr (X1) x2 = fma(av, lds_v(rb + rrx + k0 * 8), x2);
       }
-    }
-    if (ks < ks1) {
-      const int k0 = ks * 4;
-      const double av = lds_v(pa + k0 * 8);
-#pragma unroll
-      for (int j = 0; j < MT; ++j) dmma884(acc2[j][0], acc2[j][1], av, lds_v(rb + rr[j] + k0 * 8));
-    }
     };
     if (dg) stage2(std::true_type{});
     else stage2(std::false_type{});
@@ -332,13 +397,18 @@ __global__ void __launch_bounds__(512, 1) bfq_q_kernel2(const KParams p) {
     atomicAdd(p.dbg_clk + 6, 1ull);
   }
   // ---------------- epilogue: warp 1 hands its K-half partials to warp 0
-  const uint32_t xch = phu_u32 + (uint32_t)(lane * 2 * MT) * 8u;
+  if constexpr (X1) {  // out[pair][n_k-1]: sum the four kq lanes
+    x2 += __shfl_xor_sync(0xffffffffu, x2, 1);
+    x2 += __shfl_xor_sync(0xffffffffu, x2, 2);
+  }
+  const uint32_t xch = phu_u32 + (uint32_t)(lane * (2 * MT + 1)) * 8u;
   if (h == 1) {
 #pragma unroll
-    for (int j = 0; j < MT; ++j) {
+    for (int j = 0; j < MTM; ++j) {
       sts_v(xch + (uint32_t)(2 * j) * 8u, acc2[j][0] + accb[j][0]);
       sts_v(xch + (uint32_t)(2 * j + 1) * 8u, acc2[j][1] + accb[j][1]);
     }
+    if constexpr (X1) sts_v(xch + (uint32_t)(2 * MT) * 8u, x2);
   }
   named_bar_sync(bar_id, 64);
   if (h == 1) return;
@@ -351,16 +421,18 @@ __global__ void __launch_bounds__(512, 1) bfq_q_kernel2(const KParams p) {
   if (m1 >= 0 && cell < p.n_cells) {
     const int l1 = grp.l1, q1 = l1 * l1 + m1;
     double* qc = p.q + cell * (long long)NK * p.nq + q1;
+    auto put = [&](int k1, double v) {
+      if (p.conservation && ((k1 == 0 && l1 <= 1) || (k1 == 1 && l1 == 0))) v = 0.0;
+      qc[(size_t)k1 * p.nq] = v;
+    };
 #pragma unroll
-    for (int j = 0; j < MT; ++j)
+    for (int j = 0; j < MTM; ++j)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int k1 = 8 * j + 2 * kq + e;
-        if (k1 < NK) {
-          double v = (acc2[j][e] + accb[j][e]) + lds_v(xch + (uint32_t)(2 * j + e) * 8u);
-          if (p.conservation && ((k1 == 0 && l1 <= 1) || (k1 == 1 && l1 == 0))) v = 0.0;
-          qc[(size_t)k1 * p.nq] = v;
-        }
+        if (k1 < NK) put(k1, (acc2[j][e] + accb[j][e]) + lds_v(xch + (uint32_t)(2 * j + e) * 8u));
       }
+    if constexpr (X1)
+      if (kq == 0) put(NK - 1, x2 + lds_v(xch + (uint32_t)(2 * MT) * 8u));
   }
 }
