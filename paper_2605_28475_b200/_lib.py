@@ -40,6 +40,8 @@ EXPORTED_SYMBOLS = (
     "bfq_strerror",
     "bfq_last_error",
 )
+# every symbol include/bfr.h declares
+EXPORTED_SYMBOLS_BFR = ("bfr_assemble",)
 
 _i32p = ctypes.POINTER(ctypes.c_int32)
 _i64p = ctypes.POINTER(ctypes.c_int64)
@@ -87,6 +89,50 @@ class BfqPlanInfo(ctypes.Structure):
     ]
 
 
+class BfrDesc(ctypes.Structure):
+    """include/bfr.h bfr_desc."""
+
+    _fields_ = [
+        ("k_max", ctypes.c_int32),
+        ("l_max", ctypes.c_int32),
+        ("gamma", ctypes.c_double),
+        ("kernel_scale", ctypes.c_double),
+        ("n_t", ctypes.c_int32),
+        ("triplets", _i32p),
+        ("swap", _i32p),
+        ("w3j", _f64p),
+        ("chan_scale", _f64p),
+        ("n_e", ctypes.c_int32),
+        ("e_x", _f64p),
+        ("e_w", _f64p),
+        ("n_chi", ctypes.c_int32),
+        ("chi_x", _f64p),
+        ("chi_w", _f64p),
+        ("n_eps", ctypes.c_int32),
+        ("eps_x", _f64p),
+        ("eps_w", _f64p),
+        ("n_outer", ctypes.c_int32 * 2),
+        ("n_inner", ctypes.c_int32 * 2),
+        ("outer_x", _f64p * 2),
+        ("outer_w", _f64p * 2),
+        ("inner_x", _f64p * 2),
+        ("inner_w", _f64p * 2),
+        ("mono", _f64p),
+        ("norms", _f64p),
+    ]
+
+
+class BfrStats(ctypes.Structure):
+    _fields_ = [
+        ("ms_total", ctypes.c_double),
+        ("ms_contract", ctypes.c_double),
+        ("contract_macs", ctypes.c_double),
+        ("alg_macs", ctypes.c_double),
+        ("x_bytes", ctypes.c_double),
+        ("n_points", ctypes.c_int64 * 2),
+    ]
+
+
 class EngineUnavailable(RuntimeError):
     """The CUDA engine library is not built or cannot be loaded."""
 
@@ -111,7 +157,8 @@ def _declare(lib):
     lib.bfq_strerror.restype = ctypes.c_char_p
     lib.bfq_last_error.argtypes = []
     lib.bfq_last_error.restype = ctypes.c_char_p
-    for name in EXPORTED_SYMBOLS:
+    lib.bfr_assemble.argtypes = [ctypes.POINTER(BfrDesc), ctypes.c_int, vp, vp, ctypes.POINTER(BfrStats)]
+    for name in EXPORTED_SYMBOLS + EXPORTED_SYMBOLS_BFR:
         if name not in ("bfq_strerror", "bfq_last_error"):
             getattr(lib, name).restype = ctypes.c_int
 

@@ -1,0 +1,965 @@
+// bfr_build.cu -- R-tensor assembly on sm_100a (include/bfr.h).
+//
+// What the reference computes (pkg/src/boltzfact/kinematic.py), per channel
+// tau = (l1, l2, l3) and per Duffy patch, on the tensor grid
+// (E, outer o, Duffy t, deflection chi, azimuth eps):
+//
+//   p_gain   = Y_l2(0) sum_m b_m(o,t) ReY_{l1 m}(v'(chi,eps,o,t))           :427-445
+//   g_j(o,t) = kern(o,t) sum_{chi,eps} w w |v'|^l1 (|v'|^2/2)^j p_gain       :456-464
+//   core     = pref[k,E] sum_j mono[k,j] eta_E^j g_j(o,t)                     :466-471
+//   gain     = sum_{E,o,t} core phi_l2(v) phi_l3(w) env                        :480-507
+//   loss_f/s = sum phi_l1 phi_l2 phi_l3 env * loss_kern (fast / slow branch)
+//
+// and combines R = scale * sym(gain + swap(gain) - loss_f - loss_s) (:552-570).
+//
+// B200 restructuring (same integrals, different association):
+//  * the chi/eps integral of |v'|^(l1+2j) ReY_{l1 m} depends on l1 only, not on
+//    (l2, l3): one table A[l1,m,j](o,t) per patch (k_atab) replaces a per-channel
+//    azimuth/deflection contraction; g_j is then a short m-sum (k_gstack);
+//  * every channel integral is a triple product over the flattened point axis
+//    p = (E, o[, t]):  out[r,a,b] = sum_p X[r,p] U[a,p] W[b,p], with rows X =
+//    gain / fast-loss / slow-loss integrands (k_xrows) and U, W radial tables.
+//    That is a GEMM with M = rows, N = (a,b), K = p, run on the FP64 tensor
+//    pipe (DMMA m8n8k4) with the (a,b) operand formed in registers from two
+//    staged radial rows (k_tri), split over p with a deterministic reduction.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "bfq.h"
+#include "bfr.h"
+#include "bfq_internal.h"
+
+using namespace bfq;
+
+namespace {
+
+constexpr int LMX = BFR_LMAX_SUPPORTED;
+constexpr int NK_MAX = 17;     // k_tri register tiling covers n_k <= 17
+constexpr int PC = 64;         // points per staged chunk in k_tri
+constexpr int SROW = PC + 4;   // smem row stride (doubles), = 4 mod 16: conflict-free fragments
+constexpr double PI = 3.14159265358979323846;
+
+// fully normalised associated Legendre recurrence coefficients (Condon-Shortley)
+//   Ybar_{m,m}   = d_m sqrt(1-x^2) Ybar_{m-1,m-1},   d_m = -sqrt((2m+1)/(2m))
+//   Ybar_{m+1,m} = e_m x Ybar_{m,m},                 e_m = sqrt(2m+3)
+//   Ybar_{l,m}   = a_lm (x Ybar_{l-1,m} - b_lm Ybar_{l-2,m})
+__constant__ double c_ya[(LMX + 1) * (LMX + 1)];
+__constant__ double c_yb[(LMX + 1) * (LMX + 1)];
+__constant__ double c_yd[LMX + 1];
+__constant__ double c_ye[LMX + 1];
+
+__host__ __device__ inline int lm_index(int l, int m) { return l * (l + 1) / 2 + m; }
+
+// N_lm P_l^m(x) for one (l, m), m <= l (basis.py:176-193 sph_harm_theta)
+__device__ double ybar(int l, int m, double x) {
+  const double sx = sqrt(fmax((1.0 - x) * (1.0 + x), 0.0));
+  double pmm = 0.28209479177387814347;  // 1/sqrt(4 pi)
+  for (int i = 1; i <= m; ++i) pmm = c_yd[i] * sx * pmm;
+  if (l == m) return pmm;
+  double p0 = pmm, p1 = c_ye[m] * x * pmm;
+  for (int ll = m + 2; ll <= l; ++ll) {
+    const double p2 = c_ya[ll * (LMX + 1) + m] * (x * p1 - c_yb[ll * (LMX + 1) + m] * p0);
+    p0 = p1;
+    p1 = p2;
+  }
+  return p1;
+}
+
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int bytes) {
+  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+// ------------------------------------------------------------------ geometry
+// per (o,t) point of one patch (kinematic.py:322-362); fields of g[f*n_ot + i]
+enum { G_RHO, G_COSB, G_V0, G_W0, G_U0, G_FGEO, G_KERN, G_CX, G_CZ, G_UHX, G_UHZ, G_E1X, G_E1Z,
+       G_E2Y, G_NF };
+
+__global__ void k_geom(int patch, const double* ox, const double* tx, int n_o, int n_t,
+                       double gamma, double kscale, double fgeo_c, double* g) {
+  const int n_ot = n_o * n_t;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_ot) return;
+  const int o = i / n_t, t = i - o * n_t;
+  const double x = ox[o], tt = tx[t];
+  double rho, h, duffy;
+  if (patch == 0) {  // rho > h, h = rho t: Jacobian rho, duffy = rho^2 t
+    rho = x;
+    h = x * tt;
+    duffy = rho * rho * tt;
+  } else {  // h > rho, rho = h t: duffy = h^2
+    h = x;
+    rho = x * tt;
+    duffy = x * x;
+  }
+  const double cos_b = 1.0 - 2.0 * (h * h);
+  const double sin_b = 2.0 * h * sqrt(fmax(1.0 - h * h, 0.0));
+  const double v0 = 1.0 + rho, w0 = 1.0 - rho;
+  const double u0 = 2.0 * sqrt(rho * rho + (1.0 - rho * rho) * (h * h));
+  const double om = 1.0 - rho * rho;
+  const double fgeo = fgeo_c * duffy * (om * om);
+  const double cx = 0.5 * w0 * sin_b, cz = 0.5 * (v0 + w0 * cos_b);
+  const double su = u0 > 0.0 ? u0 : 1.0;
+  const double uhx = -w0 * sin_b / su, uhz = (v0 - w0 * cos_b) / su;
+  const double n1 = fabs(uhx);
+  const bool deg = n1 < 1e-14;
+  const double sn = deg ? 1.0 : n1;
+  const double e1x = deg ? 1.0 : -uhz * uhx / sn;
+  const double e1z = deg ? 0.0 : uhx * uhx / sn;
+  const double e2y = uhz * e1x - uhx * e1z;
+  const double kern = kscale * pow(u0, gamma) / (4.0 * PI);
+  const double v[G_NF] = {rho, cos_b, v0, w0, u0, fgeo, kern, cx, cz, uhx, uhz, e1x, e1z, e2y};
+#pragma unroll
+  for (int f = 0; f < G_NF; ++f) g[(size_t)f * n_ot + i] = v[f];
+}
+
+// Ybar_{l,m}(cos beta) for all (l,m) at every (o,t): yb[lm][ot]
+__global__ void k_ybar_table(const double* g, int n_ot, int L, double* yb) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_ot) return;
+  const double x = g[(size_t)G_COSB * n_ot + i];
+  const double sx = sqrt(fmax((1.0 - x) * (1.0 + x), 0.0));
+  double pmm = 0.28209479177387814347;
+  for (int m = 0; m <= L; ++m) {
+    if (m > 0) pmm = c_yd[m] * sx * pmm;
+    yb[(size_t)lm_index(m, m) * n_ot + i] = pmm;
+    if (m == L) break;
+    double p0 = pmm, p1 = c_ye[m] * x * pmm;
+    yb[(size_t)lm_index(m + 1, m) * n_ot + i] = p1;
+    for (int l = m + 2; l <= L; ++l) {
+      const double p2 = c_ya[l * (LMX + 1) + m] * (x * p1 - c_yb[l * (LMX + 1) + m] * p0);
+      p0 = p1;
+      p1 = p2;
+      yb[(size_t)lm_index(l, m) * n_ot + i] = p1;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ dd arithmetic
+// The reference expands the radial polynomial in monomials (kinematic.py:458-471):
+// core_k = pref sum_j mono[k,j] eta^j g_j is an alternating sum whose terms exceed
+// the result by ~1e3 at n_k = 13, so any rounding in g_j is amplified that much.
+// g_j and the j-sum are therefore carried in double-double (error-free products
+// via FMA); the result then differs from the reference only by the reference's
+// own fp64 rounding ("R-tensor build: accuracy").
+struct dd {
+  double hi, lo;
+};
+__device__ __forceinline__ dd two_prod(double a, double b) {
+  const double p = a * b;
+  return {p, fma(a, b, -p)};
+}
+__device__ __forceinline__ dd two_sum(double a, double b) {
+  const double s = a + b, bb = s - a;
+  return {s, (a - (s - bb)) + (b - bb)};
+}
+__device__ __forceinline__ dd fast_two_sum(double a, double b) {
+  const double s = a + b;
+  return {s, b - (s - a)};
+}
+__device__ __forceinline__ dd dd_add(dd a, dd b) {
+  dd s = two_sum(a.hi, b.hi);
+  const dd t = two_sum(a.lo, b.lo);
+  s.lo += t.hi;
+  s = fast_two_sum(s.hi, s.lo);
+  s.lo += t.lo;
+  return fast_two_sum(s.hi, s.lo);
+}
+__device__ __forceinline__ dd dd_mul(dd a, dd b) {
+  dd p = two_prod(a.hi, b.hi);
+  p.lo = fma(a.hi, b.lo, fma(a.lo, b.hi, p.lo));
+  return fast_two_sum(p.hi, p.lo);
+}
+__device__ __forceinline__ dd dd_mul_d(dd a, double b) {
+  dd p = two_prod(a.hi, b);
+  p.lo = fma(a.lo, b, p.lo);
+  return fast_two_sum(p.hi, p.lo);
+}
+
+// ------------------------------------------------------------------ A tables
+// A[l1,m,j](o,t) = sum_{chi,eps} w_chi w_eps |v'|^l1 (|v'|^2/2)^j Ybar_{l1 m}(cos th') cos(m phi')
+// (double-double).  One CTA per (o,t); the (chi,eps) axis is staged in chunks
+// of blockDim points: phase 1 builds each point's harmonic column and power
+// row, phase 2 accumulates the (l1,m) x j outer-product sums
+// (kinematic.py:366-380, 448-464).
+struct AtabParams {
+  const double* g;
+  int n_ot, L, nk, n_chi, n_eps;
+  const double *chi_x, *chi_w, *eps_c, *eps_s, *eps_w;
+  double *A_hi, *A_lo;  // [lm][j][ot]
+};
+
+__host__ __device__ inline size_t atab_smem(int nlm, int nk, int sc) {
+  return ((size_t)2 * nlm * (sc + 1) + (size_t)2 * sc * nk + (size_t)2 * nlm * nk) * 8;
+}
+
+__global__ void k_atab(AtabParams p) {
+  extern __shared__ double sm[];
+  const int sc = blockDim.x, tid = threadIdx.x, ot = blockIdx.x;
+  const int nlm = lm_index(p.L, p.L) + 1, nk = p.nk, nout = nlm * nk;
+  double* yh = sm;                                  // [nlm][sc+1]
+  double* yl = yh + (size_t)nlm * (sc + 1);
+  double* vh = yl + (size_t)nlm * (sc + 1);         // [sc][nk]
+  double* vl = vh + (size_t)sc * nk;
+  double* ah = vl + (size_t)sc * nk;                // [nlm*nk]
+  double* al = ah + (size_t)nout;
+  const int n_ot = p.n_ot;
+  const double cx = p.g[(size_t)G_CX * n_ot + ot], cz = p.g[(size_t)G_CZ * n_ot + ot];
+  const double hu = 0.5 * p.g[(size_t)G_U0 * n_ot + ot];
+  const double uhx = p.g[(size_t)G_UHX * n_ot + ot], uhz = p.g[(size_t)G_UHZ * n_ot + ot];
+  const double e1x = p.g[(size_t)G_E1X * n_ot + ot], e1z = p.g[(size_t)G_E1Z * n_ot + ot];
+  const double e2y = p.g[(size_t)G_E2Y * n_ot + ot];
+  for (int o = tid; o < nout; o += sc) ah[o] = al[o] = 0.0;
+  const int ns = p.n_chi * p.n_eps;
+  for (int s0 = 0; s0 < ns; s0 += sc) {
+    const int s = s0 + tid;
+    if (s < ns) {
+      const int ic = s / p.n_eps, ie = s - ic * p.n_eps;
+      const double cc = p.chi_x[ic];
+      const double sch = sqrt(fmax(1.0 - cc * cc, 0.0));
+      const double ce = p.eps_c[ie], se = p.eps_s[ie];
+      const double vx = cx + hu * (cc * uhx + sch * ce * e1x);
+      const double vy = hu * sch * se * e2y;
+      const double vz = cz + hu * (cc * uhz + sch * ce * e1z);
+      const double vps = sqrt(vx * vx + vy * vy + vz * vz);
+      const double ctp = fmin(fmax(vps > 0.0 ? vz / vps : 1.0, -1.0), 1.0);
+      const double c1 = cos(atan2(vy, vx));
+      // power row (|v'|^2/2)^j and the weighted radial power w |v'|^l, exact to dd
+      dd step = two_prod(vps, vps);
+      step.hi *= 0.5;
+      step.lo *= 0.5;
+      dd pw = {1.0, 0.0};
+      for (int j = 0; j < nk; ++j) {
+        vh[tid * nk + j] = pw.hi;
+        vl[tid * nk + j] = pw.lo;
+        pw = dd_mul(pw, step);
+      }
+      const dd w = two_prod(p.chi_w[ic], p.eps_w[ie]);
+      // harmonics: m outer, l inner; y = Ybar_lm cos(m phi) rounded as the reference does
+      const double sx = sqrt(fmax((1.0 - ctp) * (1.0 + ctp), 0.0));
+      double pmm = 0.28209479177387814347, cm1 = 1.0, cm2 = 0.0;
+      dd wv = w;  // w |v'|^m at the diagonal
+      for (int m = 0; m <= p.L; ++m) {
+        double cm;
+        if (m == 0) cm = 1.0;
+        else if (m == 1) cm = c1;
+        else cm = 2.0 * c1 * cm1 - cm2;
+        cm2 = cm1;
+        cm1 = cm;
+        if (m > 0) {
+          pmm = c_yd[m] * sx * pmm;
+          wv = dd_mul_d(wv, vps);
+        }
+        dd wl = wv;
+        dd t = dd_mul_d(wl, pmm * cm);
+        yh[(size_t)lm_index(m, m) * (sc + 1) + tid] = t.hi;
+        yl[(size_t)lm_index(m, m) * (sc + 1) + tid] = t.lo;
+        if (m == p.L) break;
+        double p0 = pmm, p1 = c_ye[m] * ctp * pmm;
+        wl = dd_mul_d(wl, vps);
+        t = dd_mul_d(wl, p1 * cm);
+        yh[(size_t)lm_index(m + 1, m) * (sc + 1) + tid] = t.hi;
+        yl[(size_t)lm_index(m + 1, m) * (sc + 1) + tid] = t.lo;
+        for (int l = m + 2; l <= p.L; ++l) {
+          const double p2 = c_ya[l * (LMX + 1) + m] * (ctp * p1 - c_yb[l * (LMX + 1) + m] * p0);
+          p0 = p1;
+          p1 = p2;
+          wl = dd_mul_d(wl, vps);
+          t = dd_mul_d(wl, p1 * cm);
+          yh[(size_t)lm_index(l, m) * (sc + 1) + tid] = t.hi;
+          yl[(size_t)lm_index(l, m) * (sc + 1) + tid] = t.lo;
+        }
+      }
+    } else {
+      for (int j = 0; j < nk; ++j) vh[tid * nk + j] = vl[tid * nk + j] = 0.0;
+      for (int r = 0; r < nlm; ++r) yh[(size_t)r * (sc + 1) + tid] = yl[(size_t)r * (sc + 1) + tid] = 0.0;
+    }
+    __syncthreads();
+    const int cnt = min(sc, ns - s0);
+    for (int o = tid; o < nout; o += sc) {
+      const int r = o / nk, j = o - r * nk;
+      dd a = {ah[o], al[o]};
+      const double* yrh = yh + (size_t)r * (sc + 1);
+      const double* yrl = yl + (size_t)r * (sc + 1);
+      for (int q = 0; q < cnt; ++q)
+        a = dd_add(a, dd_mul({yrh[q], yrl[q]}, {vh[q * nk + j], vl[q * nk + j]}));
+      ah[o] = a.hi;
+      al[o] = a.lo;
+    }
+    __syncthreads();
+  }
+  for (int o = tid; o < nout; o += sc) {
+    p.A_hi[(size_t)o * n_ot + ot] = ah[o];
+    p.A_lo[(size_t)o * n_ot + ot] = al[o];
+  }
+}
+
+// --------------------------------------------------------------- radial/env
+// phi[(l*2 + which)*nk + k][p] at speed sqrt(eta_E) * (1 +- rho)  (basis.py:123-141,
+// kinematic.py:304-319); env[p] = w_E eta^2 exp(-eta rho^2) w_o [w_t f_geo]
+struct RadParams {
+  const double* g;
+  const double *eta, *w_e, *ow, *tw, *norms;
+  int patch, n_e, n_o, n_t, nq, L, nk;
+  long long P, PS;
+  double *phi, *env;
+};
+
+__global__ void k_radial(RadParams p) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= p.P) return;
+  const int E = (int)(i / p.nq), q = (int)(i - (long long)E * p.nq);
+  const int n_ot = p.n_o * p.n_t;
+  const int ot = p.patch == 0 ? q * p.n_t : q;  // patch 0: radial speeds use t = 0 (rho = outer node)
+  const int o = p.patch == 0 ? q : q / p.n_t;
+  const double eta = p.eta[E];
+  const double rho = p.g[(size_t)G_RHO * n_ot + ot];
+  const double se = sqrt(eta);
+  double env = p.w_e[E] * (eta * eta) * exp(-eta * (rho * rho));
+  if (p.patch == 0) env *= p.ow[o];
+  else env *= (p.ow[o] * p.tw[q - o * p.n_t]) * p.g[(size_t)G_FGEO * n_ot + ot];
+  p.env[i] = env;
+  for (int which = 0; which < 2; ++which) {
+    const double v = se * (which == 0 ? p.g[(size_t)G_V0 * n_ot + ot] : p.g[(size_t)G_W0 * n_ot + ot]);
+    const double x = 0.5 * v * v;
+    for (int l = 0; l <= p.L; ++l) {
+      const double a = l + 0.5;
+      const double sc = pow(v, (double)l);
+      double* out = p.phi + (size_t)((l * 2 + which) * p.nk) * p.PS + i;
+      double lm1 = 1.0, lk = 1.0 + a - x;
+      out[0] = p.norms[l * p.nk] * sc * 1.0;
+      if (p.nk > 1) out[(size_t)p.PS] = p.norms[l * p.nk + 1] * sc * lk;
+      for (int k = 1; k < p.nk - 1; ++k) {
+        const double ln = ((2 * k + a + 1 - x) * lk - (k + a) * lm1) / (k + 1);
+        lm1 = lk;
+        lk = ln;
+        out[(size_t)(k + 1) * p.PS] = p.norms[l * p.nk + k + 1] * sc * lk;
+      }
+    }
+  }
+}
+
+// --------------------------------------------------------------- per channel
+// gq[c][j][q] = kern Y_l2(0) sum_m b_m A[l1,m,j]  (patch 1: (o,t); patch 0: the
+// Duffy integral sum_t (.) f_geo w_t folded in, q = o), and the loss kernel
+// lq[c][q] = 2 pi sum(w_chi) kern p_loss (patch 0: Duffy-integrated likewise)
+struct GsParams {
+  const double *g, *A_hi, *A_lo, *yb, *tw, *w3j;
+  const int32_t* trip;
+  int c0, patch, n_o, n_t, nq, L, nk;
+  double swc;  // 2 pi sum(w_chi)
+  double *gq, *lq;
+};
+
+__global__ void k_gstack(GsParams p) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = blockIdx.y;
+  if (q >= p.nq) return;
+  const int tau = p.c0 + c;
+  const int l1 = p.trip[3 * tau], l2 = p.trip[3 * tau + 1], l3 = p.trip[3 * tau + 2];
+  const int mm = min(l1, l3);
+  const int n_ot = p.n_o * p.n_t;
+  const double* w3 = p.w3j + (size_t)tau * (p.L + 1);
+  const double zon1 = sqrt((2 * l1 + 1) / (4.0 * PI)), zon2 = sqrt((2 * l2 + 1) / (4.0 * PI));
+  const int t_n = p.patch == 0 ? p.n_t : 1;
+  for (int j = 0; j < p.nk; ++j) {
+    dd acc = {0.0, 0.0};
+    for (int tt = 0; tt < t_n; ++tt) {
+      const int ot = p.patch == 0 ? q * p.n_t + tt : q;
+      dd s = {0.0, 0.0};
+      for (int m = 0; m <= mm; ++m) {
+        const double w = w3[m];
+        if (w == 0.0) continue;
+        const double fac = (m == 0 ? 1.0 : 2.0) * ((m & 1) ? -1.0 : 1.0);
+        const double b = fac * w * p.yb[(size_t)lm_index(l3, m) * n_ot + ot];
+        const size_t ai = ((size_t)lm_index(l1, m) * p.nk + j) * n_ot + ot;
+        s = dd_add(s, dd_mul_d({p.A_hi[ai], p.A_lo[ai]}, b));
+      }
+      dd gv = dd_mul_d(dd_mul_d(s, zon2), p.g[(size_t)G_KERN * n_ot + ot]);
+      if (p.patch == 0) acc = dd_add(acc, dd_mul_d(dd_mul_d(gv, p.g[(size_t)G_FGEO * n_ot + ot]), p.tw[tt]));
+      else acc = gv;
+    }
+    p.gq[((size_t)c * p.nk + j) * p.nq + q] = acc.hi + acc.lo;
+  }
+  double la = 0.0;
+  for (int tt = 0; tt < t_n; ++tt) {
+    const int ot = p.patch == 0 ? q * p.n_t + tt : q;
+    const double pl = zon1 * zon2 * w3[0] * p.yb[(size_t)lm_index(l3, 0) * n_ot + ot];
+    const double lk = p.swc * p.g[(size_t)G_KERN * n_ot + ot] * pl;
+    if (p.patch == 0) la += p.g[(size_t)G_FGEO * n_ot + ot] * lk * p.tw[tt];
+    else la = lk;
+  }
+  p.lq[(size_t)c * p.nq + q] = la;
+}
+
+// X[c][r][p]: r < nk gain integrand core*env, nk <= r < 2nk fast loss phi_l1(v) lenv,
+// 2nk <= r < 3nk slow loss phi_l1(w) lenv
+struct XrParams {
+  const double *gq, *lq, *me, *pf, *phi, *env;
+  const int32_t* trip;
+  int c0, n_e, nq, nk;
+  long long P, PS;
+  double* X;
+};
+
+template <int NK>
+__global__ void k_xrows(XrParams p) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = blockIdx.y;
+  if (i >= p.P) return;
+  const int nk = NK > 0 ? NK : p.nk;
+  const int tau = p.c0 + c;
+  const int l1 = p.trip[3 * tau];
+  const int E = (int)(i / p.nq), q = (int)(i - (long long)E * p.nq);
+  constexpr int NA = NK > 0 ? NK : NK_MAX;
+  double gj[NA];
+#pragma unroll
+  for (int j = 0; j < NA; ++j) gj[j] = j < nk ? p.gq[((size_t)c * nk + j) * p.nq + q] : 0.0;
+  const double env = p.env[i];
+  const double lenv = env * p.lq[(size_t)c * p.nq + q];
+  const double* me = p.me + ((size_t)l1 * p.n_e + E) * nk * nk;
+  double* X = p.X + (size_t)c * 3 * nk * p.PS + i;
+  const double* pv = p.phi + (size_t)((l1 * 2 + 0) * nk) * p.PS + i;
+  const double* pw = p.phi + (size_t)((l1 * 2 + 1) * nk) * p.PS + i;
+  const double* pf = p.pf + ((size_t)l1 * p.n_e + E) * nk;
+  for (int k = 0; k < nk; ++k) {
+    // compensated dot product (Ogita-Rump-Oishi Dot2) of the alternating monomial sum
+    double s = 0.0, comp = 0.0;
+#pragma unroll
+    for (int j = 0; j < NA; ++j)
+      if (j < nk) {
+        const dd pr = two_prod(me[k * nk + j], gj[j]);
+        const dd sm = two_sum(s, pr.hi);
+        s = sm.hi;
+        comp += pr.lo + sm.lo;
+      }
+    X[(size_t)k * p.PS] = ((s + comp) * pf[k]) * env;
+    X[(size_t)(nk + k) * p.PS] = pv[(size_t)k * p.PS] * lenv;
+    X[(size_t)(2 * nk + k) * p.PS] = pw[(size_t)k * p.PS] * lenv;
+  }
+}
+
+// ------------------------------------------------------------ contraction
+// part[job][split][row][a*nk+b] = sum_{p in split} X[row,p] U[a,p] W[b,p]
+// kind 0: rows = gain + fast loss (2 nk), U = phi_l2(v), W = phi_l3(w)
+// kind 1: rows = slow loss (nk),          U = phi_l2(w), W = phi_l3(v)
+struct TriParams {
+  const double *X, *phi;
+  const int32_t* trip;
+  int c0, nk, kind, S, PR;
+  long long P, PS;
+  double* part;  // [(2c+kind)*S + split][2nk][nk*nk]
+};
+
+template <int MT, int NPW>
+__global__ void __launch_bounds__(256) k_tri(TriParams p) {
+  extern __shared__ double sm[];
+  const int c = blockIdx.y, split = blockIdx.x;
+  const int nk = p.nk, nn = nk * nk, kind = p.kind;
+  const int rows = kind ? nk : 2 * nk;
+  const int rs = rows + 2 * nk;  // staged rows per chunk
+  const int tau = p.c0 + c;
+  const int l2 = p.trip[3 * tau + 1], l3 = p.trip[3 * tau + 2];
+  const double* X = p.X + ((size_t)c * 3 * nk + (kind ? 2 * nk : 0)) * p.PS;
+  const double* U = p.phi + (size_t)((l2 * 2 + kind) * nk) * p.PS;
+  const double* W = p.phi + (size_t)((l3 * 2 + (1 - kind)) * nk) * p.PS;
+  const long long pb = (long long)split * p.PR;
+  const long long pe = min((long long)p.P, pb + p.PR);
+  const int nchunk = (int)((pe - pb + PC - 1) / PC);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r0 = lane >> 2, kq = lane & 3;
+  const int ntiles = (nn + 7) / 8;
+
+  int xoff[MT];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) xoff[mt] = min(mt * 8 + r0, rows - 1) * SROW;
+  int uoff[NPW], woff[NPW];
+#pragma unroll
+  for (int i = 0; i < NPW; ++i) {
+    const int n = min((warp + 8 * i) * 8 + r0, nn - 1);
+    const int a = n / nk, b = n - a * nk;
+    uoff[i] = (rows + a) * SROW;
+    woff[i] = (rows + nk + b) * SROW;
+  }
+  double acc[MT][NPW][2];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int i = 0; i < NPW; ++i) acc[mt][i][0] = acc[mt][i][1] = 0.0;
+
+  const int stage_d = rs * SROW;
+  auto load_chunk = [&](int ch, int st) {
+    const long long p0 = pb + (long long)ch * PC;
+    double* dst = sm + st * stage_d;
+    const int nv = rs * (PC / 2);
+    for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+      const int r = v / (PC / 2), cc = (v - r * (PC / 2)) * 2;
+      const double* src = r < rows ? X + (size_t)r * p.PS
+                                   : (r < rows + nk ? U + (size_t)(r - rows) * p.PS
+                                                    : W + (size_t)(r - rows - nk) * p.PS);
+      const long long pp = p0 + cc;
+      const int bytes = pp + 2 <= pe ? 16 : (pp < pe ? 8 : 0);
+      cp_async16(dst + r * SROW + cc, src + (bytes ? pp : 0), bytes);
+    }
+    cp_async_commit();
+  };
+
+  if (nchunk > 0) load_chunk(0, 0);
+  for (int ch = 0; ch < nchunk; ++ch) {
+    if (ch + 1 < nchunk) {
+      load_chunk(ch + 1, (ch + 1) & 1);
+      cp_async_wait1();
+    } else {
+      cp_async_wait0();
+    }
+    __syncthreads();
+    const double* s = sm + (ch & 1) * stage_d;
+#pragma unroll 2
+    for (int kk = 0; kk < PC / 4; ++kk) {
+      const int col = kk * 4 + kq;
+      double a[MT];
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) a[mt] = s[xoff[mt] + col];
+#pragma unroll
+      for (int i = 0; i < NPW; ++i) {
+        if (warp + 8 * i < ntiles) {
+          const double b = s[uoff[i] + col] * s[woff[i] + col];
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) dmma884(acc[mt][i][0], acc[mt][i][1], a[mt], b);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  double* out = p.part + ((size_t)(2 * c + kind) * p.S + split) * (size_t)(2 * nk * nn);
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) {
+    const int row = mt * 8 + r0;
+    if (row >= rows) continue;
+#pragma unroll
+    for (int i = 0; i < NPW; ++i) {
+      const int tile = warp + 8 * i;
+      if (tile >= ntiles) continue;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int n = tile * 8 + 2 * kq + e;
+        if (n < nn) out[(size_t)row * nn + n] = acc[mt][i][e];
+      }
+    }
+  }
+}
+
+// halves[h][tau][k][ab] += sum over splits (fixed order): h = 0 gain, 1 fast loss, 2 slow loss
+__global__ void k_reduce(const double* part, int c0, int nb, int nk, int S, int n_t, double* halves) {
+  const int nn = nk * nk;
+  const long long tot = (long long)nb * 3 * nk * nn;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= tot) return;
+  const int ab = (int)(i % nn);
+  const int r = (int)((i / nn) % (3 * nk));
+  const int c = (int)(i / ((long long)nn * 3 * nk));
+  const int kind = r >= 2 * nk;
+  const int row = kind ? r - 2 * nk : r;
+  const double* src = part + ((size_t)(2 * c + kind) * S) * (size_t)(2 * nk * nn) + (size_t)row * nn + ab;
+  double s = 0.0;
+  for (int sp = 0; sp < S; ++sp) s += src[(size_t)sp * 2 * nk * nn];
+  const int h = r / nk, k = r - h * nk;
+  halves[(((size_t)h * n_t + c0 + c) * nk + k) * nn + ab] += s;
+}
+
+// full[tau] = gain[tau] + gain[swap]^T(2,3) - (loss_f + loss_s)[tau]  (kinematic.py:552-558)
+__global__ void k_full(const double* halves, const int32_t* swap, int n_t, int nk, double* full) {
+  const int nn = nk * nk, n3 = nn * nk;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)n_t * n3) return;
+  const int tau = (int)(i / n3), r = (int)(i - (long long)tau * n3);
+  const int k = r / nn, a = (r / nk) % nk, b = r % nk;
+  const size_t hs = (size_t)n_t * n3;
+  const double g = halves[i];
+  const double gs = halves[(size_t)swap[tau] * n3 + (size_t)k * nn + b * nk + a];
+  const double lf = halves[hs + i], ls = halves[2 * hs + i];
+  full[i] = g + gs - (lf + ls);
+}
+
+// R[k][a][b][tau] = scale * 0.5 (full[tau] + full[swap]^T)  (kinematic.py:559-569)
+__global__ void k_final(const double* full, const int32_t* swap, const double* scale, int n_t, int nk,
+                        double* r) {
+  const int nn = nk * nk, n3 = nn * nk;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)n_t * n3) return;
+  const int tau = (int)(i / n3), rr = (int)(i - (long long)tau * n3);
+  const int k = rr / nn, a = (rr / nk) % nk, b = rr % nk;
+  const double f = full[i];
+  const double fs = full[(size_t)swap[tau] * n3 + (size_t)k * nn + b * nk + a];
+  r[(size_t)rr * n_t + tau] = scale[tau] * (0.5 * (f + fs));
+}
+
+// ---------------------------------------------------------------- host side
+typedef void (*TriKernel)(TriParams);
+
+template <int MT>
+TriKernel pick_tri_npw(int npw) {
+  switch (npw) {
+    case 1: return k_tri<MT, 1>;
+    case 2: return k_tri<MT, 2>;
+    case 3: return k_tri<MT, 3>;
+    case 4: return k_tri<MT, 4>;
+    case 5: return k_tri<MT, 5>;
+  }
+  return nullptr;
+}
+
+TriKernel pick_tri(int mt, int npw) {
+  switch (mt) {
+    case 1: return pick_tri_npw<1>(npw);
+    case 2: return pick_tri_npw<2>(npw);
+    case 3: return pick_tri_npw<3>(npw);
+    case 4: return pick_tri_npw<4>(npw);
+    case 5: return pick_tri_npw<5>(npw);
+  }
+  return nullptr;
+}
+
+typedef void (*XrKernel)(XrParams);
+XrKernel pick_xrows(int nk) {
+  switch (nk) {
+    case 3: return k_xrows<3>;
+    case 5: return k_xrows<5>;
+    case 7: return k_xrows<7>;
+    case 9: return k_xrows<9>;
+    case 11: return k_xrows<11>;
+    case 13: return k_xrows<13>;
+    case 15: return k_xrows<15>;
+    case 17: return k_xrows<17>;
+  }
+  return k_xrows<0>;
+}
+
+struct DevBuf {
+  std::vector<void*> ptrs;
+  ~DevBuf() {
+    for (void* q : ptrs) cudaFree(q);
+  }
+  template <class T>
+  T* alloc(size_t n) {
+    void* q = nullptr;
+    if (cudaMalloc(&q, std::max<size_t>(n, 1) * sizeof(T)) != cudaSuccess) return nullptr;
+    ptrs.push_back(q);
+    return (T*)q;
+  }
+  void release(void* q) {
+    for (auto& x : ptrs)
+      if (x == q) {
+        cudaFree(x);
+        x = nullptr;
+      }
+  }
+};
+
+template <class T>
+int upload(DevBuf& db, const T* host, size_t n, T** out) {
+  *out = db.alloc<T>(n);
+  if (!*out) {
+    set_error("device allocation failed");
+    return BFQ_ENOMEM;
+  }
+  if (n && cudaMemcpy(*out, host, n * sizeof(T), cudaMemcpyHostToDevice) != cudaSuccess) {
+    set_error("host-to-device copy failed");
+    return BFQ_ECUDA;
+  }
+  return BFQ_OK;
+}
+
+int set_ybar_constants() {
+  static bool done = false;  // device-independent values, but constant memory is per device
+  (void)done;
+  std::vector<double> ya((LMX + 1) * (LMX + 1), 0.0), yb((LMX + 1) * (LMX + 1), 0.0), yd(LMX + 1, 0.0),
+      ye(LMX + 1, 0.0);
+  for (int m = 0; m <= LMX; ++m) {
+    yd[m] = m > 0 ? -std::sqrt((2.0 * m + 1.0) / (2.0 * m)) : 1.0;
+    ye[m] = std::sqrt(2.0 * m + 3.0);
+    for (int l = m + 2; l <= LMX; ++l) {
+      const double l2 = (double)l * l, m2 = (double)m * m, lp = (double)(l - 1) * (l - 1);
+      ya[l * (LMX + 1) + m] = std::sqrt((4.0 * l2 - 1.0) / (l2 - m2));
+      yb[l * (LMX + 1) + m] = std::sqrt((lp - m2) / (4.0 * lp - 1.0));
+    }
+  }
+  if (cudaMemcpyToSymbol(c_ya, ya.data(), ya.size() * 8) != cudaSuccess ||
+      cudaMemcpyToSymbol(c_yb, yb.data(), yb.size() * 8) != cudaSuccess ||
+      cudaMemcpyToSymbol(c_yd, yd.data(), yd.size() * 8) != cudaSuccess ||
+      cudaMemcpyToSymbol(c_ye, ye.data(), ye.size() * 8) != cudaSuccess) {
+    set_error("constant upload failed");
+    return BFQ_ECUDA;
+  }
+  return BFQ_OK;
+}
+
+#define BFR_TRY(expr)                                                               \
+  do {                                                                              \
+    cudaError_t e_ = (expr);                                                        \
+    if (e_ != cudaSuccess) {                                                        \
+      set_error(std::string(#expr) + ": " + cudaGetErrorString(e_));               \
+      return BFQ_ECUDA;                                                             \
+    }                                                                               \
+  } while (0)
+
+#define BFR_LAUNCH_CHECK(name)                                                      \
+  do {                                                                              \
+    cudaError_t e_ = cudaGetLastError();                                            \
+    if (e_ != cudaSuccess) {                                                        \
+      set_error(std::string("kernel launch " name ": ") + cudaGetErrorString(e_));  \
+      return BFQ_ECUDA;                                                             \
+    }                                                                               \
+  } while (0)
+
+inline unsigned blocks_for(long long n, int bs) { return (unsigned)((n + bs - 1) / bs); }
+
+int assemble(const bfr_desc& d, int device, double* r_out, double* halves_out, bfr_stats* st) {
+  const int L = d.l_max, nk = d.k_max + 1, n_t = d.n_t;
+  const int nlm = lm_index(L, L) + 1, nn = nk * nk, n3 = nn * nk;
+  int ndev = 0;
+  BFR_TRY(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) {
+    set_error("device ordinal out of range");
+    return BFQ_EINVAL;
+  }
+  BFR_TRY(cudaSetDevice(device));
+  int rc;
+  if ((rc = set_ybar_constants())) return rc;
+  DevBuf db;
+  int32_t *d_trip, *d_swap;
+  double *d_w3j, *d_scale, *d_eta, *d_we, *d_chix, *d_chiw, *d_epsc, *d_epss, *d_epsw, *d_norms, *d_me;
+  (void)d_norms;
+  if ((rc = upload(db, d.triplets, (size_t)3 * n_t, &d_trip))) return rc;
+  if ((rc = upload(db, d.swap, (size_t)n_t, &d_swap))) return rc;
+  if ((rc = upload(db, d.w3j, (size_t)n_t * (L + 1), &d_w3j))) return rc;
+  if ((rc = upload(db, d.chan_scale, (size_t)n_t, &d_scale))) return rc;
+  if ((rc = upload(db, d.e_x, (size_t)d.n_e, &d_eta))) return rc;
+  if ((rc = upload(db, d.e_w, (size_t)d.n_e, &d_we))) return rc;
+  if ((rc = upload(db, d.chi_x, (size_t)d.n_chi, &d_chix))) return rc;
+  if ((rc = upload(db, d.chi_w, (size_t)d.n_chi, &d_chiw))) return rc;
+  std::vector<double> ec(d.n_eps), es(d.n_eps);
+  for (int i = 0; i < d.n_eps; ++i) {
+    ec[i] = std::cos(d.eps_x[i]);
+    es[i] = std::sin(d.eps_x[i]);
+  }
+  if ((rc = upload(db, ec.data(), ec.size(), &d_epsc))) return rc;
+  if ((rc = upload(db, es.data(), es.size(), &d_epss))) return rc;
+  if ((rc = upload(db, d.eps_w, (size_t)d.n_eps, &d_epsw))) return rc;
+  if ((rc = upload(db, d.norms, (size_t)(L + 1) * nk, &d_norms))) return rc;
+  // me[l][E][k][j] = mono[l][k][j] * eta_E^j and pf[l][E][k] = norms[l][k] * eta_E^(l/2),
+  // rounded exactly as the reference's einsum operands (kinematic.py:466-471)
+  double* d_pf;
+  {
+    std::vector<double> me((size_t)(L + 1) * d.n_e * nn), pf((size_t)(L + 1) * d.n_e * nk);
+    for (int l = 0; l <= L; ++l)
+      for (int E = 0; E < d.n_e; ++E) {
+        const double eta = d.e_x[E];
+        const double eh = l == 0 ? 1.0 : std::pow(eta, 0.5 * l);
+        for (int k = 0; k < nk; ++k) {
+          pf[((size_t)l * d.n_e + E) * nk + k] = d.norms[l * nk + k] * eh;
+          for (int j = 0; j < nk; ++j) {
+            const double ep = j == 0 ? 1.0 : (j == 1 ? eta : std::pow(eta, (double)j));
+            me[(((size_t)l * d.n_e + E) * nk + k) * nk + j] = d.mono[((size_t)l * nk + k) * nk + j] * ep;
+          }
+        }
+      }
+    if ((rc = upload(db, me.data(), me.size(), &d_me))) return rc;
+    if ((rc = upload(db, pf.data(), pf.size(), &d_pf))) return rc;
+  }
+  double swc = 0.0;
+  for (int i = 0; i < d.n_chi; ++i) swc += d.chi_w[i];
+  swc = swc * 2.0 * PI;
+  const double fgeo_c = 4.0 * std::pow(2.0 * PI, -3.0);
+
+  double* halves = db.alloc<double>((size_t)3 * n_t * n3);
+  double* full = db.alloc<double>((size_t)n_t * n3);
+  double* rdev = db.alloc<double>((size_t)n_t * n3);
+  if (!halves || !full || !rdev) {
+    set_error("device allocation failed");
+    return BFQ_ENOMEM;
+  }
+  BFR_TRY(cudaMemset(halves, 0, (size_t)3 * n_t * n3 * 8));
+
+  cudaEvent_t ev0, ev1, ta, tb;
+  BFR_TRY(cudaEventCreate(&ev0));
+  BFR_TRY(cudaEventCreate(&ev1));
+  BFR_TRY(cudaEventCreate(&ta));
+  BFR_TRY(cudaEventCreate(&tb));
+  struct EvGuard {
+    cudaEvent_t e[4];
+    ~EvGuard() {
+      for (auto x : e) cudaEventDestroy(x);
+    }
+  } evg{{ev0, ev1, ta, tb}};
+  BFR_TRY(cudaEventRecord(ev0));
+  double ms_contract = 0.0, exec_macs = 0.0, alg_macs = 0.0, xbytes = 0.0;
+
+  const int mt0 = (2 * nk + 7) / 8, mt1 = (nk + 7) / 8, npw = ((nn + 7) / 8 + 7) / 8;
+  TriKernel tri0 = pick_tri(mt0, npw), tri1 = pick_tri(mt1, npw);
+  if (!tri0 || !tri1) {
+    set_error("n_k outside the contraction kernel's tiling (n_k <= 17)");
+    return BFQ_EINVAL;
+  }
+  const size_t tri_smem0 = (size_t)2 * (2 * nk + 2 * nk) * SROW * 8;
+  const size_t tri_smem1 = (size_t)2 * (nk + 2 * nk) * SROW * 8;
+  // tri0 and tri1 may be the same instantiation (small n_k): give both the larger size
+  BFR_TRY(cudaFuncSetAttribute(tri0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tri_smem0));
+  if (tri1 != tri0)
+    BFR_TRY(cudaFuncSetAttribute(tri1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tri_smem1));
+  XrKernel xr = pick_xrows(nk);
+
+  for (int patch = 0; patch < 2; ++patch) {
+    const int n_o = d.n_outer[patch], n_tt = d.n_inner[patch], n_ot = n_o * n_tt;
+    const int nq = patch == 0 ? n_o : n_ot;
+    const long long P = (long long)d.n_e * nq, PS = (P + 3) / 4 * 4;
+    if (st) st->n_points[patch] = P;
+    double *d_ox, *d_ow, *d_tx, *d_tw;
+    if ((rc = upload(db, d.outer_x[patch], (size_t)n_o, &d_ox))) return rc;
+    if ((rc = upload(db, d.outer_w[patch], (size_t)n_o, &d_ow))) return rc;
+    if ((rc = upload(db, d.inner_x[patch], (size_t)n_tt, &d_tx))) return rc;
+    if ((rc = upload(db, d.inner_w[patch], (size_t)n_tt, &d_tw))) return rc;
+    double* geo = db.alloc<double>((size_t)G_NF * n_ot);
+    double* yb = db.alloc<double>((size_t)nlm * n_ot);
+    double* A = db.alloc<double>((size_t)2 * nlm * nk * n_ot);  // hi, lo
+    double* env = db.alloc<double>((size_t)PS);
+    double* phi = db.alloc<double>((size_t)(L + 1) * 2 * nk * PS);
+    if (!geo || !yb || !A || !env || !phi) {
+      set_error("device allocation failed");
+      return BFQ_ENOMEM;
+    }
+    BFR_TRY(cudaMemset(phi, 0, (size_t)(L + 1) * 2 * nk * PS * 8));
+    k_geom<<<blocks_for(n_ot, 128), 128>>>(patch, d_ox, d_tx, n_o, n_tt, d.gamma, d.kernel_scale, fgeo_c,
+                                           geo);
+    BFR_LAUNCH_CHECK("k_geom");
+    k_ybar_table<<<blocks_for(n_ot, 128), 128>>>(geo, n_ot, L, yb);
+    BFR_LAUNCH_CHECK("k_ybar_table");
+    {
+      AtabParams ap{geo, n_ot, L, nk, d.n_chi, d.n_eps, d_chix, d_chiw, d_epsc, d_epss, d_epsw,
+                    A, A + (size_t)nlm * nk * n_ot};
+      int sc = 64;
+      while (atab_smem(nlm, nk, sc) > 200 * 1024 && sc > 16) sc /= 2;
+      const size_t smem = atab_smem(nlm, nk, sc);
+      BFR_TRY(cudaFuncSetAttribute(k_atab, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      k_atab<<<n_ot, sc, smem>>>(ap);
+      BFR_LAUNCH_CHECK("k_atab");
+    }
+    {
+      RadParams rp{geo, d_eta, d_we, d_ow, d_tw, d_norms, patch, d.n_e, n_o, n_tt, nq, L, nk, P, PS, phi, env};
+      k_radial<<<blocks_for(P, 128), 128>>>(rp);
+      BFR_LAUNCH_CHECK("k_radial");
+    }
+    // channel batches: X scratch <= ~6 GB
+    const size_t xrow_bytes = (size_t)3 * nk * PS * 8;
+    int nb = (int)std::max<size_t>(1, std::min<size_t>((size_t)n_t, ((size_t)6 << 30) / xrow_bytes));
+    const int PR = P >= 16384 * 4 ? 16384 : (int)((P + PC - 1) / PC * PC);
+    const int S = (int)((P + PR - 1) / PR);
+    double* X = db.alloc<double>((size_t)nb * 3 * nk * PS);
+    double* gq = db.alloc<double>((size_t)nb * nk * nq);
+    double* lq = db.alloc<double>((size_t)nb * nq);
+    double* part = db.alloc<double>((size_t)nb * 2 * S * 2 * nk * nn);
+    if (!X || !gq || !lq || !part) {
+      set_error("device allocation failed");
+      return BFQ_ENOMEM;
+    }
+    BFR_TRY(cudaMemset(X, 0, (size_t)nb * 3 * nk * PS * 8));
+    for (int c0 = 0; c0 < n_t; c0 += nb) {
+      const int cb = std::min(nb, n_t - c0);
+      GsParams gp{geo, A, A + (size_t)nlm * nk * n_ot, yb, d_tw, d_w3j, d_trip, c0, patch, n_o, n_tt, nq, L, nk, swc, gq, lq};
+      k_gstack<<<dim3(blocks_for(nq, 128), cb), 128>>>(gp);
+      BFR_LAUNCH_CHECK("k_gstack");
+      XrParams xp{gq, lq, d_me, d_pf, phi, env, d_trip, c0, d.n_e, nq, nk, P, PS, X};
+      xr<<<dim3(blocks_for(P, 128), cb), 128>>>(xp);
+      BFR_LAUNCH_CHECK("xr");
+      BFR_TRY(cudaEventRecord(ta));
+      TriParams tp{X, phi, d_trip, c0, nk, 0, S, PR, P, PS, part};
+      tri0<<<dim3(S, cb), 256, tri_smem0>>>(tp);
+      BFR_LAUNCH_CHECK("tri0");
+      tp.kind = 1;
+      tri1<<<dim3(S, cb), 256, tri_smem1>>>(tp);
+      BFR_LAUNCH_CHECK("tri1");
+      BFR_TRY(cudaEventRecord(tb));
+      k_reduce<<<blocks_for((long long)cb * 3 * nk * nn, 256), 256>>>(part, c0, cb, nk, S, n_t, halves);
+      BFR_LAUNCH_CHECK("k_reduce");
+      BFR_TRY(cudaEventSynchronize(tb));
+      float ms = 0.f;
+      BFR_TRY(cudaEventElapsedTime(&ms, ta, tb));
+      ms_contract += ms;
+      exec_macs += (double)cb * (double)S * PR * 8.0 * 8.0 *
+                   ((double)mt0 * ((nn + 7) / 8) + (double)mt1 * ((nn + 7) / 8));
+      alg_macs += (double)cb * P * 3.0 * nk * nn;
+      xbytes += (double)cb * 3 * nk * P * 8.0 * 2.0;
+    }
+    db.release(X);
+    db.release(part);
+    db.release(phi);
+    db.release(A);
+  }
+  k_full<<<blocks_for((long long)n_t * n3, 256), 256>>>(halves, d_swap, n_t, nk, full);
+  BFR_LAUNCH_CHECK("k_full");
+  k_final<<<blocks_for((long long)n_t * n3, 256), 256>>>(full, d_swap, d_scale, n_t, nk, rdev);
+  BFR_LAUNCH_CHECK("k_final");
+  BFR_TRY(cudaEventRecord(ev1));
+  BFR_TRY(cudaEventSynchronize(ev1));
+  float ms_tot = 0.f;
+  BFR_TRY(cudaEventElapsedTime(&ms_tot, ev0, ev1));
+  BFR_TRY(cudaMemcpy(r_out, rdev, (size_t)n_t * n3 * 8, cudaMemcpyDeviceToHost));
+  if (halves_out) BFR_TRY(cudaMemcpy(halves_out, halves, (size_t)3 * n_t * n3 * 8, cudaMemcpyDeviceToHost));
+  if (st) {
+    st->ms_total = ms_tot;
+    st->ms_contract = ms_contract;
+    st->contract_macs = exec_macs;
+    st->alg_macs = alg_macs;
+    st->x_bytes = xbytes;
+  }
+  return BFQ_OK;
+}
+
+}  // namespace
+
+extern "C" int bfr_assemble(const bfr_desc* desc, int device, double* r_out, double* halves,
+                            bfr_stats* stats) {
+  if (!desc || !r_out) {
+    set_error("null argument");
+    return BFQ_EINVAL;
+  }
+  const bfr_desc& d = *desc;
+  if (d.k_max < 0 || d.l_max < 0 || d.l_max > LMX || d.k_max + 1 > NK_MAX || d.n_t <= 0 || d.n_e <= 0 ||
+      d.n_chi <= 0 || d.n_eps <= 0 || !d.triplets || !d.swap || !d.w3j || !d.chan_scale || !d.e_x ||
+      !d.e_w || !d.chi_x || !d.chi_w || !d.eps_x || !d.eps_w || !d.mono || !d.norms) {
+    set_error("invalid R-assembly descriptor (k_max+1 <= 17, l_max <= 24, all tables required)");
+    return BFQ_EINVAL;
+  }
+  for (int p = 0; p < 2; ++p)
+    if (d.n_outer[p] <= 0 || d.n_inner[p] <= 0 || !d.outer_x[p] || !d.outer_w[p] || !d.inner_x[p] ||
+        !d.inner_w[p]) {
+      set_error("invalid patch rule");
+      return BFQ_EINVAL;
+    }
+  for (int t = 0; t < d.n_t; ++t) {
+    const int* tr = d.triplets + 3 * t;
+    if (tr[0] < 0 || tr[1] < 0 || tr[2] < 0 || tr[0] > d.l_max || tr[1] > d.l_max || tr[2] > d.l_max ||
+        d.swap[t] < 0 || d.swap[t] >= d.n_t) {
+      set_error("channel table out of range");
+      return BFQ_EINVAL;
+    }
+  }
+  if (stats) std::memset(stats, 0, sizeof(*stats));
+  return assemble(d, device, r_out, halves, stats);
+}

@@ -14,6 +14,7 @@ reference so that either object can be handed to :mod:`.engine`:
 * ``RTensor``            -- kinematic.py:241-255
 * ``FactorizedOperator`` -- contraction.py:76-108 (validation, 0-based views)
 * ``load_cache``         -- cache.py:92-166 (BFCT reader, CRC-32 checked)
+* ``save_cache``         -- cache.py:52-89 (BFCT writer, same layout)
 """
 
 from __future__ import annotations
@@ -38,6 +39,7 @@ __all__ = [
     "q_degree",
     "moments",
     "load_cache",
+    "save_cache",
 ]
 
 
@@ -173,6 +175,7 @@ class RTensor:
     grid: tuple = ()
     conservation_applied: bool = False
     detailed_balance_applied: bool = False
+    max_zeroed: float = 0.0  # largest magnitude overwritten by the corrections
 
     @property
     def n_k(self) -> int:
@@ -268,3 +271,25 @@ def load_cache(path) -> FactorizedOperator:
     coo = GauntCOO(l_max, n_q, channels, q1, q2, q3, tau, g, starts, s_tau, s_q1)
     r = RTensor(values, channels, gamma, grid, bool(flags & 1), bool(flags & 2))
     return FactorizedOperator(r, coo, SpectralConfig(k_max, l_max, gamma))
+
+
+def save_cache(path, op: FactorizedOperator) -> int:
+    """Serialise an operator in the reference's BFCT layout (cache.py:52-89);
+    returns the number of bytes written.  The reference's ``load_cache`` reads it."""
+    chans = np.asarray(op.g.channels.triplets, dtype="<u4")
+    payload = b"".join([
+        chans.tobytes(),
+        *(np.asarray(c).astype("<u4").tobytes() for c in (op.g.q1, op.g.q2, op.g.q3, op.g.tau)),
+        np.asarray(op.g.g).astype("<f8").tobytes(),
+        np.ascontiguousarray(op.r.values).astype("<f8").tobytes(),
+    ])
+    flags = (1 if op.r.conservation_applied else 0) | (2 if op.r.detailed_balance_applied else 0)
+    grid = tuple(op.r.grid) if op.r.grid else (0,) * 9
+    if len(grid) != 9:
+        raise ValueError("operator grid spec must have 9 entries")
+    header = _HDR.pack(_MAGIC, 1, op.cfg.k_max, op.cfg.l_max, float(op.cfg.gamma), *grid,
+                       op.g.channels.n_t, op.g.n_g, flags, zlib.crc32(payload) & 0xFFFFFFFF)
+    with open(path, "wb") as fh:
+        fh.write(header)
+        fh.write(payload)
+    return len(header) + len(payload)

@@ -1,4 +1,4 @@
-"""The C-ABI library loads and exports exactly what include/bfq.h declares."""
+"""The C-ABI library loads and exports exactly what include/bfq.h and bfr.h declare."""
 
 import os
 import re
@@ -7,9 +7,9 @@ from conftest import ROOT
 from paper_2605_28475_b200 import _lib
 
 
-def header_functions():
-    text = open(os.path.join(ROOT, "include", "bfq.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(bfq_\w+)\s*\(", text, re.M)))
+def header_functions(header="bfq.h", prefix="bfq"):
+    text = open(os.path.join(ROOT, "include", header)).read()
+    return sorted(set(re.findall(rf"^\s*(?:int|const char\*)\s+({prefix}_\w+)\s*\(", text, re.M)))
 
 
 def test_library_exports_every_header_symbol():
@@ -19,6 +19,11 @@ def test_library_exports_every_header_symbol():
     for name in names:
         assert hasattr(lib, name), name
     assert sorted(_lib.EXPORTED_SYMBOLS) == names
+    bfr = header_functions("bfr.h", "bfr")
+    assert bfr, "no functions parsed from bfr.h"
+    for name in bfr:
+        assert hasattr(lib, name), name
+    assert sorted(_lib.EXPORTED_SYMBOLS_BFR) == bfr
 
 
 def test_strerror_codes():
