@@ -19,7 +19,7 @@ not speed:
   kinematic.py:513-570;
 * null-space corrections -- kinematic.py:594-620.
 
-Parity of this restatement is pinned by ``tests/test_rbuild_oracle.py``
+Parity of this restatement is pinned by ``tests/test_rbuild.py``
 against the R tensors of the reference-built operator caches in
 ``operators/`` (``boltzfact build``; the cache stores R after the
 corrections).
@@ -237,9 +237,15 @@ class Patch:
 
 
 class Assembly:
-    """kinematic.py:383-406 context + :408-510 half-plane integrals."""
+    """kinematic.py:383-406 context + :408-510 half-plane integrals.
 
-    def __init__(self, k_max, l_max, gamma, grid, kernel_scale=1.0):
+    ``precision="ld"`` evaluates the gain integrand from the m-sum through the
+    monomial radial expansion (kinematic.py:427-471) in numpy long double
+    (64-bit mantissa) -- a higher-precision restatement used to measure the
+    reference's own fp64 rounding there (tests/precision/)."""
+
+    def __init__(self, k_max, l_max, gamma, grid, kernel_scale=1.0, precision="f64"):
+        self.precision = precision
         n_e, n_r1, n_t1, n_h2, n_t2, n_chi, n_eps = grid[:7]
         self.n_k, self.l_max, self.gamma, self.ks = k_max + 1, l_max, gamma, kernel_scale
         self.eta, self.w_e = gauss_laguerre_gen(n_e, 0.5 * gamma)
@@ -262,6 +268,8 @@ class Assembly:
 
     def patch_half(self, geo, l1, l2, l3):
         n_k, eta = self.n_k, self.eta
+        if self.precision == "ld":
+            return self._patch_half_ld(geo, l1, l2, l3)
         p_gain = np.zeros_like(geo.vps)
         for m in range(min(l1, l3) + 1):
             w3 = wigner3j(l1, l2, l3, m, 0, -m)
@@ -303,6 +311,46 @@ class Assembly:
         ls = np.einsum("kEot,aEot,bEot,Eot->kab", r[l1, "w"], r[l2, "w"], r[l3, "v"], lenv)
         return gain, lf, ls
 
+    def _patch_half_ld(self, geo, l1, l2, l3):
+        LD = np.longdouble
+        n_k, eta = self.n_k, self.eta
+        p_gain = np.zeros(geo.vps.shape, dtype=LD)
+        for m in range(min(l1, l3) + 1):
+            w3 = wigner3j(l1, l2, l3, m, 0, -m)
+            if w3 == 0.0:
+                continue
+            b = (1.0 if m == 0 else 2.0) * (-1.0) ** m * w3 * sph_theta(l3, m, geo.cos_b)
+            y = sph_theta(l1, m, geo.cos_tp) * geo.cos_m_phi(m)
+            p_gain = p_gain + b[None, None].astype(LD) * y.astype(LD)
+        p_gain *= LD(zonal(l2))
+        vps = geo.vps.astype(LD)
+        kern = (self.ks * geo.u0**self.gamma / (4.0 * math.pi)).astype(LD)
+        pw, step = vps**l1, LD(0.5) * vps**2
+        gs = np.empty((n_k,) + geo.u0.shape, dtype=LD)
+        for j in range(n_k):
+            if j > 0:
+                pw = pw * step
+            s = np.einsum("cest,e->cst", pw * p_gain, geo.w_eps.astype(LD))
+            gs[j] = np.einsum("cst,c->st", s, geo.w_chi.astype(LD)) * kern
+        pref = (self.norms[l1][:, None] * eta ** (0.5 * l1)).astype(LD)
+        core = np.einsum("kj,jE,jot->kEot", self.mono[l1].astype(LD), self.eta_pow.astype(LD), gs)
+        core = (core * pref[:, :, None, None]).astype(np.float64)
+        self.precision = "f64"
+        try:
+            _, lf, ls = self.patch_half(geo, l1, l2, l3)
+        finally:
+            self.precision = "ld"
+        r2v, r3w = self._radial(geo, l2, "v"), self._radial(geo, l3, "w")
+        if geo.patch == 1:
+            env = self.w_e[:, None] * eta[:, None] ** 2 * np.exp(-eta[:, None] * geo.rho[:, 0][None] ** 2) \
+                * geo.wo[None, :]
+            theta = np.tensordot(core * geo.f_geo[None, None], geo.wt, axes=(3, 0))
+            return np.einsum("kEo,aEo,bEo,Eo->kab", theta, r2v, r3w, env), lf, ls
+        env = self.w_e[:, None, None] * eta[:, None, None] ** 2 \
+            * np.exp(-eta[:, None, None] * geo.rho[None] ** 2) \
+            * (geo.wo[:, None] * geo.wt[None, :] * geo.f_geo)[None]
+        return np.einsum("kEot,aEot,bEot,Eot->kab", core, r2v, r3w, env), lf, ls
+
     def channel_half(self, l1, l2, l3):
         """kinematic.py:390-406: both patches."""
         out = [np.zeros((self.n_k,) * 3) for _ in range(3)]
@@ -319,14 +367,14 @@ def channel_scale(l1, l2, l3):
 
 
 def assemble_r(k_max, l_max, gamma, grid=None, kernel_scale=1.0, conservation=True,
-               detailed_balance=True, only=None):
+               detailed_balance=True, only=None, precision="f64"):
     """kinematic.py:521-570 + 594-620 -> R (n_k, n_k, n_k, N_T).
 
     ``only``: optional list of 0-based channel indices; the others stay NaN
     (for spot checks at sizes where the full assembly is too slow).
     """
     grid = grid or grid_sizes(k_max, l_max)
-    ctx = Assembly(k_max, l_max, gamma, grid, kernel_scale)
+    ctx = Assembly(k_max, l_max, gamma, grid, kernel_scale, precision)
     trip = channels(l_max)
     look = {t: i for i, t in enumerate(trip)}
     n_k, n_t = k_max + 1, len(trip)

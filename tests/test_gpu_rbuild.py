@@ -116,7 +116,7 @@ def test_build_operator_drives_q_to_reference_golden(tmp_path):
         q = engine.evaluate_batch(op, torch.from_numpy(g["cells"]).cuda()).cpu().numpy()
         for qi, qr in zip(q, g["q"]):
             assert np.abs(qi - qr).max() / np.abs(qr).max() <= 1e-12
-            mass, mom, en = moments(qi)
+            mass, mom, en = moments(CoefficientField(qi, ref.cfg))
             assert mass == 0.0 and np.all(mom == 0.0) and en == 0.0
         eq = CoefficientField.equilibrium(ref.cfg)
         assert np.abs(engine.evaluate(op, eq, "gpu").values).max() == 0.0
