@@ -35,7 +35,15 @@ CONFIGS = {
     "rk4": ("mm_n10", 32768, "bimodal", "config5: Maxwell N=L=10, bimodal cells, GPU-resident RK4 dt=0.01 "
                                          "(one step = one RK4 step = 4 Q(f,f) per cell)"),
 }
+# the operator build.  One step = one full R-tensor
+# assembly (every channel's gain / loss integrals over both Duffy patches).
+RBUILD = {
+    "rbuild8": (8, 8, 1.0),
+    "rbuild12": (12, 12, 1.0),
+    "rbuild16": (16, 16, 1.0),
+}
 METRIC = "Q(f,f) cell-evals/s (fp64, hard spheres L=N=12) and FP64/HBM roofline frac"
+RBUILD_METRIC = "R-tensor assembly channel integrals/s (fp64, hard spheres, pad 16/16)"
 FP64_PEAK_TFLOPS = 37.1  # DMMA.8x8x4 sustained, measured on this pool (profiles/fp64_peak.txt)
 
 
@@ -109,6 +117,51 @@ def cpu_port_rate(cfg_name, cells, budget_s=15.0, cores=None):
             "single_cell_s": dt1}
 
 
+def _rbuild_cpu_worker(args):
+    k_max, l_max, gamma, grid, taus = args
+    from oracle import r_oracle
+
+    try:
+        from threadpoolctl import threadpool_limits
+    except ImportError:  # pragma: no cover
+        threadpool_limits = None
+    ctx = threadpool_limits(limits=1) if threadpool_limits else None
+    if ctx:
+        ctx.__enter__()
+    asm = r_oracle.Assembly(k_max, l_max, gamma, grid)
+    trip = r_oracle.channels(l_max)
+    t0 = time.perf_counter()
+    for t in taus:
+        asm.channel_half(*trip[t])
+    dt = time.perf_counter() - t0
+    if ctx:
+        ctx.__exit__(None, None, None)
+    return len(taus), dt
+
+
+def rbuild_cpu_rate(config, per_core=1, cores=None):
+    """Oracle port of kinematic.channel_half (the reference's per-channel work) on
+    host cores, one thread per process: channel integrals/s (init excluded)."""
+    import multiprocessing as mp
+
+    from paper_2605_28475_b200 import rbuild
+
+    k, l, gam = RBUILD[config]
+    grid = rbuild.grid_sizes(k, l).as_tuple()[:7]
+    n_t = rbuild.enumerate_channels(l).n_t
+    cores = cores or os.cpu_count() or 1
+    rng = __import__("random").Random(7)
+    taus = rng.sample(range(n_t), min(n_t, per_core * cores))
+    chunks = [(k, l, gam, grid, taus[i::cores]) for i in range(cores) if taus[i::cores]]
+    t0 = time.perf_counter()
+    with mp.get_context("spawn").Pool(len(chunks)) as pool:
+        res = pool.map(_rbuild_cpu_worker, chunks)
+    wall = time.perf_counter() - t0
+    done = sum(r[0] for r in res)
+    busy = max(r[1] for r in res)
+    return {"value": done / busy, "channels": done, "cores": len(chunks), "wall_s": wall, "busy_s": busy}
+
+
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -159,6 +212,25 @@ def run_reference(args, rank, world):
     contraction.q_angular_first) on all host cores, rank 0 only."""
     if rank != 0:
         return
+    if args.config in RBUILD:
+        rates, walls = [], []
+        for _ in range(args.steps):
+            r = rbuild_cpu_rate(args.config)
+            rates.append(r["value"])
+            walls.append(r["wall_s"])
+        v = statistics.median(rates)
+        k, l, gam = RBUILD[args.config]
+        print(json.dumps({
+            "impl": "reference", "metric": RBUILD_METRIC, "value": v, "unit": "channels/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(walls),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "none",
+            "config": {"workload": f"R-tensor assembly N={k} L={l} gamma={gam}",
+                       "step": "one channel per host core (random sample), oracle port of channel_half"},
+            "cpu_baseline": {"value": v, "unit": "channels/s", "cores": r["cores"], "kind": "port",
+                             "sample": f"{r['channels']} random channels, one per core"},
+            "e2e": {"value": v, "unit": "channels/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }), flush=True)
+        return
     opfile, n_cells, _, desc = CONFIGS[args.config]
     from paper_2605_28475_b200.operator import load_cache
 
@@ -185,6 +257,80 @@ def run_reference(args, rank, world):
         "e2e": {"value": v, "unit": "cells/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def run_rbuild(args, rank, world, local_rank):
+    """R-tensor assembly on the GPU (include/bfr.h).  Replicas only: every rank
+    assembles the full tensor (the build is one-time per operator)."""
+    import torch
+
+    from paper_2605_28475_b200 import rbuild
+    from paper_2605_28475_b200.operator import SpectralConfig
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    k, l, gam = RBUILD[args.config]
+    cfg = SpectralConfig(k, l, gam)
+    grid = rbuild.grid_sizes(k, l)
+    for _ in range(max(args.warmup, 0)):
+        rbuild.assemble_r_tensor(cfg, grid, device=local_rank)
+    stats, walls = [], []
+    with ClockSampler(local_rank) as clk:
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            r = rbuild.assemble_r_tensor(cfg, grid, device=local_rank)
+            walls.append(time.perf_counter() - t0)
+            stats.append(rbuild.last_stats())
+    n_t = r.channels.n_t
+    total_ms = sum(s["ms_total"] for s in stats)
+    t = torch.tensor([total_ms, sum(walls)], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms, wall_tot = float(t[0]), float(t[1])
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+    st = stats[-1]
+    contract_ms = statistics.mean(s["ms_contract"] for s in stats)
+    achieved = 2.0 * st["alg_macs"] / (contract_ms / 1e3) / 1e12
+    line = {
+        "metric": RBUILD_METRIC, "value": n_t * world * args.steps / (total_ms / 1e3), "unit": "channels/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "none (deterministic quadrature grids)",
+        "config": {"workload": f"R-tensor assembly N={k} L={l} gamma={gam} (kinematic.assemble_r_tensor)",
+                   "grid": grid.as_tuple(), "channels": n_t,
+                   "parallelism": f"replicas on {world} GPU(s)",
+                   "l2": "working set (radial tables + integrand rows) larger than L2",
+                   "points_per_patch": st["n_points"]},
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                     "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
+                     "kernel": "k_tri (channel contraction, DMMA m8n8k4)",
+                     "alg_flops_per_step": 2.0 * st["alg_macs"],
+                     "exec_flops_per_step": 2.0 * st["contract_macs"],
+                     "contract_share_of_step": contract_ms / (total_ms / args.steps),
+                     "peak_source": "measured FP64 DMMA.8x8x4 sustained (profiles/fp64_peak.txt)"},
+        "e2e": {"value": n_t * world * args.steps / wall_tot, "unit": "channels/s",
+                "h2d_bytes_per_step": None, "d2h_bytes_per_step": r.values.nbytes,
+                "path": "rbuild.assemble_r_tensor (host tables -> bfr_assemble -> R on host)"},
+        "gpu_launches": st["launches"] * args.steps,
+        "clocks": clk.summary(),
+        "build_s": {"device": total_ms / args.steps / 1e3, "wall": wall_tot / args.steps,
+                    "reference_cpu_8proc_s": {"rbuild12": 1263.0}.get(args.config)},
+    }
+    if world == 1 and not args.no_cpu:
+        cpu = rbuild_cpu_rate(args.config)
+        line["cpu_baseline"] = {"value": cpu["value"], "unit": "channels/s", "cores": cpu["cores"], "kind": "port",
+                                "sample": f"{cpu['channels']} random channels, one per core (oracle port of "
+                                          "kinematic channel_half, 1 thread per process)"}
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
 
 
 def run_ours(args, rank, world, local_rank):
@@ -347,7 +493,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="hs12", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="hs12", choices=sorted(CONFIGS) + sorted(RBUILD))
     ap.add_argument("--cells", type=int, default=0, help="override cells per GPU")
     ap.add_argument("--seed", type=int, default=20260520)
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -359,6 +505,8 @@ def main():
     local_rank = env_int("LOCAL_RANK", 0)
     if args.impl == "reference":
         run_reference(args, rank, world)
+    elif args.config in RBUILD:
+        run_rbuild(args, rank, world, local_rank)
     else:
         run_ours(args, rank, world, local_rank)
 

@@ -66,6 +66,7 @@ typedef struct bfr_stats {
                             channel: gain, fast loss, slow loss)                   */
   double x_bytes;        /* bytes of integrand rows written + read by the contraction */
   int64_t n_points[2];   /* contraction points per patch (E x outer [x Duffy])     */
+  int64_t launches;      /* kernels launched by this assembly                     */
 } bfr_stats;
 
 /* Assemble the raw R tensor (before the null-space corrections) into

@@ -130,6 +130,7 @@ class BfrStats(ctypes.Structure):
         ("alg_macs", ctypes.c_double),
         ("x_bytes", ctypes.c_double),
         ("n_points", ctypes.c_int64 * 2),
+        ("launches", ctypes.c_int64),
     ]
 
 

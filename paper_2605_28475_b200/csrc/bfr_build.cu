@@ -27,6 +27,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -194,119 +195,169 @@ __device__ __forceinline__ dd dd_mul_d(dd a, double b) {
 
 // ------------------------------------------------------------------ A tables
 // A[l1,m,j](o,t) = sum_{chi,eps} w_chi w_eps |v'|^l1 (|v'|^2/2)^j Ybar_{l1 m}(cos th') cos(m phi')
-// (double-double).  One CTA per (o,t); the (chi,eps) axis is staged in chunks
-// of blockDim points: phase 1 builds each point's harmonic column and power
-// row, phase 2 accumulates the (l1,m) x j outer-product sums
-// (kinematic.py:366-380, 448-464).
+// in double-double.  One CTA (256 threads) per (o,t); the (chi,eps) axis is
+// staged ATAB_SC points at a time (kinematic.py:366-380, 448-464):
+//  1a  one thread per point: post-collision speed/direction, the dd power row
+//      (|v'|^2/2)^j and the dd weight w_chi w_eps;
+//  1b  one thread per (point, m): Ybar_{l,m} for l = m..L by the upward
+//      recurrence, times cos(m phi') (rounded as the reference rounds it) and
+//      the dd weighted radial power w |v'|^l;
+//  2   one thread per (row (l1,m), 4 j's): compensated (Dot2) accumulation of
+//      the point sum, carried across chunks in shared memory.
+constexpr int ATAB_SC = 32;
+constexpr int ATAB_JT = 4;
+
 struct AtabParams {
   const double* g;
   int n_ot, L, nk, n_chi, n_eps;
   const double *chi_x, *chi_w, *eps_c, *eps_s, *eps_w;
   double *A_hi, *A_lo;  // [lm][j][ot]
+  int fast;             // experiments only (BFR_ATAB_F64): plain fp64 accumulation
 };
 
-__host__ __device__ inline size_t atab_smem(int nlm, int nk, int sc) {
-  return ((size_t)2 * nlm * (sc + 1) + (size_t)2 * sc * nk + (size_t)2 * nlm * nk) * 8;
+__host__ __device__ inline size_t atab_smem(int nlm, int nk) {
+  const int njt = (nk + ATAB_JT - 1) / ATAB_JT;
+  return ((size_t)2 * nlm * (ATAB_SC + 1)                 // yh, yl
+          + (size_t)2 * ATAB_SC * njt * ATAB_JT            // vh, vl
+          + (size_t)2 * nlm * njt * ATAB_JT                // acc s, c
+          + (size_t)6 * ATAB_SC) * 8;                      // per-point scalars
 }
 
-__global__ void k_atab(AtabParams p) {
+__global__ void __launch_bounds__(256) k_atab(AtabParams p) {
   extern __shared__ double sm[];
-  const int sc = blockDim.x, tid = threadIdx.x, ot = blockIdx.x;
-  const int nlm = lm_index(p.L, p.L) + 1, nk = p.nk, nout = nlm * nk;
-  double* yh = sm;                                  // [nlm][sc+1]
-  double* yl = yh + (size_t)nlm * (sc + 1);
-  double* vh = yl + (size_t)nlm * (sc + 1);         // [sc][nk]
-  double* vl = vh + (size_t)sc * nk;
-  double* ah = vl + (size_t)sc * nk;                // [nlm*nk]
-  double* al = ah + (size_t)nout;
+  const int tid = threadIdx.x, nth = blockDim.x, ot = blockIdx.x;
+  const int L = p.L, nlm = lm_index(L, L) + 1, nk = p.nk;
+  const int njt = (nk + ATAB_JT - 1) / ATAB_JT, nkp = njt * ATAB_JT;
+  constexpr int SC = ATAB_SC, SS = ATAB_SC + 1;
+  double* yh = sm;                         // [nlm][SS]
+  double* yl = yh + (size_t)nlm * SS;
+  double* vh = yl + (size_t)nlm * SS;      // [SC][nkp]
+  double* vl = vh + (size_t)SC * nkp;
+  double* as = vl + (size_t)SC * nkp;      // [nlm][nkp]
+  double* ac = as + (size_t)nlm * nkp;
+  double* pv = ac + (size_t)nlm * nkp;     // per point: vps, ctp, sx, c1, w_hi, w_lo
   const int n_ot = p.n_ot;
   const double cx = p.g[(size_t)G_CX * n_ot + ot], cz = p.g[(size_t)G_CZ * n_ot + ot];
   const double hu = 0.5 * p.g[(size_t)G_U0 * n_ot + ot];
   const double uhx = p.g[(size_t)G_UHX * n_ot + ot], uhz = p.g[(size_t)G_UHZ * n_ot + ot];
   const double e1x = p.g[(size_t)G_E1X * n_ot + ot], e1z = p.g[(size_t)G_E1Z * n_ot + ot];
   const double e2y = p.g[(size_t)G_E2Y * n_ot + ot];
-  for (int o = tid; o < nout; o += sc) ah[o] = al[o] = 0.0;
+  for (int o = tid; o < nlm * nkp; o += nth) as[o] = ac[o] = 0.0;
   const int ns = p.n_chi * p.n_eps;
-  for (int s0 = 0; s0 < ns; s0 += sc) {
-    const int s = s0 + tid;
-    if (s < ns) {
-      const int ic = s / p.n_eps, ie = s - ic * p.n_eps;
-      const double cc = p.chi_x[ic];
-      const double sch = sqrt(fmax(1.0 - cc * cc, 0.0));
-      const double ce = p.eps_c[ie], se = p.eps_s[ie];
-      const double vx = cx + hu * (cc * uhx + sch * ce * e1x);
-      const double vy = hu * sch * se * e2y;
-      const double vz = cz + hu * (cc * uhz + sch * ce * e1z);
-      const double vps = sqrt(vx * vx + vy * vy + vz * vz);
-      const double ctp = fmin(fmax(vps > 0.0 ? vz / vps : 1.0, -1.0), 1.0);
-      const double c1 = cos(atan2(vy, vx));
-      // power row (|v'|^2/2)^j and the weighted radial power w |v'|^l, exact to dd
+  for (int s0 = 0; s0 < ns; s0 += SC) {
+    // 1a: per point
+    if (tid < SC) {
+      const int s = s0 + tid;
+      double vps = 0.0, ctp = 1.0, c1 = 1.0;
+      dd w = {0.0, 0.0};
+      if (s < ns) {
+        const int ic = s / p.n_eps, ie = s - ic * p.n_eps;
+        const double cc = p.chi_x[ic];
+        const double sch = sqrt(fmax(1.0 - cc * cc, 0.0));
+        const double ce = p.eps_c[ie], se = p.eps_s[ie];
+        const double vx = cx + hu * (cc * uhx + sch * ce * e1x);
+        const double vy = hu * sch * se * e2y;
+        const double vz = cz + hu * (cc * uhz + sch * ce * e1z);
+        vps = sqrt(vx * vx + vy * vy + vz * vz);
+        ctp = fmin(fmax(vps > 0.0 ? vz / vps : 1.0, -1.0), 1.0);
+        c1 = cos(atan2(vy, vx));
+        w = two_prod(p.chi_w[ic], p.eps_w[ie]);
+      }
       dd step = two_prod(vps, vps);
       step.hi *= 0.5;
       step.lo *= 0.5;
-      dd pw = {1.0, 0.0};
-      for (int j = 0; j < nk; ++j) {
-        vh[tid * nk + j] = pw.hi;
-        vl[tid * nk + j] = pw.lo;
+      dd pw = {s < ns ? 1.0 : 0.0, 0.0};
+      for (int j = 0; j < nkp; ++j) {
+        vh[tid * nkp + j] = j < nk ? pw.hi : 0.0;
+        vl[tid * nkp + j] = j < nk ? pw.lo : 0.0;
         pw = dd_mul(pw, step);
       }
-      const dd w = two_prod(p.chi_w[ic], p.eps_w[ie]);
-      // harmonics: m outer, l inner; y = Ybar_lm cos(m phi) rounded as the reference does
-      const double sx = sqrt(fmax((1.0 - ctp) * (1.0 + ctp), 0.0));
-      double pmm = 0.28209479177387814347, cm1 = 1.0, cm2 = 0.0;
-      dd wv = w;  // w |v'|^m at the diagonal
-      for (int m = 0; m <= p.L; ++m) {
-        double cm;
-        if (m == 0) cm = 1.0;
-        else if (m == 1) cm = c1;
-        else cm = 2.0 * c1 * cm1 - cm2;
+      double* q = pv + tid * 6;
+      q[0] = vps;
+      q[1] = ctp;
+      q[2] = sqrt(fmax((1.0 - ctp) * (1.0 + ctp), 0.0));
+      q[3] = c1;
+      q[4] = w.hi;
+      q[5] = w.lo;
+    }
+    __syncthreads();
+    // 1b: per (point, m)
+    for (int it = tid; it < SC * (L + 1); it += nth) {
+      const int m = it / SC, sl = it - m * SC;
+      const double* q = pv + sl * 6;
+      const double vps = q[0], ctp = q[1], sx = q[2], c1 = q[3];
+      double cm = 1.0, cm1 = 1.0, cm2 = 0.0, pmm = 0.28209479177387814347;
+      dd wl = {q[4], q[5]};
+      for (int i = 1; i <= m; ++i) {
+        cm = i == 1 ? c1 : 2.0 * c1 * cm1 - cm2;
         cm2 = cm1;
         cm1 = cm;
-        if (m > 0) {
-          pmm = c_yd[m] * sx * pmm;
-          wv = dd_mul_d(wv, vps);
-        }
-        dd wl = wv;
-        dd t = dd_mul_d(wl, pmm * cm);
-        yh[(size_t)lm_index(m, m) * (sc + 1) + tid] = t.hi;
-        yl[(size_t)lm_index(m, m) * (sc + 1) + tid] = t.lo;
-        if (m == p.L) break;
+        pmm = c_yd[i] * sx * pmm;
+        wl = dd_mul_d(wl, vps);
+      }
+      dd t = dd_mul_d(wl, pmm * cm);
+      yh[(size_t)lm_index(m, m) * SS + sl] = t.hi;
+      yl[(size_t)lm_index(m, m) * SS + sl] = t.lo;
+      if (m < L) {
         double p0 = pmm, p1 = c_ye[m] * ctp * pmm;
         wl = dd_mul_d(wl, vps);
         t = dd_mul_d(wl, p1 * cm);
-        yh[(size_t)lm_index(m + 1, m) * (sc + 1) + tid] = t.hi;
-        yl[(size_t)lm_index(m + 1, m) * (sc + 1) + tid] = t.lo;
-        for (int l = m + 2; l <= p.L; ++l) {
+        yh[(size_t)lm_index(m + 1, m) * SS + sl] = t.hi;
+        yl[(size_t)lm_index(m + 1, m) * SS + sl] = t.lo;
+        for (int l = m + 2; l <= L; ++l) {
           const double p2 = c_ya[l * (LMX + 1) + m] * (ctp * p1 - c_yb[l * (LMX + 1) + m] * p0);
           p0 = p1;
           p1 = p2;
           wl = dd_mul_d(wl, vps);
           t = dd_mul_d(wl, p1 * cm);
-          yh[(size_t)lm_index(l, m) * (sc + 1) + tid] = t.hi;
-          yl[(size_t)lm_index(l, m) * (sc + 1) + tid] = t.lo;
+          yh[(size_t)lm_index(l, m) * SS + sl] = t.hi;
+          yl[(size_t)lm_index(l, m) * SS + sl] = t.lo;
         }
       }
-    } else {
-      for (int j = 0; j < nk; ++j) vh[tid * nk + j] = vl[tid * nk + j] = 0.0;
-      for (int r = 0; r < nlm; ++r) yh[(size_t)r * (sc + 1) + tid] = yl[(size_t)r * (sc + 1) + tid] = 0.0;
     }
     __syncthreads();
-    const int cnt = min(sc, ns - s0);
-    for (int o = tid; o < nout; o += sc) {
-      const int r = o / nk, j = o - r * nk;
-      dd a = {ah[o], al[o]};
-      const double* yrh = yh + (size_t)r * (sc + 1);
-      const double* yrl = yl + (size_t)r * (sc + 1);
-      for (int q = 0; q < cnt; ++q)
-        a = dd_add(a, dd_mul({yrh[q], yrl[q]}, {vh[q * nk + j], vl[q * nk + j]}));
-      ah[o] = a.hi;
-      al[o] = a.lo;
+    // 2: Dot2 accumulation, 4 j's per thread item
+    for (int it = tid; it < nlm * njt; it += nth) {
+      const int r = it / njt, j0 = (it - r * njt) * ATAB_JT;
+      double sa[ATAB_JT], ca[ATAB_JT];
+#pragma unroll
+      for (int u = 0; u < ATAB_JT; ++u) {
+        sa[u] = as[r * nkp + j0 + u];
+        ca[u] = ac[r * nkp + j0 + u];
+      }
+      const double* yrh = yh + (size_t)r * SS;
+      const double* yrl = yl + (size_t)r * SS;
+      if (p.fast) {
+        for (int q = 0; q < SC; ++q)
+#pragma unroll
+          for (int u = 0; u < ATAB_JT; ++u) sa[u] = fma(yrh[q], vh[q * nkp + j0 + u], sa[u]);
+      } else {
+#pragma unroll 4
+        for (int q = 0; q < SC; ++q) {
+          const double a_h = yrh[q], a_l = yrl[q];
+#pragma unroll
+          for (int u = 0; u < ATAB_JT; ++u) {
+            const double b_h = vh[q * nkp + j0 + u], b_l = vl[q * nkp + j0 + u];
+            const dd pr = two_prod(a_h, b_h);
+            const dd sm2 = two_sum(sa[u], pr.hi);
+            sa[u] = sm2.hi;
+            ca[u] = fma(a_h, b_l, fma(a_l, b_h, ca[u] + (pr.lo + sm2.lo)));
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < ATAB_JT; ++u) {
+        as[r * nkp + j0 + u] = sa[u];
+        ac[r * nkp + j0 + u] = ca[u];
+      }
     }
     __syncthreads();
   }
-  for (int o = tid; o < nout; o += sc) {
-    p.A_hi[(size_t)o * n_ot + ot] = ah[o];
-    p.A_lo[(size_t)o * n_ot + ot] = al[o];
+  for (int o = tid; o < nlm * nk; o += nth) {
+    const int r = o / nk, j = o - r * nk;
+    const dd v = fast_two_sum(as[r * nkp + j], ac[r * nkp + j]);
+    p.A_hi[(size_t)o * n_ot + ot] = v.hi;
+    p.A_lo[(size_t)o * n_ot + ot] = v.lo;
   }
 }
 
@@ -721,6 +772,7 @@ int set_ybar_constants() {
 
 #define BFR_LAUNCH_CHECK(name)                                                      \
   do {                                                                              \
+    ++n_launch;                                                                     \
     cudaError_t e_ = cudaGetLastError();                                            \
     if (e_ != cudaSuccess) {                                                        \
       set_error(std::string("kernel launch " name ": ") + cudaGetErrorString(e_));  \
@@ -810,6 +862,7 @@ int assemble(const bfr_desc& d, int device, double* r_out, double* halves_out, b
   } evg{{ev0, ev1, ta, tb}};
   BFR_TRY(cudaEventRecord(ev0));
   double ms_contract = 0.0, exec_macs = 0.0, alg_macs = 0.0, xbytes = 0.0;
+  long long n_launch = 0;
 
   const int mt0 = (2 * nk + 7) / 8, mt1 = (nk + 7) / 8, npw = ((nn + 7) / 8 + 7) / 8;
   TriKernel tri0 = pick_tri(mt0, npw), tri1 = pick_tri(mt1, npw);
@@ -852,12 +905,16 @@ int assemble(const bfr_desc& d, int device, double* r_out, double* halves_out, b
     BFR_LAUNCH_CHECK("k_ybar_table");
     {
       AtabParams ap{geo, n_ot, L, nk, d.n_chi, d.n_eps, d_chix, d_chiw, d_epsc, d_epss, d_epsw,
-                    A, A + (size_t)nlm * nk * n_ot};
-      int sc = 64;
-      while (atab_smem(nlm, nk, sc) > 200 * 1024 && sc > 16) sc /= 2;
-      const size_t smem = atab_smem(nlm, nk, sc);
+                    A, A + (size_t)nlm * nk * n_ot, std::getenv("BFR_ATAB_F64") ? 1 : 0};
+      const size_t smem = atab_smem(nlm, nk);
+      int optin = 0;
+      BFR_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+      if (smem > (size_t)optin) {
+        set_error("l_max too large for the angular-table kernel's shared memory");
+        return BFQ_EINVAL;
+      }
       BFR_TRY(cudaFuncSetAttribute(k_atab, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      k_atab<<<n_ot, sc, smem>>>(ap);
+      k_atab<<<n_ot, 256, smem>>>(ap);
       BFR_LAUNCH_CHECK("k_atab");
     }
     {
@@ -927,6 +984,7 @@ int assemble(const bfr_desc& d, int device, double* r_out, double* halves_out, b
     st->contract_macs = exec_macs;
     st->alg_macs = alg_macs;
     st->x_bytes = xbytes;
+    st->launches = n_launch;
   }
   return BFQ_OK;
 }

@@ -327,7 +327,7 @@ def assemble_r_tensor(cfg: SpectralConfig, grid: GridSpec | None = None, *, kern
     _LAST_STATS.clear()
     _LAST_STATS.update(ms_total=st.ms_total, ms_contract=st.ms_contract, contract_macs=st.contract_macs,
                        alg_macs=st.alg_macs, x_bytes=st.x_bytes,
-                       n_points=(int(st.n_points[0]), int(st.n_points[1])))
+                       n_points=(int(st.n_points[0]), int(st.n_points[1])), launches=int(st.launches))
     r = RTensor(out, chans, float(cfg.gamma), grid.as_tuple())
     if return_halves:
         return r, halves
