@@ -14,8 +14,12 @@
 // The two warps of a unit meet at a named barrier twice per channel (Phi
 // complete; Phi consumed).
 
+// DUAL (n_k = 17, where shared memory holds only 8 warps): stage 1 walks the
+// slice two row groups per iteration into two accumulator sets, doubling the
+// independent DMMA chains per warp (ncu at 8 warps: 37% "wait" stalls on the
+// single chain); the second group of an odd tail has g = 0 (fetch_row_bf).
 template <int MT, int CELLS, bool BILIN, int NKT, int QST>
-__global__ void __launch_bounds__(512, 1) bfq_q_kernel2(const KParams p) {
+__global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const KParams p) {
   constexpr int M1T = 8 / CELLS;
   constexpr int HC = CELLS / 2;  // cells per warp in stage 1
   static_assert(CELLS >= 2, "pair split needs at least two cells per tile");
@@ -247,14 +251,17 @@ __global__ void __launch_bounds__(512, 1) bfq_q_kernel2(const KParams p) {
           for (int t = 0; t < MTM; ++t) xr[cc][t] = xc[cc][t] = 0.0;
           xd[cc] = 0.0;
         }
-        for (int z0 = zs[ml]; z0 < ze[ml]; z0 += 4) {
-          const Row rw = nxt_row;
-          {
-            const bool same = z0 + 4 < ze[ml];
-            const int zn = ml + 1 < M1T ? zs[ml + 1 < M1T ? ml + 1 : ml] : zs_n[0];
-            const int en = ml + 1 < M1T ? ze[ml + 1 < M1T ? ml + 1 : ml] : (i + 1 < nch ? ze_n[0] : 0);
-            nxt_row = fetch_row_bf(p.rows, (same ? z0 + 4 : zn) + kq, same ? ze[ml] : en);
-          }
+        constexpr bool DUAL = NKT == 17;
+        double acc2[DUAL ? HC : 1][MT][MT][2];
+        if constexpr (DUAL) {
+#pragma unroll
+          for (int cc = 0; cc < HC; ++cc)
+#pragma unroll
+            for (int a = 0; a < MT; ++a)
+#pragma unroll
+              for (int b = 0; b < MT; ++b) acc2[cc][a][b][0] = acc2[cc][a][b][1] = 0.0;
+        }
+        auto group = [&](const Row& rw, double (&ac)[HC][MT][MT][2]) {
           const uint32_t qa = (uint32_t)rw.q2 * 8u, qb = (uint32_t)rw.q3 * 8u;
 #pragma unroll
           for (int cc = 0; cc < HC; ++cc) {
@@ -268,7 +275,7 @@ __global__ void __launch_bounds__(512, 1) bfq_q_kernel2(const KParams p) {
             for (int a = 0; a < MTM; ++a)
 #pragma unroll
               for (int b = 0; b < MTM; ++b)
-                if (b >= a || !DGC) dmma884(acc[cc][a][b][0], acc[cc][a][b][1], av[a], bv[b]);
+                if (b >= a || !DGC) dmma884(ac[cc][a][b][0], ac[cc][a][b][1], av[a], bv[b]);
             if constexpr (X1) {
               const double ea = rw.g * lds_ro(fx_a + qa + cc * cell_bytes);  // g f2[n_k-1, q2]
               const double eb = lds_ro(fx_b + qb + cc * cell_bytes);         // f3[n_k-1, q3]
@@ -279,6 +286,34 @@ __global__ void __launch_bounds__(512, 1) bfq_q_kernel2(const KParams p) {
               }
               xd[cc] = fma(ea, eb, xd[cc]);
             }
+          }
+        };
+        const int zn = ml + 1 < M1T ? zs[ml + 1 < M1T ? ml + 1 : ml] : zs_n[0];
+        const int en = ml + 1 < M1T ? ze[ml + 1 < M1T ? ml + 1 : ml] : (i + 1 < nch ? ze_n[0] : 0);
+        if constexpr (DUAL) {
+          for (int z0 = zs[ml]; z0 < ze[ml]; z0 += 8) {
+            const Row rwa = nxt_row;
+            const Row rwb = fetch_row_bf(p.rows, z0 + 4 + kq, ze[ml]);  // g = 0 past the slice end
+            const bool same = z0 + 8 < ze[ml];
+            nxt_row = fetch_row_bf(p.rows, (same ? z0 + 8 : zn) + kq, same ? ze[ml] : en);
+            group(rwa, acc);
+            group(rwb, acc2);
+          }
+#pragma unroll
+          for (int cc = 0; cc < HC; ++cc)
+#pragma unroll
+            for (int a = 0; a < MT; ++a)
+#pragma unroll
+              for (int b = 0; b < MT; ++b) {
+                acc[cc][a][b][0] += acc2[cc][a][b][0];
+                acc[cc][a][b][1] += acc2[cc][a][b][1];
+              }
+        } else {
+          for (int z0 = zs[ml]; z0 < ze[ml]; z0 += 4) {
+            const Row rw = nxt_row;
+            const bool same = z0 + 4 < ze[ml];
+            nxt_row = fetch_row_bf(p.rows, (same ? z0 + 4 : zn) + kq, same ? ze[ml] : en);
+            group(rw, acc);
           }
         }
         if (zs[ml] >= ze[ml]) {

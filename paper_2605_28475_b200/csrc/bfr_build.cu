@@ -849,21 +849,6 @@ int assemble(const bfr_desc& d, int device, double* r_out, double* halves_out, b
   }
   BFR_TRY(cudaMemset(halves, 0, (size_t)3 * n_t * n3 * 8));
 
-  cudaEvent_t ev0, ev1, ta, tb;
-  BFR_TRY(cudaEventCreate(&ev0));
-  BFR_TRY(cudaEventCreate(&ev1));
-  BFR_TRY(cudaEventCreate(&ta));
-  BFR_TRY(cudaEventCreate(&tb));
-  struct EvGuard {
-    cudaEvent_t e[4];
-    ~EvGuard() {
-      for (auto x : e) cudaEventDestroy(x);
-    }
-  } evg{{ev0, ev1, ta, tb}};
-  BFR_TRY(cudaEventRecord(ev0));
-  double ms_contract = 0.0, exec_macs = 0.0, alg_macs = 0.0, xbytes = 0.0;
-  long long n_launch = 0;
-
   const int mt0 = (2 * nk + 7) / 8, mt1 = (nk + 7) / 8, npw = ((nn + 7) / 8 + 7) / 8;
   TriKernel tri0 = pick_tri(mt0, npw), tri1 = pick_tri(mt1, npw);
   if (!tri0 || !tri1) {
@@ -877,96 +862,122 @@ int assemble(const bfr_desc& d, int device, double* r_out, double* halves_out, b
   if (tri1 != tri0)
     BFR_TRY(cudaFuncSetAttribute(tri1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tri_smem1));
   XrKernel xr = pick_xrows(nk);
+  const size_t atab_sm = atab_smem(nlm, nk);
+  {
+    int optin = 0;
+    BFR_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+    if (atab_sm > (size_t)optin) {
+      set_error("l_max too large for the angular-table kernel's shared memory");
+      return BFQ_EINVAL;
+    }
+    BFR_TRY(cudaFuncSetAttribute(k_atab, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)atab_sm));
+  }
+
+  // per-patch sizes; every buffer is allocated once, before the timed region
+  struct PatchDims {
+    int n_o, n_t, n_ot, nq, PR, S;
+    long long P, PS;
+    double *ox, *ow, *tx, *tw;
+  } pd[2];
+  int max_ot = 0, max_nq = 0, max_S = 0;
+  long long max_PS = 0;
+  for (int patch = 0; patch < 2; ++patch) {
+    PatchDims& q = pd[patch];
+    q.n_o = d.n_outer[patch];
+    q.n_t = d.n_inner[patch];
+    q.n_ot = q.n_o * q.n_t;
+    q.nq = patch == 0 ? q.n_o : q.n_ot;
+    q.P = (long long)d.n_e * q.nq;
+    q.PS = (q.P + 3) / 4 * 4;
+    q.PR = q.P >= 16384 * 4 ? 16384 : (int)((q.P + PC - 1) / PC * PC);
+    q.S = (int)((q.P + q.PR - 1) / q.PR);
+    if ((rc = upload(db, d.outer_x[patch], (size_t)q.n_o, &q.ox))) return rc;
+    if ((rc = upload(db, d.outer_w[patch], (size_t)q.n_o, &q.ow))) return rc;
+    if ((rc = upload(db, d.inner_x[patch], (size_t)q.n_t, &q.tx))) return rc;
+    if ((rc = upload(db, d.inner_w[patch], (size_t)q.n_t, &q.tw))) return rc;
+    max_ot = std::max(max_ot, q.n_ot);
+    max_nq = std::max(max_nq, q.nq);
+    max_S = std::max(max_S, q.S);
+    max_PS = std::max(max_PS, q.PS);
+    if (st) st->n_points[patch] = q.P;
+  }
+  // channel batches: integrand-row scratch <= ~6 GB
+  const size_t xrow_bytes = (size_t)3 * nk * max_PS * 8;
+  const int nb = (int)std::max<size_t>(1, std::min<size_t>((size_t)n_t, ((size_t)6 << 30) / xrow_bytes));
+  double* geo = db.alloc<double>((size_t)G_NF * max_ot);
+  double* yb = db.alloc<double>((size_t)nlm * max_ot);
+  double* A = db.alloc<double>((size_t)2 * nlm * nk * max_ot);  // hi, lo
+  double* env = db.alloc<double>((size_t)max_PS);
+  double* phi = db.alloc<double>((size_t)(L + 1) * 2 * nk * max_PS);
+  double* X = db.alloc<double>((size_t)nb * 3 * nk * max_PS);
+  double* gq = db.alloc<double>((size_t)nb * nk * max_nq);
+  double* lq = db.alloc<double>((size_t)nb * max_nq);
+  double* part = db.alloc<double>((size_t)nb * 2 * max_S * 2 * nk * nn);
+  if (!geo || !yb || !A || !env || !phi || !X || !gq || !lq || !part) {
+    set_error("device allocation failed");
+    return BFQ_ENOMEM;
+  }
+  // Row tails [P, PS) are never read: k_tri zero-fills past the last point.
+
+  const int n_batches = 2 * ((n_t + nb - 1) / nb);
+  std::vector<cudaEvent_t> evs(2 + 2 * n_batches, nullptr);
+  struct EvGuard {
+    std::vector<cudaEvent_t>& e;
+    ~EvGuard() {
+      for (auto x : e)
+        if (x) cudaEventDestroy(x);
+    }
+  } evg{evs};
+  for (auto& e : evs) BFR_TRY(cudaEventCreate(&e));
+  cudaEvent_t ev0 = evs[0], ev1 = evs[1];
+  BFR_TRY(cudaEventRecord(ev0));
+  double exec_macs = 0.0, alg_macs = 0.0, xbytes = 0.0;
+  long long n_launch = 0;
+  int ib = 0;
 
   for (int patch = 0; patch < 2; ++patch) {
-    const int n_o = d.n_outer[patch], n_tt = d.n_inner[patch], n_ot = n_o * n_tt;
-    const int nq = patch == 0 ? n_o : n_ot;
-    const long long P = (long long)d.n_e * nq, PS = (P + 3) / 4 * 4;
-    if (st) st->n_points[patch] = P;
-    double *d_ox, *d_ow, *d_tx, *d_tw;
-    if ((rc = upload(db, d.outer_x[patch], (size_t)n_o, &d_ox))) return rc;
-    if ((rc = upload(db, d.outer_w[patch], (size_t)n_o, &d_ow))) return rc;
-    if ((rc = upload(db, d.inner_x[patch], (size_t)n_tt, &d_tx))) return rc;
-    if ((rc = upload(db, d.inner_w[patch], (size_t)n_tt, &d_tw))) return rc;
-    double* geo = db.alloc<double>((size_t)G_NF * n_ot);
-    double* yb = db.alloc<double>((size_t)nlm * n_ot);
-    double* A = db.alloc<double>((size_t)2 * nlm * nk * n_ot);  // hi, lo
-    double* env = db.alloc<double>((size_t)PS);
-    double* phi = db.alloc<double>((size_t)(L + 1) * 2 * nk * PS);
-    if (!geo || !yb || !A || !env || !phi) {
-      set_error("device allocation failed");
-      return BFQ_ENOMEM;
-    }
-    BFR_TRY(cudaMemset(phi, 0, (size_t)(L + 1) * 2 * nk * PS * 8));
-    k_geom<<<blocks_for(n_ot, 128), 128>>>(patch, d_ox, d_tx, n_o, n_tt, d.gamma, d.kernel_scale, fgeo_c,
-                                           geo);
+    const PatchDims& q = pd[patch];
+    const int n_o = q.n_o, n_tt = q.n_t, n_ot = q.n_ot, nq = q.nq, PR = q.PR, S = q.S;
+    const long long P = q.P, PS = q.PS;
+    k_geom<<<blocks_for(n_ot, 128), 128>>>(patch, q.ox, q.tx, n_o, n_tt, d.gamma, d.kernel_scale, fgeo_c, geo);
     BFR_LAUNCH_CHECK("k_geom");
     k_ybar_table<<<blocks_for(n_ot, 128), 128>>>(geo, n_ot, L, yb);
     BFR_LAUNCH_CHECK("k_ybar_table");
     {
       AtabParams ap{geo, n_ot, L, nk, d.n_chi, d.n_eps, d_chix, d_chiw, d_epsc, d_epss, d_epsw,
                     A, A + (size_t)nlm * nk * n_ot, std::getenv("BFR_ATAB_F64") ? 1 : 0};
-      const size_t smem = atab_smem(nlm, nk);
-      int optin = 0;
-      BFR_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
-      if (smem > (size_t)optin) {
-        set_error("l_max too large for the angular-table kernel's shared memory");
-        return BFQ_EINVAL;
-      }
-      BFR_TRY(cudaFuncSetAttribute(k_atab, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      k_atab<<<n_ot, 256, smem>>>(ap);
+      k_atab<<<n_ot, 256, atab_sm>>>(ap);
       BFR_LAUNCH_CHECK("k_atab");
     }
     {
-      RadParams rp{geo, d_eta, d_we, d_ow, d_tw, d_norms, patch, d.n_e, n_o, n_tt, nq, L, nk, P, PS, phi, env};
+      RadParams rp{geo, d_eta, d_we, q.ow, q.tw, d_norms, patch, d.n_e, n_o, n_tt, nq, L, nk, P, PS, phi, env};
       k_radial<<<blocks_for(P, 128), 128>>>(rp);
       BFR_LAUNCH_CHECK("k_radial");
     }
-    // channel batches: X scratch <= ~6 GB
-    const size_t xrow_bytes = (size_t)3 * nk * PS * 8;
-    int nb = (int)std::max<size_t>(1, std::min<size_t>((size_t)n_t, ((size_t)6 << 30) / xrow_bytes));
-    const int PR = P >= 16384 * 4 ? 16384 : (int)((P + PC - 1) / PC * PC);
-    const int S = (int)((P + PR - 1) / PR);
-    double* X = db.alloc<double>((size_t)nb * 3 * nk * PS);
-    double* gq = db.alloc<double>((size_t)nb * nk * nq);
-    double* lq = db.alloc<double>((size_t)nb * nq);
-    double* part = db.alloc<double>((size_t)nb * 2 * S * 2 * nk * nn);
-    if (!X || !gq || !lq || !part) {
-      set_error("device allocation failed");
-      return BFQ_ENOMEM;
-    }
-    BFR_TRY(cudaMemset(X, 0, (size_t)nb * 3 * nk * PS * 8));
-    for (int c0 = 0; c0 < n_t; c0 += nb) {
+    for (int c0 = 0; c0 < n_t; c0 += nb, ++ib) {
       const int cb = std::min(nb, n_t - c0);
-      GsParams gp{geo, A, A + (size_t)nlm * nk * n_ot, yb, d_tw, d_w3j, d_trip, c0, patch, n_o, n_tt, nq, L, nk, swc, gq, lq};
+      GsParams gp{geo, A, A + (size_t)nlm * nk * n_ot, yb, q.tw, d_w3j, d_trip, c0, patch, n_o, n_tt, nq, L, nk,
+                  swc, gq, lq};
       k_gstack<<<dim3(blocks_for(nq, 128), cb), 128>>>(gp);
       BFR_LAUNCH_CHECK("k_gstack");
       XrParams xp{gq, lq, d_me, d_pf, phi, env, d_trip, c0, d.n_e, nq, nk, P, PS, X};
       xr<<<dim3(blocks_for(P, 128), cb), 128>>>(xp);
       BFR_LAUNCH_CHECK("xr");
-      BFR_TRY(cudaEventRecord(ta));
+      BFR_TRY(cudaEventRecord(evs[2 + 2 * ib]));
       TriParams tp{X, phi, d_trip, c0, nk, 0, S, PR, P, PS, part};
       tri0<<<dim3(S, cb), 256, tri_smem0>>>(tp);
       BFR_LAUNCH_CHECK("tri0");
       tp.kind = 1;
       tri1<<<dim3(S, cb), 256, tri_smem1>>>(tp);
       BFR_LAUNCH_CHECK("tri1");
-      BFR_TRY(cudaEventRecord(tb));
+      BFR_TRY(cudaEventRecord(evs[3 + 2 * ib]));
       k_reduce<<<blocks_for((long long)cb * 3 * nk * nn, 256), 256>>>(part, c0, cb, nk, S, n_t, halves);
       BFR_LAUNCH_CHECK("k_reduce");
-      BFR_TRY(cudaEventSynchronize(tb));
-      float ms = 0.f;
-      BFR_TRY(cudaEventElapsedTime(&ms, ta, tb));
-      ms_contract += ms;
       exec_macs += (double)cb * (double)S * PR * 8.0 * 8.0 *
                    ((double)mt0 * ((nn + 7) / 8) + (double)mt1 * ((nn + 7) / 8));
       alg_macs += (double)cb * P * 3.0 * nk * nn;
       xbytes += (double)cb * 3 * nk * P * 8.0 * 2.0;
     }
-    db.release(X);
-    db.release(part);
-    db.release(phi);
-    db.release(A);
   }
   k_full<<<blocks_for((long long)n_t * n3, 256), 256>>>(halves, d_swap, n_t, nk, full);
   BFR_LAUNCH_CHECK("k_full");
@@ -976,6 +987,12 @@ int assemble(const bfr_desc& d, int device, double* r_out, double* halves_out, b
   BFR_TRY(cudaEventSynchronize(ev1));
   float ms_tot = 0.f;
   BFR_TRY(cudaEventElapsedTime(&ms_tot, ev0, ev1));
+  double ms_contract = 0.0;
+  for (int i = 0; i < ib; ++i) {
+    float ms = 0.f;
+    BFR_TRY(cudaEventElapsedTime(&ms, evs[2 + 2 * i], evs[3 + 2 * i]));
+    ms_contract += ms;
+  }
   BFR_TRY(cudaMemcpy(r_out, rdev, (size_t)n_t * n3 * 8, cudaMemcpyDeviceToHost));
   if (halves_out) BFR_TRY(cudaMemcpy(halves_out, halves, (size_t)3 * n_t * n3 * 8, cudaMemcpyDeviceToHost));
   if (st) {

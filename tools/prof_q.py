@@ -41,7 +41,7 @@ if os.environ.get("BFQ_DEBUG", "0") != "0" and int(os.environ["BFQ_DEBUG"]) & 8:
     lib = _lib.lib()
     buf = (ctypes.c_ulonglong * 8)()
     lib.bfq_debug_phase_clocks(buf)
-    if plan.info["warps_per_cta"] == 16:  # pair-split kernel
+    if plan.info["warps_per_cta"] in (8, 16) and os.environ.get("BFQ_KERNEL", "2") == "2":  # pair-split kernel
         names = ["stage1", "bar1", "wait R", "stage2", "bar2", "total"]
         n = max(buf[6], 1)
     else:
