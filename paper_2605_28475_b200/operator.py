@@ -284,7 +284,8 @@ def save_cache(path, op: FactorizedOperator) -> int:
         np.ascontiguousarray(op.r.values).astype("<f8").tobytes(),
     ])
     flags = (1 if op.r.conservation_applied else 0) | (2 if op.r.detailed_balance_applied else 0)
-    grid = tuple(op.r.grid) if op.r.grid else (0,) * 9
+    g = op.r.grid
+    grid = tuple(g.as_tuple()) if hasattr(g, "as_tuple") else (tuple(g) if g else (0,) * 9)
     if len(grid) != 9:
         raise ValueError("operator grid spec must have 9 entries")
     header = _HDR.pack(_MAGIC, 1, op.cfg.k_max, op.cfg.l_max, float(op.cfg.gamma), *grid,

@@ -55,6 +55,7 @@ __all__ = [
     "build_gaunt_coo",
     "build_operator",
     "last_stats",
+    "register_with_reference",
 ]
 
 
@@ -328,7 +329,7 @@ def assemble_r_tensor(cfg: SpectralConfig, grid: GridSpec | None = None, *, kern
     _LAST_STATS.update(ms_total=st.ms_total, ms_contract=st.ms_contract, contract_macs=st.contract_macs,
                        alg_macs=st.alg_macs, x_bytes=st.x_bytes,
                        n_points=(int(st.n_points[0]), int(st.n_points[1])), launches=int(st.launches))
-    r = RTensor(out, chans, float(cfg.gamma), grid.as_tuple())
+    r = RTensor(out, chans, float(cfg.gamma), grid)
     if return_halves:
         return r, halves
     return r
@@ -431,3 +432,25 @@ def build_operator(cfg: SpectralConfig, pad_rad: int = 16, pad_ang: int = 16, *,
     if detailed_balance:
         r = apply_detailed_balance(r)
     return FactorizedOperator(r, build_gaunt_coo(cfg.l_max), cfg)
+
+
+def register_with_reference(kinematic_module=None, contraction_module=None) -> bool:
+    """Route the reference's operator build through the GPU assembler.
+
+    ``boltzfact.contraction.build_operator`` calls ``assemble_r_tensor`` by the
+    name it imported from ``kinematic`` (contraction.py:22-25, :172), so both
+    module attributes are replaced.  The returned ``RTensor`` carries the
+    attributes the reference's ``apply_conservation`` / ``apply_detailed_balance``
+    / ``FactorizedOperator`` / ``save_cache`` use (values, channels, gamma,
+    grid.as_tuple(), flags, max_zeroed).  Returns False if the reference is not
+    importable."""
+    try:
+        if kinematic_module is None:
+            import boltzfact.kinematic as kinematic_module  # noqa: PLC0415
+        if contraction_module is None:
+            import boltzfact.contraction as contraction_module  # noqa: PLC0415
+    except ImportError:
+        return False
+    kinematic_module.assemble_r_tensor = assemble_r_tensor
+    contraction_module.assemble_r_tensor = assemble_r_tensor
+    return True

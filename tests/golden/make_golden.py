@@ -45,6 +45,7 @@ CASES = {
     "hs_n8": (3, 3),
     "mm_n10": (2, 2),
     "hs_n12": (2, 2),
+    "hs_n16": (1, 2),
 }
 
 

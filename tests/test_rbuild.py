@@ -134,3 +134,36 @@ def test_gpu_build_without_library_fails_loudly(monkeypatch):
     monkeypatch.setattr(_lib, "_lib", None)
     with pytest.raises(_lib.EngineUnavailable):
         rbuild.assemble_r_tensor(SpectralConfig(2, 2, 1.0))
+
+
+def test_gpu_rtensor_type_flows_through_reference_build(reference, tmp_path, monkeypatch):
+    """register_with_reference swaps the reference's assemble_r_tensor; the
+    RTensor we return satisfies the reference's corrections, FactorizedOperator
+    and save_cache/load_cache (GPU call stubbed with the reference's own R)."""
+    import boltzfact.cache as rcache
+    import boltzfact.contraction as rcon
+    import boltzfact.kinematic as rkin
+
+    from paper_2605_28475_b200.operator import RTensor
+
+    ref = load_op("hs_n4")
+    raw = r_oracle.assemble_r(4, 4, 1.0, conservation=False, detailed_balance=False)
+
+    def fake_assemble(cfg, grid=None, *, kernel_scale=1.0, threads=1, device=0, return_halves=False):
+        g = grid or rbuild.grid_sizes(cfg.k_max, cfg.l_max)
+        return RTensor(raw.copy(), rbuild.enumerate_channels(cfg.l_max), float(cfg.gamma), g)
+
+    monkeypatch.setattr(rbuild, "assemble_r_tensor", fake_assemble)
+    monkeypatch.setattr(rkin, "assemble_r_tensor", rkin.assemble_r_tensor)
+    monkeypatch.setattr(rcon, "assemble_r_tensor", rcon.assemble_r_tensor)
+    assert rbuild.register_with_reference(rkin, rcon)
+    assert rcon.assemble_r_tensor is fake_assemble
+    from boltzfact.basis import SpectralConfig as RCfg
+
+    op = rcon.build_operator(RCfg(4, 4, 1.0))
+    assert np.abs(op.r.values - ref.r.values).max() / np.abs(ref.r.values).max() < 2e-15
+    assert op.r.conservation_applied and op.r.detailed_balance_applied
+    path = tmp_path / "x.bfct"
+    rcache.save_cache(path, op)
+    back = rcache.load_cache(path)
+    assert np.array_equal(back.r.values, op.r.values)
