@@ -62,10 +62,16 @@ def measured_peaks():
         return {}
 
 
-def make_cells(cfg_name, n_k, l_max, n, seed, start):
+def make_cells(cfg_name, n_k, l_max, n, seed, start, device=None):
+    """Seeded cells (host numpy); with ``device`` the Maxwellian projection runs
+    on the GPU (bfq_project_maxwellians, same draws, equal to rounding)."""
     from paper_2605_28475_b200 import inputs
 
     gen = CONFIGS[cfg_name][2]
+    if device is not None:
+        if gen == "pm":
+            return inputs.perturbed_maxwellians_device(n_k, l_max, n, seed=seed, start=start, device=device).cpu().numpy()
+        return inputs.bimodal_device(n_k, l_max, n, seed=seed, start=start, device=device).cpu().numpy()
     if gen == "pm":
         return inputs.perturbed_maxwellians(n_k, l_max, n, seed=seed, start=start)
     return inputs.bimodal(n_k, l_max, n, seed=seed, start=start)
@@ -370,7 +376,8 @@ def run_ours(args, rank, world, local_rank):
         desc += " [operator assembled on this GPU by bfr_assemble: reference build not present]"
     plan = engine.plan_for(op, local_rank)
     cfg = op.cfg
-    host = make_cells(args.config, cfg.n_k, cfg.l_max, n_cells, seed=args.seed, start=rank * n_cells)
+    host = make_cells(args.config, cfg.n_k, cfg.l_max, n_cells, seed=args.seed, start=rank * n_cells,
+                      device=local_rank)
     f = torch.from_numpy(host).to(dev)
     q = torch.empty_like(f)
     stream = torch.cuda.current_stream(dev)

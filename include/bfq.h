@@ -18,6 +18,9 @@
  *   bfq_plan_work         <- ContractionStats accounting (contraction.py:51-73, :314-316)
  *   bfq_rk4_step          <- one step of harness.rk4_integrate (harness.py:79-120)
  *   bfq_moments           <- basis.moments per cell (basis.py:346-363)
+ *   bfq_project_maxwellians <- basis.project(M_{u,T}, cfg, order) batched over
+ *                            drifting Maxwellians (basis.py:262-299), closed
+ *                            angular form (input generator of configs 2-5)
  *
  * Conventions: plain pointers and sizes, no torch types.  Every function returns
  * 0 on success and a negative BFQ_E* code otherwise; bfq_strerror() maps a code
@@ -121,6 +124,18 @@ int bfq_rk4_step(const bfq_plan* plan, double* y, double* work, int64_t n_cells,
 /* Moments per cell (basis.py:346-363): out[cell] = {mass, px, py, pz, energy}. */
 int bfq_moments(const bfq_plan* plan, const double* c, double* out, int64_t n_cells,
                 void* stream);
+
+/* Projection of drifting Maxwellians M_{u,T}(v) = (2 pi T)^{-3/2} exp(-|v-u|^2/2T)
+ * onto the basis (basis.project, basis.py:262-299), one cell per (u_i, T_i):
+ *   c_klm = (2/sqrt(pi)) e^{-|u|^2/2T} Y_lm(u^) sum_j w_j i_l(v_j |u|/T) phi_kl(v_j),
+ *   v_j = sqrt(2 T x_j),
+ * the angular integral done in closed form by the addition theorem.  (x_j, w_j)
+ * is a generalised Gauss-Laguerre rule (alpha = 1/2) of n_rule points (HOST
+ * arrays).  u [n][3], temp [n], out [n][n_k][n_q] and the optional additive
+ * noise [n][n_k][n_q] (may be NULL) are DEVICE pointers; stream-ordered. */
+int bfq_project_maxwellians(int32_t k_max, int32_t l_max, const double* rule_x, const double* rule_w,
+                            int32_t n_rule, const double* u, const double* temp, const double* noise,
+                            double* out, int64_t n, void* stream);
 
 /* Diagnostic: validate `desc` and build the host-side plan (folding check,
  * tiling, CTA schedule) WITHOUT touching a GPU; fills `info` as

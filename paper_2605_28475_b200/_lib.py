@@ -37,6 +37,7 @@ EXPORTED_SYMBOLS = (
     "bfq_rk4_step",
     "bfq_moments",
     "bfq_host_plan_info",
+    "bfq_project_maxwellians",
     "bfq_strerror",
     "bfq_last_error",
 )
@@ -158,6 +159,8 @@ def _declare(lib):
     lib.bfq_strerror.restype = ctypes.c_char_p
     lib.bfq_last_error.argtypes = []
     lib.bfq_last_error.restype = ctypes.c_char_p
+    lib.bfq_project_maxwellians.argtypes = [ctypes.c_int32, ctypes.c_int32, _f64p, _f64p, ctypes.c_int32, vp, vp, vp,
+                                            vp, ctypes.c_int64, vp]
     lib.bfr_assemble.argtypes = [ctypes.POINTER(BfrDesc), ctypes.c_int, vp, vp, ctypes.POINTER(BfrStats)]
     for name in EXPORTED_SYMBOLS + EXPORTED_SYMBOLS_BFR:
         if name not in ("bfq_strerror", "bfq_last_error"):

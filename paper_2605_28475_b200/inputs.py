@@ -163,3 +163,75 @@ def uniform_fields(n_k: int, l_max: int, n_cells: int, seed: int) -> np.ndarray:
     c = rng.uniform(-1.0, 1.0, (n_cells, n_k, (l_max + 1) ** 2))
     c[:, 0, 0] = 1.0
     return c
+
+
+# ------------------------------------------------------------------ on the GPU
+def project_maxwellians_device(n_k: int, l_max: int, u, temp, noise=None, order: int = 96, out=None):
+    """``project_maxwellians`` on the device (bfq_project_maxwellians): u (B, 3),
+    temp (B,) and the optional additive noise (B, n_k, n_q) are float64 CUDA
+    tensors; returns the (B, n_k, n_q) CUDA tensor.  Same closed form and rule."""
+    import ctypes
+
+    import torch
+
+    from . import _lib
+
+    b = u.shape[0]
+    if out is None:
+        out = torch.empty((b, n_k, (l_max + 1) ** 2), dtype=torch.float64, device=u.device)
+    for t, shape in ((u, (b, 3)), (temp, (b,)), (out, (b, n_k, (l_max + 1) ** 2))):
+        if tuple(t.shape) != shape or t.dtype != torch.float64 or not t.is_cuda or not t.is_contiguous():
+            raise ValueError(f"expected a contiguous float64 CUDA tensor of shape {shape}")
+    if noise is not None and (tuple(noise.shape) != tuple(out.shape) or not noise.is_cuda
+                              or noise.dtype != torch.float64 or not noise.is_contiguous()):
+        raise ValueError("noise must match the output tensor")
+    x, w = roots_genlaguerre(order, 0.5)
+    x, w = np.ascontiguousarray(x), np.ascontiguousarray(w)
+    stream = torch.cuda.current_stream(u.device).cuda_stream
+    _lib.check(_lib.lib().bfq_project_maxwellians(
+        n_k - 1, l_max, x.ctypes.data_as(_lib._f64p), w.ctypes.data_as(_lib._f64p), order,
+        u.data_ptr(), temp.data_ptr(), noise.data_ptr() if noise is not None else None, out.data_ptr(),
+        b, stream))
+    return out
+
+
+def perturbed_maxwellians_device(n_k: int, l_max: int, n_cells: int, seed: int, start: int = 0, device=0):
+    """``perturbed_maxwellians`` with the projection on the GPU: the same seeded
+    draws (u, T, noise per 1024-cell block), so the cells agree with the host
+    generator to rounding.  Returns a float64 CUDA tensor."""
+    import torch
+
+    n_q = (l_max + 1) ** 2
+    sig = noise_sigma(n_k, l_max)
+    us, ts, ns = [], [], []
+    for blk, lo, hi, _ in _blocks(n_cells, start):
+        rng = np.random.default_rng(np.random.SeedSequence((seed, blk)))
+        u = rng.uniform(-0.3, 0.3, (BLOCK, 3))
+        t = rng.uniform(0.8, 1.2, BLOCK)
+        noise = rng.normal(size=(BLOCK, n_k, n_q)) * sig
+        _zero_invariants(noise)
+        us.append(u[lo:hi])
+        ts.append(t[lo:hi])
+        ns.append(noise[lo:hi])
+    dev = torch.device("cuda", device) if isinstance(device, int) else torch.device(device)
+    to = lambda a: torch.from_numpy(np.ascontiguousarray(np.concatenate(a))).to(dev)  # noqa: E731
+    return project_maxwellians_device(n_k, l_max, to(us), to(ts), noise=to(ns))
+
+
+def bimodal_device(n_k: int, l_max: int, n_cells: int, seed: int, start: int = 0, device=0):
+    """``bimodal`` (config 5) with the projection on the GPU."""
+    import torch
+
+    ds = []
+    for blk, lo, hi, _ in _blocks(n_cells, start):
+        rng = np.random.default_rng(np.random.SeedSequence((seed, blk)))
+        u = rng.uniform(0.5, 1.5, BLOCK)
+        n = rng.normal(size=(BLOCK, 3))
+        n /= np.linalg.norm(n, axis=1, keepdims=True)
+        ds.append((u[:, None] * n)[lo:hi])
+    dev = torch.device("cuda", device) if isinstance(device, int) else torch.device(device)
+    d = torch.from_numpy(np.ascontiguousarray(np.concatenate(ds))).to(dev)
+    ones = torch.ones(d.shape[0], dtype=torch.float64, device=dev)
+    a = project_maxwellians_device(n_k, l_max, d.contiguous(), ones)
+    b = project_maxwellians_device(n_k, l_max, (-d).contiguous(), ones)
+    return 0.5 * (a + b)

@@ -25,6 +25,12 @@ for name in names:
     st = rbuild.last_stats()
     err = np.abs(r.values - ref.r.values).max() / np.abs(ref.r.values).max()
     tf = 2 * st["contract_macs"] / st["ms_contract"] / 1e9 if st["ms_contract"] else 0
+    d = np.abs(r.values - ref.r.values) / np.abs(ref.r.values).max()
+    worst = np.unravel_index(d.argmax(), d.shape)
+    if len(sys.argv) > 1:
+        print(f"  by k1: {[float(f'{d[k].max():.1e}') for k in range(d.shape[0])]}  argmax (k,a,b,tau) {worst} "
+              f"{ref.r.channels.triplets[worst[3]]}")
+        np.save(os.path.join(ROOT, "gpurun_out", f"r_{name}_tau{worst[3]}.npy"), r.values[..., worst[3]])
     print(f"{name}: rel_linf {err:.3e}  wall {wall:.2f}s  device {st['ms_total']:.1f} ms  "
           f"contract {st['ms_contract']:.1f} ms ({tf:.2f} exec TF/s, alg {2*st['alg_macs']/1e12:.3f} TFLOP)  "
           f"points {st['n_points']}", flush=True)
