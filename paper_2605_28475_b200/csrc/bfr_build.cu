@@ -413,23 +413,27 @@ __global__ void k_radial(RadParams p) {
 struct GsParams {
   const double *g, *A_hi, *A_lo, *yb, *tw, *w3j;
   const int32_t* trip;
-  int c0, patch, n_o, n_t, nq, L, nk;
+  const int32_t* chan;  // batch slot -> channel
+  int patch, n_o, n_t, nq, L, nk;
   double swc;  // 2 pi sum(w_chi)
   double *gq, *lq;
 };
 
 __global__ void k_gstack(GsParams p) {
-  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  // one thread per (q, j): patch 0 loops over the Duffy axis, so (q) alone is too little parallelism
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int c = blockIdx.y;
-  if (q >= p.nq) return;
-  const int tau = p.c0 + c;
+  if (i >= p.nq * p.nk) return;
+  const int jj = i / p.nq, q = i - jj * p.nq;
+  const int tau = p.chan[c];
   const int l1 = p.trip[3 * tau], l2 = p.trip[3 * tau + 1], l3 = p.trip[3 * tau + 2];
   const int mm = min(l1, l3);
   const int n_ot = p.n_o * p.n_t;
   const double* w3 = p.w3j + (size_t)tau * (p.L + 1);
   const double zon1 = sqrt((2 * l1 + 1) / (4.0 * PI)), zon2 = sqrt((2 * l2 + 1) / (4.0 * PI));
   const int t_n = p.patch == 0 ? p.n_t : 1;
-  for (int j = 0; j < p.nk; ++j) {
+  {
+    const int j = jj;
     dd acc = {0.0, 0.0};
     for (int tt = 0; tt < t_n; ++tt) {
       const int ot = p.patch == 0 ? q * p.n_t + tt : q;
@@ -448,6 +452,7 @@ __global__ void k_gstack(GsParams p) {
     }
     p.gq[((size_t)c * p.nk + j) * p.nq + q] = acc.hi + acc.lo;
   }
+  if (jj != 0) return;
   double la = 0.0;
   for (int tt = 0; tt < t_n; ++tt) {
     const int ot = p.patch == 0 ? q * p.n_t + tt : q;
@@ -464,7 +469,8 @@ __global__ void k_gstack(GsParams p) {
 struct XrParams {
   const double *gq, *lq, *me, *pf, *phi, *env;
   const int32_t* trip;
-  int c0, n_e, nq, nk;
+  const int32_t* chan;  // batch slot -> channel
+  int n_e, nq, nk;
   long long P, PS;
   double* X;
 };
@@ -475,7 +481,7 @@ __global__ void k_xrows(XrParams p) {
   const int c = blockIdx.y;
   if (i >= p.P) return;
   const int nk = NK > 0 ? NK : p.nk;
-  const int tau = p.c0 + c;
+  const int tau = p.chan[c];
   const int l1 = p.trip[3 * tau];
   const int E = (int)(i / p.nq), q = (int)(i - (long long)E * p.nq);
   constexpr int NA = NK > 0 ? NK : NK_MAX;
@@ -507,29 +513,35 @@ __global__ void k_xrows(XrParams p) {
 }
 
 // ------------------------------------------------------------ contraction
-// part[job][split][row][a*nk+b] = sum_{p in split} X[row,p] U[a,p] W[b,p]
-// kind 0: rows = gain + fast loss (2 nk), U = phi_l2(v), W = phi_l3(w)
-// kind 1: rows = slow loss (nk),          U = phi_l2(w), W = phi_l3(v)
+// Jobs are ordered (l2, l3) = (x, y) pairs: every channel (l1, x, y) contributes
+// its gain and fast-loss rows (U = phi_x(v), W = phi_y(w)), every channel
+// (l1, y, x) its slow-loss rows -- those share the same U (x) W product with
+// (a, b) swapped.  A job's rows are cut into blocks of <= MT 8-row tiles;
+//   part[block][split][row][a*nk+b] = sum_{p in split} X[rowtab[row], p] U[a,p] W[b,p].
+struct TriBlock {
+  int x, y, row0, nrows;  // rows [row0, row0+nrows) of the batch row table
+};
+
 struct TriParams {
   const double *X, *phi;
-  const int32_t* trip;
-  int c0, nk, kind, S, PR;
+  const TriBlock* blocks;
+  const int32_t* rowtab;  // batch row -> X row (slot*3nk + offset)
+  int nk, S, PR, rows_max;
   long long P, PS;
-  double* part;  // [(2c+kind)*S + split][2nk][nk*nk]
+  double* part;  // [block][split][rows_max][nk*nk]
 };
 
 template <int MT, int NPW>
 __global__ void __launch_bounds__(256) k_tri(TriParams p) {
   extern __shared__ double sm[];
-  const int c = blockIdx.y, split = blockIdx.x;
-  const int nk = p.nk, nn = nk * nk, kind = p.kind;
-  const int rows = kind ? nk : 2 * nk;
+  const TriBlock blk = p.blocks[blockIdx.y];
+  const int split = blockIdx.x;
+  const int nk = p.nk, nn = nk * nk;
+  const int rows = blk.nrows, mtn = (rows + 7) / 8;
   const int rs = rows + 2 * nk;  // staged rows per chunk
-  const int tau = p.c0 + c;
-  const int l2 = p.trip[3 * tau + 1], l3 = p.trip[3 * tau + 2];
-  const double* X = p.X + ((size_t)c * 3 * nk + (kind ? 2 * nk : 0)) * p.PS;
-  const double* U = p.phi + (size_t)((l2 * 2 + kind) * nk) * p.PS;
-  const double* W = p.phi + (size_t)((l3 * 2 + (1 - kind)) * nk) * p.PS;
+  const int* rt = p.rowtab + blk.row0;
+  const double* U = p.phi + (size_t)((blk.x * 2 + 0) * nk) * p.PS;
+  const double* W = p.phi + (size_t)((blk.y * 2 + 1) * nk) * p.PS;
   const long long pb = (long long)split * p.PR;
   const long long pe = min((long long)p.P, pb + p.PR);
   const int nchunk = (int)((pe - pb + PC - 1) / PC);
@@ -554,14 +566,14 @@ __global__ void __launch_bounds__(256) k_tri(TriParams p) {
 #pragma unroll
     for (int i = 0; i < NPW; ++i) acc[mt][i][0] = acc[mt][i][1] = 0.0;
 
-  const int stage_d = rs * SROW;
+  const int stage_d = (p.rows_max + 2 * nk) * SROW;
   auto load_chunk = [&](int ch, int st) {
     const long long p0 = pb + (long long)ch * PC;
     double* dst = sm + st * stage_d;
     const int nv = rs * (PC / 2);
     for (int v = threadIdx.x; v < nv; v += blockDim.x) {
       const int r = v / (PC / 2), cc = (v - r * (PC / 2)) * 2;
-      const double* src = r < rows ? X + (size_t)r * p.PS
+      const double* src = r < rows ? p.X + (size_t)rt[r] * p.PS
                                    : (r < rows + nk ? U + (size_t)(r - rows) * p.PS
                                                     : W + (size_t)(r - rows - nk) * p.PS);
       const long long pp = p0 + cc;
@@ -592,13 +604,14 @@ __global__ void __launch_bounds__(256) k_tri(TriParams p) {
         if (warp + 8 * i < ntiles) {
           const double b = s[uoff[i] + col] * s[woff[i] + col];
 #pragma unroll
-          for (int mt = 0; mt < MT; ++mt) dmma884(acc[mt][i][0], acc[mt][i][1], a[mt], b);
+          for (int mt = 0; mt < MT; ++mt)
+            if (mt < mtn) dmma884(acc[mt][i][0], acc[mt][i][1], a[mt], b);
         }
       }
     }
     __syncthreads();
   }
-  double* out = p.part + ((size_t)(2 * c + kind) * p.S + split) * (size_t)(2 * nk * nn);
+  double* out = p.part + ((size_t)blockIdx.y * p.S + split) * (size_t)p.rows_max * nn;
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt) {
     const int row = mt * 8 + r0;
@@ -616,22 +629,29 @@ __global__ void __launch_bounds__(256) k_tri(TriParams p) {
   }
 }
 
-// halves[h][tau][k][ab] += sum over splits (fixed order): h = 0 gain, 1 fast loss, 2 slow loss
-__global__ void k_reduce(const double* part, int c0, int nb, int nk, int S, int n_t, double* halves) {
+// halves[h][tau][k][ab] += sum over splits (fixed order); rowmap[i] = (tau*3 + h)*nk + k,
+// negative (-1 - code) when the job computed the transposed (b, a) block
+__global__ void k_reduce(const double* part, const TriBlock* blocks, int nblk, const int32_t* rowmap, int nk,
+                         int S, int rows_max, int n_t, double* halves) {
   const int nn = nk * nk;
-  const long long tot = (long long)nb * 3 * nk * nn;
+  const long long tot = (long long)nblk * rows_max * nn;
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= tot) return;
   const int ab = (int)(i % nn);
-  const int r = (int)((i / nn) % (3 * nk));
-  const int c = (int)(i / ((long long)nn * 3 * nk));
-  const int kind = r >= 2 * nk;
-  const int row = kind ? r - 2 * nk : r;
-  const double* src = part + ((size_t)(2 * c + kind) * S) * (size_t)(2 * nk * nn) + (size_t)row * nn + ab;
+  const int row = (int)((i / nn) % rows_max);
+  const int b = (int)(i / ((long long)nn * rows_max));
+  const TriBlock blk = blocks[b];
+  if (row >= blk.nrows) return;
+  int code = rowmap[blk.row0 + row];
+  const bool trans = code < 0;
+  if (trans) code = -1 - code;
+  const double* src = part + ((size_t)b * S) * (size_t)rows_max * nn + (size_t)row * nn + ab;
   double s = 0.0;
-  for (int sp = 0; sp < S; ++sp) s += src[(size_t)sp * 2 * nk * nn];
-  const int h = r / nk, k = r - h * nk;
-  halves[(((size_t)h * n_t + c0 + c) * nk + k) * nn + ab] += s;
+  for (int sp = 0; sp < S; ++sp) s += src[(size_t)sp * rows_max * nn];
+  const int k = code % nk, th = code / nk, h = th % 3, tau = th / 3;
+  const int a = ab / nk, bb = ab - a * nk;
+  const int dst = trans ? bb * nk + a : ab;
+  halves[(((size_t)h * n_t + tau) * nk + k) * nn + dst] += s;
 }
 
 // full[tau] = gain[tau] + gain[swap]^T(2,3) - (loss_f + loss_s)[tau]  (kinematic.py:552-558)
@@ -849,18 +869,18 @@ int assemble(const bfr_desc& d, int device, double* r_out, double* halves_out, b
   }
   BFR_TRY(cudaMemset(halves, 0, (size_t)3 * n_t * n3 * 8));
 
-  const int mt0 = (2 * nk + 7) / 8, mt1 = (nk + 7) / 8, npw = ((nn + 7) / 8 + 7) / 8;
-  TriKernel tri0 = pick_tri(mt0, npw), tri1 = pick_tri(mt1, npw);
-  if (!tri0 || !tri1) {
+  // 8-row tiles per contraction block: 5 while the accumulators (MT x NPW x 2) keep
+  // k_tri at <= 128 registers (two CTAs per SM), 3 for the wider n_k = 14..17 tiling
+  const int npw = ((nn + 7) / 8 + 7) / 8;
+  const int MT_BLK = npw <= 3 ? 5 : 3;
+  TriKernel tri = pick_tri(MT_BLK, npw);
+  if (!tri) {
     set_error("n_k outside the contraction kernel's tiling (n_k <= 17)");
     return BFQ_EINVAL;
   }
-  const size_t tri_smem0 = (size_t)2 * (2 * nk + 2 * nk) * SROW * 8;
-  const size_t tri_smem1 = (size_t)2 * (nk + 2 * nk) * SROW * 8;
-  // tri0 and tri1 may be the same instantiation (small n_k): give both the larger size
-  BFR_TRY(cudaFuncSetAttribute(tri0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tri_smem0));
-  if (tri1 != tri0)
-    BFR_TRY(cudaFuncSetAttribute(tri1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tri_smem1));
+  const int rows_max = 8 * MT_BLK;
+  const size_t tri_smem = (size_t)2 * (rows_max + 2 * nk) * SROW * 8;
+  BFR_TRY(cudaFuncSetAttribute(tri, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tri_smem));
   XrKernel xr = pick_xrows(nk);
   const size_t atab_sm = atab_smem(nlm, nk);
   {
@@ -901,25 +921,98 @@ int assemble(const bfr_desc& d, int device, double* r_out, double* halves_out, b
     max_PS = std::max(max_PS, q.PS);
     if (st) st->n_points[patch] = q.P;
   }
-  // channel batches: integrand-row scratch <= ~6 GB
+
+  // channel batches = unions of unordered (l2, l3) pairs, integrand rows <= ~6 GB
   const size_t xrow_bytes = (size_t)3 * nk * max_PS * 8;
-  const int nb = (int)std::max<size_t>(1, std::min<size_t>((size_t)n_t, ((size_t)6 << 30) / xrow_bytes));
+  const int cap = (int)std::max<size_t>(1, std::min<size_t>((size_t)n_t, ((size_t)6 << 30) / xrow_bytes));
+  struct Batch {
+    std::vector<int32_t> chan, rowtab, rowmap;
+    std::vector<TriBlock> blocks;
+  };
+  std::vector<Batch> batches;
+  {
+    std::vector<std::vector<int>> by_pair((size_t)(L + 1) * (L + 1));
+    for (int t = 0; t < n_t; ++t) by_pair[d.triplets[3 * t + 1] * (L + 1) + d.triplets[3 * t + 2]].push_back(t);
+    Batch cur;
+    auto flush = [&]() {
+      if (cur.chan.empty()) return;
+      // slots in (l1, tau) order: consecutive k_gstack CTAs then share one l1's A table in L2
+      std::sort(cur.chan.begin(), cur.chan.end());  // channels are enumerated l1-major
+      // slots, then the ordered-pair jobs of every pair present
+      std::vector<int> slot(n_t, -1);
+      for (size_t i = 0; i < cur.chan.size(); ++i) slot[cur.chan[i]] = (int)i;
+      for (int x = 0; x <= L; ++x)
+        for (int y = 0; y <= L; ++y) {
+          const auto& fwd = by_pair[x * (L + 1) + y];  // gain + fast loss rows
+          const auto& rev = by_pair[y * (L + 1) + x];  // slow loss rows, transposed
+          if (fwd.empty() && rev.empty()) continue;
+          if ((!fwd.empty() && slot[fwd[0]] < 0) || (!rev.empty() && slot[rev[0]] < 0)) continue;
+          const int row0 = (int)cur.rowtab.size();
+          for (int t : fwd)
+            for (int h = 0; h < 2; ++h)
+              for (int k = 0; k < nk; ++k) {
+                cur.rowtab.push_back(slot[t] * 3 * nk + h * nk + k);
+                cur.rowmap.push_back((t * 3 + h) * nk + k);
+              }
+          for (int t : rev)
+            for (int k = 0; k < nk; ++k) {
+              cur.rowtab.push_back(slot[t] * 3 * nk + 2 * nk + k);
+              cur.rowmap.push_back(-1 - ((t * 3 + 2) * nk + k));
+            }
+          const int nrows = (int)cur.rowtab.size() - row0;
+          const int ntile = (nrows + 7) / 8, nblk = (ntile + MT_BLK - 1) / MT_BLK;
+          int r = 0;
+          for (int bi = 0; bi < nblk; ++bi) {
+            const int tiles = (ntile - bi * (ntile / nblk)) > 0 ? (ntile / nblk + (bi < ntile % nblk ? 1 : 0)) : 0;
+            const int nr = std::min(tiles * 8, nrows - r);
+            if (nr > 0) cur.blocks.push_back({x, y, row0 + r, nr});
+            r += nr;
+          }
+        }
+      batches.push_back(std::move(cur));
+      cur = Batch();
+    };
+    for (int x = 0; x <= L; ++x)
+      for (int y = x; y <= L; ++y) {
+        std::vector<int> members = by_pair[x * (L + 1) + y];
+        if (y != x) members.insert(members.end(), by_pair[y * (L + 1) + x].begin(), by_pair[y * (L + 1) + x].end());
+        if (members.empty()) continue;
+        if (!cur.chan.empty() && (int)(cur.chan.size() + members.size()) > cap) flush();
+        cur.chan.insert(cur.chan.end(), members.begin(), members.end());
+      }
+    flush();
+  }
+  int max_chan = 0, max_rows = 0, max_blocks = 0;
+  for (const Batch& bt : batches) {
+    max_chan = std::max(max_chan, (int)bt.chan.size());
+    max_rows = std::max(max_rows, (int)bt.rowtab.size());
+    max_blocks = std::max(max_blocks, (int)bt.blocks.size());
+  }
   double* geo = db.alloc<double>((size_t)G_NF * max_ot);
   double* yb = db.alloc<double>((size_t)nlm * max_ot);
   double* A = db.alloc<double>((size_t)2 * nlm * nk * max_ot);  // hi, lo
   double* env = db.alloc<double>((size_t)max_PS);
   double* phi = db.alloc<double>((size_t)(L + 1) * 2 * nk * max_PS);
-  double* X = db.alloc<double>((size_t)nb * 3 * nk * max_PS);
-  double* gq = db.alloc<double>((size_t)nb * nk * max_nq);
-  double* lq = db.alloc<double>((size_t)nb * max_nq);
-  double* part = db.alloc<double>((size_t)nb * 2 * max_S * 2 * nk * nn);
+  double* X = db.alloc<double>((size_t)max_chan * 3 * nk * max_PS);
+  double* gq = db.alloc<double>((size_t)max_chan * nk * max_nq);
+  double* lq = db.alloc<double>((size_t)max_chan * max_nq);
+  double* part = db.alloc<double>((size_t)max_blocks * max_S * rows_max * nn);
   if (!geo || !yb || !A || !env || !phi || !X || !gq || !lq || !part) {
     set_error("device allocation failed");
     return BFQ_ENOMEM;
   }
+  // batch tables, uploaded once
+  std::vector<int32_t*> d_chan(batches.size()), d_rowtab(batches.size()), d_rowmap(batches.size());
+  std::vector<TriBlock*> d_blocks(batches.size());
+  for (size_t bi = 0; bi < batches.size(); ++bi) {
+    if ((rc = upload(db, batches[bi].chan.data(), batches[bi].chan.size(), &d_chan[bi]))) return rc;
+    if ((rc = upload(db, batches[bi].rowtab.data(), batches[bi].rowtab.size(), &d_rowtab[bi]))) return rc;
+    if ((rc = upload(db, batches[bi].rowmap.data(), batches[bi].rowmap.size(), &d_rowmap[bi]))) return rc;
+    if ((rc = upload(db, batches[bi].blocks.data(), batches[bi].blocks.size(), &d_blocks[bi]))) return rc;
+  }
   // Row tails [P, PS) are never read: k_tri zero-fills past the last point.
 
-  const int n_batches = 2 * ((n_t + nb - 1) / nb);
+  const int n_batches = 2 * (int)batches.size();
   std::vector<cudaEvent_t> evs(2 + 2 * n_batches, nullptr);
   struct EvGuard {
     std::vector<cudaEvent_t>& e;
@@ -954,27 +1047,26 @@ int assemble(const bfr_desc& d, int device, double* r_out, double* halves_out, b
       k_radial<<<blocks_for(P, 128), 128>>>(rp);
       BFR_LAUNCH_CHECK("k_radial");
     }
-    for (int c0 = 0; c0 < n_t; c0 += nb, ++ib) {
-      const int cb = std::min(nb, n_t - c0);
-      GsParams gp{geo, A, A + (size_t)nlm * nk * n_ot, yb, q.tw, d_w3j, d_trip, c0, patch, n_o, n_tt, nq, L, nk,
-                  swc, gq, lq};
-      k_gstack<<<dim3(blocks_for(nq, 128), cb), 128>>>(gp);
+    for (size_t bi = 0; bi < batches.size(); ++bi, ++ib) {
+      const Batch& bt = batches[bi];
+      const int cb = (int)bt.chan.size(), nblk = (int)bt.blocks.size();
+      GsParams gp{geo, A, A + (size_t)nlm * nk * n_ot, yb, q.tw, d_w3j, d_trip, d_chan[bi], patch, n_o, n_tt, nq,
+                  L, nk, swc, gq, lq};
+      k_gstack<<<dim3(blocks_for((long long)nq * nk, 128), cb), 128>>>(gp);
       BFR_LAUNCH_CHECK("k_gstack");
-      XrParams xp{gq, lq, d_me, d_pf, phi, env, d_trip, c0, d.n_e, nq, nk, P, PS, X};
+      XrParams xp{gq, lq, d_me, d_pf, phi, env, d_trip, d_chan[bi], d.n_e, nq, nk, P, PS, X};
       xr<<<dim3(blocks_for(P, 128), cb), 128>>>(xp);
       BFR_LAUNCH_CHECK("xr");
       BFR_TRY(cudaEventRecord(evs[2 + 2 * ib]));
-      TriParams tp{X, phi, d_trip, c0, nk, 0, S, PR, P, PS, part};
-      tri0<<<dim3(S, cb), 256, tri_smem0>>>(tp);
-      BFR_LAUNCH_CHECK("tri0");
-      tp.kind = 1;
-      tri1<<<dim3(S, cb), 256, tri_smem1>>>(tp);
-      BFR_LAUNCH_CHECK("tri1");
+      TriParams tp{X, phi, d_blocks[bi], d_rowtab[bi], nk, S, PR, rows_max, P, PS, part};
+      tri<<<dim3(S, nblk), 256, tri_smem>>>(tp);
+      BFR_LAUNCH_CHECK("tri");
       BFR_TRY(cudaEventRecord(evs[3 + 2 * ib]));
-      k_reduce<<<blocks_for((long long)cb * 3 * nk * nn, 256), 256>>>(part, c0, cb, nk, S, n_t, halves);
+      k_reduce<<<blocks_for((long long)nblk * rows_max * nn, 256), 256>>>(part, d_blocks[bi], nblk, d_rowmap[bi],
+                                                                             nk, S, rows_max, n_t, halves);
       BFR_LAUNCH_CHECK("k_reduce");
-      exec_macs += (double)cb * (double)S * PR * 8.0 * 8.0 *
-                   ((double)mt0 * ((nn + 7) / 8) + (double)mt1 * ((nn + 7) / 8));
+      for (const TriBlock& tb : bt.blocks)
+        exec_macs += (double)S * PR * 64.0 * ((tb.nrows + 7) / 8) * ((nn + 7) / 8);
       alg_macs += (double)cb * P * 3.0 * nk * nn;
       xbytes += (double)cb * 3 * nk * P * 8.0 * 2.0;
     }
