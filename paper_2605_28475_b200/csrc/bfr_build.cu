@@ -414,6 +414,7 @@ struct GsParams {
   const double *g, *A_hi, *A_lo, *yb, *tw, *w3j;
   const int32_t* trip;
   const int32_t* chan;  // batch slot -> channel
+  int nb;               // slots in the batch (gq holds hi then lo halves)
   int patch, n_o, n_t, nq, L, nk;
   double swc;  // 2 pi sum(w_chi)
   double *gq, *lq;
@@ -450,7 +451,9 @@ __global__ void k_gstack(GsParams p) {
       if (p.patch == 0) acc = dd_add(acc, dd_mul_d(dd_mul_d(gv, p.g[(size_t)G_FGEO * n_ot + ot]), p.tw[tt]));
       else acc = gv;
     }
-    p.gq[((size_t)c * p.nk + j) * p.nq + q] = acc.hi + acc.lo;
+    const dd g = fast_two_sum(acc.hi, acc.lo);
+    p.gq[((size_t)c * p.nk + j) * p.nq + q] = g.hi;  // kept double-double into the monomial sum
+    p.gq[((size_t)(p.nb + c) * p.nk + j) * p.nq + q] = g.lo;
   }
   if (jj != 0) return;
   double la = 0.0;
@@ -470,7 +473,8 @@ struct XrParams {
   const double *gq, *lq, *me, *pf, *phi, *env;
   const int32_t* trip;
   const int32_t* chan;  // batch slot -> channel
-  int n_e, nq, nk;
+  int nb;               // slots in the batch (gq holds hi then lo halves)
+  int n_e, nq, nk, L;
   long long P, PS;
   double* X;
 };
@@ -485,9 +489,12 @@ __global__ void k_xrows(XrParams p) {
   const int l1 = p.trip[3 * tau];
   const int E = (int)(i / p.nq), q = (int)(i - (long long)E * p.nq);
   constexpr int NA = NK > 0 ? NK : NK_MAX;
-  double gj[NA];
+  double gj[NA], gl[NA];
 #pragma unroll
-  for (int j = 0; j < NA; ++j) gj[j] = j < nk ? p.gq[((size_t)c * nk + j) * p.nq + q] : 0.0;
+  for (int j = 0; j < NA; ++j) {
+    gj[j] = j < nk ? p.gq[((size_t)c * nk + j) * p.nq + q] : 0.0;
+    gl[j] = j < nk ? p.gq[((size_t)(p.nb + c) * nk + j) * p.nq + q] : 0.0;
+  }
   const double env = p.env[i];
   const double lenv = env * p.lq[(size_t)c * p.nq + q];
   const double* me = p.me + ((size_t)l1 * p.n_e + E) * nk * nk;
@@ -501,10 +508,12 @@ __global__ void k_xrows(XrParams p) {
 #pragma unroll
     for (int j = 0; j < NA; ++j)
       if (j < nk) {
-        const dd pr = two_prod(me[k * nk + j], gj[j]);
+        // the reference rounds mono * eta^j before its j-sum (einsum path jE,kj->jkE); so do we
+        const double ch = me[k * nk + j];
+        const dd pr = two_prod(ch, gj[j]);
         const dd sm = two_sum(s, pr.hi);
         s = sm.hi;
-        comp += pr.lo + sm.lo;
+        comp = fma(ch, gl[j], comp + (pr.lo + sm.lo));
       }
     X[(size_t)k * p.PS] = ((s + comp) * pf[k]) * env;
     X[(size_t)(nk + k) * p.PS] = pv[(size_t)k * p.PS] * lenv;
@@ -835,8 +844,10 @@ int assemble(const bfr_desc& d, int device, double* r_out, double* halves_out, b
   if ((rc = upload(db, es.data(), es.size(), &d_epss))) return rc;
   if ((rc = upload(db, d.eps_w, (size_t)d.n_eps, &d_epsw))) return rc;
   if ((rc = upload(db, d.norms, (size_t)(L + 1) * nk, &d_norms))) return rc;
-  // me[l][E][k][j] = mono[l][k][j] * eta_E^j and pf[l][E][k] = norms[l][k] * eta_E^(l/2),
-  // rounded exactly as the reference's einsum operands (kinematic.py:466-471)
+  // me[l][E][k][j] = fl(mono[l][k][j] * eta_E^j) and pf[l][E][k] = norms[l][k] * eta_E^(l/2):
+  // the reference's own fp64 einsum operands (kinematic.py:466-471; numpy's path rounds
+  // mono * eta^j first).  Measured: keeping that product exact moves R further from the
+  // reference (N=12 1.2e-12 -> 2.3e-12), so the reference's rounding is reproduced.
   double* d_pf;
   {
     std::vector<double> me((size_t)(L + 1) * d.n_e * nn), pf((size_t)(L + 1) * d.n_e * nk);
@@ -994,7 +1005,7 @@ int assemble(const bfr_desc& d, int device, double* r_out, double* halves_out, b
   double* env = db.alloc<double>((size_t)max_PS);
   double* phi = db.alloc<double>((size_t)(L + 1) * 2 * nk * max_PS);
   double* X = db.alloc<double>((size_t)max_chan * 3 * nk * max_PS);
-  double* gq = db.alloc<double>((size_t)max_chan * nk * max_nq);
+  double* gq = db.alloc<double>((size_t)2 * max_chan * nk * max_nq);
   double* lq = db.alloc<double>((size_t)max_chan * max_nq);
   double* part = db.alloc<double>((size_t)max_blocks * max_S * rows_max * nn);
   if (!geo || !yb || !A || !env || !phi || !X || !gq || !lq || !part) {
@@ -1050,11 +1061,11 @@ int assemble(const bfr_desc& d, int device, double* r_out, double* halves_out, b
     for (size_t bi = 0; bi < batches.size(); ++bi, ++ib) {
       const Batch& bt = batches[bi];
       const int cb = (int)bt.chan.size(), nblk = (int)bt.blocks.size();
-      GsParams gp{geo, A, A + (size_t)nlm * nk * n_ot, yb, q.tw, d_w3j, d_trip, d_chan[bi], patch, n_o, n_tt, nq,
-                  L, nk, swc, gq, lq};
+      GsParams gp{geo, A, A + (size_t)nlm * nk * n_ot, yb, q.tw, d_w3j, d_trip, d_chan[bi], cb, patch, n_o, n_tt,
+                  nq, L, nk, swc, gq, lq};
       k_gstack<<<dim3(blocks_for((long long)nq * nk, 128), cb), 128>>>(gp);
       BFR_LAUNCH_CHECK("k_gstack");
-      XrParams xp{gq, lq, d_me, d_pf, phi, env, d_trip, d_chan[bi], d.n_e, nq, nk, P, PS, X};
+      XrParams xp{gq, lq, d_me, d_pf, phi, env, d_trip, d_chan[bi], cb, d.n_e, nq, nk, L, P, PS, X};
       xr<<<dim3(blocks_for(P, 128), cb), 128>>>(xp);
       BFR_LAUNCH_CHECK("xr");
       BFR_TRY(cudaEventRecord(evs[2 + 2 * ib]));
