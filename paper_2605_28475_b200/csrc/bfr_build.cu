@@ -592,16 +592,16 @@ __global__ void __launch_bounds__(256) k_tri(TriParams p) {
     cp_async_commit();
   };
 
+  // three-stage ring, one barrier per chunk: the load of chunk ch+2 is issued after
+  // the barrier that ends chunk ch-1's reads of the same stage
   if (nchunk > 0) load_chunk(0, 0);
+  if (nchunk > 1) load_chunk(1, 1);
   for (int ch = 0; ch < nchunk; ++ch) {
-    if (ch + 1 < nchunk) {
-      load_chunk(ch + 1, (ch + 1) & 1);
-      cp_async_wait1();
-    } else {
-      cp_async_wait0();
-    }
+    if (ch + 1 < nchunk) cp_async_wait1();
+    else cp_async_wait0();
     __syncthreads();
-    const double* s = sm + (ch & 1) * stage_d;
+    if (ch + 2 < nchunk) load_chunk(ch + 2, (ch + 2) % 3);
+    const double* s = sm + (ch % 3) * stage_d;
 #pragma unroll 2
     for (int kk = 0; kk < PC / 4; ++kk) {
       const int col = kk * 4 + kq;
@@ -618,7 +618,6 @@ __global__ void __launch_bounds__(256) k_tri(TriParams p) {
         }
       }
     }
-    __syncthreads();
   }
   double* out = p.part + ((size_t)blockIdx.y * p.S + split) * (size_t)p.rows_max * nn;
 #pragma unroll
@@ -890,7 +889,7 @@ int assemble(const bfr_desc& d, int device, double* r_out, double* halves_out, b
     return BFQ_EINVAL;
   }
   const int rows_max = 8 * MT_BLK;
-  const size_t tri_smem = (size_t)2 * (rows_max + 2 * nk) * SROW * 8;
+  const size_t tri_smem = (size_t)3 * (rows_max + 2 * nk) * SROW * 8;
   BFR_TRY(cudaFuncSetAttribute(tri, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tri_smem));
   XrKernel xr = pick_xrows(nk);
   const size_t atab_sm = atab_smem(nlm, nk);
