@@ -142,3 +142,12 @@ def test_rtensor_type_is_reference_compatible():
     r = rbuild.assemble_r_tensor(SpectralConfig(2, 2, 1.0))
     assert isinstance(r, RTensor) and r.values.shape == (3, 3, 3, r.channels.n_t)
     assert r.values.flags.c_contiguous and r.max_zeroed == 0.0
+
+
+def test_build_is_bitwise_deterministic():
+    """Fixed-order split reduction: two assemblies of the same operator are identical."""
+    ref = load_op("hs_n8")
+    g = rbuild.GridSpec(*ref.r.grid)
+    a = rbuild.assemble_r_tensor(ref.cfg, g).values
+    b = rbuild.assemble_r_tensor(ref.cfg, g).values
+    assert np.array_equal(a, b)
