@@ -268,6 +268,9 @@ QKernel pick_fixed2(int mt, int cells) {
     if (cells == 8) return bfq_q_kernel2<1, 8, BILIN, NK, QS>;
     if (cells == 4) return bfq_q_kernel2<1, 4, BILIN, NK, QS>;
   } else if constexpr (MT == 2) {
+    if constexpr (NK == 9) {
+      if (cells == 8) return bfq_q_kernel2<2, 8, BILIN, NK, QS>;  // X1: one DMMA tile per cell
+    }
     if (cells == 4) return bfq_q_kernel2<2, 4, BILIN, NK, QS>;
     if (cells == 2) return bfq_q_kernel2<2, 2, BILIN, NK, QS>;
   } else {

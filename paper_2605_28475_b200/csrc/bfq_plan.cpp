@@ -52,7 +52,10 @@ static int header_bytes(int max_chan) { return 96 + (MAX_TEAMS * max_chan * 4 + 
 static bool choose_config(int nk, int qs, int k2s, int nf, int smem_limit, int max_chan, KernelConfig& c) {
   c.mt = (nk + 7) / 8;
   c.nf = nf;
-  const int max_cells = c.mt == 1 ? 8 : (c.mt == 2 ? 4 : 2);  // stage-1 accumulators in registers
+  // stage-1 accumulators in registers; n_k = 9 runs its last index on DFMA (X1,
+  // bfq_qkernel2.cuh), leaving one 8x8 tile per cell, so it takes 8 cells per tile
+  int max_cells = c.mt == 1 ? 8 : (c.mt == 2 ? 4 : 2);
+  if (nk == 9 && qs == 84 && !std::getenv("BFQ_GENERIC") && !std::getenv("BFQ_NO_X1_CELLS8")) max_cells = 8;
   int force_cells = 0, kernel = 2;
   if (const char* e = std::getenv("BFQ_CELLS")) force_cells = std::atoi(e);
   if (const char* e = std::getenv("BFQ_KERNEL")) kernel = std::atoi(e);
