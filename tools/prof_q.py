@@ -17,7 +17,14 @@ ap.add_argument("--cells", type=int, default=8192)
 ap.add_argument("--iters", type=int, default=4)
 ap.add_argument("--bilinear", action="store_true")
 a = ap.parse_args()
-op = load_cache(os.path.join(ROOT, "operators", a.op + ".bfct"))
+path = os.path.join(ROOT, "operators", a.op + ".bfct")
+if os.path.exists(path):
+    op = load_cache(path)
+else:  # hs_n16 is not shipped: assemble it on the GPU (bfr_assemble)
+    from paper_2605_28475_b200 import rbuild
+    from paper_2605_28475_b200.operator import SpectralConfig
+    n = int(a.op.split("_n")[1])
+    op = rbuild.build_operator(SpectralConfig(n, n, 0.0 if a.op.startswith("mm") else 1.0))
 cells = inputs.perturbed_maxwellians(op.cfg.n_k, op.cfg.l_max, a.cells, seed=1)
 f = torch.from_numpy(cells).cuda()
 f3 = f.clone() if a.bilinear else None
