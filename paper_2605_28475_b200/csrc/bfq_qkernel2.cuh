@@ -128,8 +128,10 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
 
 #ifdef BFQ_PHASE_CLOCKS
   const bool clk_on = (p.debug & 8) != 0;
+  const bool skip1 = (p.debug & 1) != 0, skip2 = (p.debug & 2) != 0;  // timing experiments
 #else
   constexpr bool clk_on = false;  // build with -DBFQ_PHASE_CLOCKS for per-phase cycle counts
+  constexpr bool skip1 = false, skip2 = false;
 #endif
   long long ck_s1 = 0, ck_b1 = 0, ck_w = 0, ck_s2 = 0, ck_b2 = 0, ck0 = clock64(), ckt = ck0;
   auto tick = [&](long long& acc) {
@@ -291,7 +293,7 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
         const int zn = ml + 1 < M1T ? zs[ml + 1 < M1T ? ml + 1 : ml] : zs_n[0];
         const int en = ml + 1 < M1T ? ze[ml + 1 < M1T ? ml + 1 : ml] : (i + 1 < nch ? ze_n[0] : 0);
         if constexpr (DUAL) {
-          for (int z0 = zs[ml]; z0 < ze[ml]; z0 += 8) {
+          for (int z0 = zs[ml]; z0 < (skip1 ? zs[ml] : ze[ml]); z0 += 8) {
             const Row rwa = nxt_row;
             const Row rwb = fetch_row_bf(p.rows, z0 + 4 + kq, ze[ml]);  // g = 0 past the slice end
             const bool same = z0 + 8 < ze[ml];
@@ -309,7 +311,7 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
                 acc[cc][a][b][1] += acc2[cc][a][b][1];
               }
         } else {
-          for (int z0 = zs[ml]; z0 < ze[ml]; z0 += 4) {
+          for (int z0 = zs[ml]; z0 < (skip1 ? zs[ml] : ze[ml]); z0 += 4) {
             const Row rw = nxt_row;
             const bool same = z0 + 4 < ze[ml];
             nxt_row = fetch_row_bf(p.rows, (same ? z0 + 4 : zn) + kq, same ? ze[ml] : en);
@@ -374,7 +376,7 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
       constexpr bool DGC = decltype(dgtag)::value;
       // this warp's half of the k-steps (K = n_k^2, or the packed triangle)
       const int nks = (DGC ? K2PD : K2P) / 4;
-      const int ks0 = h ? (nks + 1) / 2 : 0, ks1 = h ? nks : (nks + 1) / 2;
+      const int ks0 = h ? (nks + 1) / 2 : 0, ks1 = skip2 ? ks0 : (h ? nks : (nks + 1) / 2);
       uint32_t rr[MT];
 #pragma unroll
       for (int j = 0; j < MT; ++j) rr[j] = DGC ? rrowd[j] : rrow[j];
