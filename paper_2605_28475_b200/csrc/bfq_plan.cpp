@@ -66,7 +66,7 @@ static bool choose_config(int nk, int qs, int k2s, int nf, int smem_limit, int m
   // with one stage each (measured as fast as two stages: the refill has a
   // whole stage 1 to land), else 2 teams.
   static const int popts[][4] = {  // cells, units, stages, teams
-      {8, 8, 1, 4}, {8, 8, 2, 2}, {4, 8, 1, 4}, {4, 8, 2, 2}, {4, 8, 1, 2},
+      {8, 8, 1, 4}, {8, 8, 2, 2}, {4, 8, 1, 4}, {4, 8, 1, 3}, {4, 8, 2, 2}, {4, 8, 1, 2},
       {2, 8, 1, 4}, {2, 8, 2, 2}, {2, 8, 1, 2}, {2, 4, 1, 2}, {2, 4, 1, 1}};
   int force_stages = 0, force_teams = 0;
   if (const char* e = std::getenv("BFQ_STAGES")) force_stages = std::atoi(e);
@@ -241,6 +241,12 @@ static void build_items(const HostPlan& hp, Program& pg) {
   }
   pg.unit_m1.swap(new_m1);
   pg.exec_macs_per_cell = total / c.cells;
+  if (std::getenv("BFQ_PLAN_STATS")) {  // packing efficiency: unit work / (slots x slowest unit)
+    double cap = 0.0;
+    for (const Cta& cta : ctas) cap += cta.work * c.upc;
+    std::fprintf(stderr, "plan: %zu CTAs per tile, %zu units, packing efficiency %.3f\n", ctas.size(),
+                 units_all.size(), total / cap);
+  }
 }
 
 // Shared-memory wavefronts of one stage-1 gather instruction for a group of

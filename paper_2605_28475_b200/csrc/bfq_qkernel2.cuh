@@ -218,6 +218,10 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
   if (nch > 1) slice_bounds(1, zs_nn, ze_nn);
   prefetch_rows_l1(zs_n, ze_n);
   Row nxt_row = fetch_row_bf(p.rows, zs_n[0] + kq, ze_n[0]);
+  // DUAL: the second row group of the next iteration, also one iteration ahead
+  // (rows of a 600k-row table miss L1; ncu showed long-scoreboard stalls on it)
+  constexpr bool DUALK = NKT == 17;
+  Row nxt_b = DUALK ? fetch_row_bf(p.rows, zs_n[0] + 4 + kq, ze_n[0]) : nxt_row;
 
   for (int i = 0; i < nch; ++i) {
     int zs[M1T], ze[M1T];
@@ -295,9 +299,10 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
         if constexpr (DUAL) {
           for (int z0 = zs[ml]; z0 < (skip1 ? zs[ml] : ze[ml]); z0 += 8) {
             const Row rwa = nxt_row;
-            const Row rwb = fetch_row_bf(p.rows, z0 + 4 + kq, ze[ml]);  // g = 0 past the slice end
+            const Row rwb = nxt_b;  // g = 0 past the slice end
             const bool same = z0 + 8 < ze[ml];
             nxt_row = fetch_row_bf(p.rows, (same ? z0 + 8 : zn) + kq, same ? ze[ml] : en);
+            nxt_b = fetch_row_bf(p.rows, (same ? z0 + 12 : zn + 4) + kq, same ? ze[ml] : en);
             group(rwa, acc);
             group(rwb, acc2);
           }
@@ -321,6 +326,10 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
         if (zs[ml] >= ze[ml]) {
           if (ml + 1 < M1T) nxt_row = fetch_row_bf(p.rows, zs[ml + 1 < M1T ? ml + 1 : ml] + kq, ze[ml + 1 < M1T ? ml + 1 : ml]);
           else nxt_row = fetch_row_bf(p.rows, zs_n[0] + kq, i + 1 < nch ? ze_n[0] : 0);
+          if constexpr (DUALK) {
+            if (ml + 1 < M1T) nxt_b = fetch_row_bf(p.rows, zs[ml + 1 < M1T ? ml + 1 : ml] + 4 + kq, ze[ml + 1 < M1T ? ml + 1 : ml]);
+            else nxt_b = fetch_row_bf(p.rows, zs_n[0] + 4 + kq, i + 1 < nch ? ze_n[0] : 0);
+          }
         }
         store_phi(ml, acc, DGC);
         if constexpr (X1) {
