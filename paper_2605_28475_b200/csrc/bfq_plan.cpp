@@ -67,14 +67,42 @@ static bool choose_config(int nk, int qs, int k2s, int nf, int smem_limit, int m
   // whole stage 1 to land), else 2 teams.
   static const int popts[][4] = {  // cells, units, stages, teams
       {8, 8, 1, 4}, {8, 8, 2, 2}, {4, 8, 1, 4}, {4, 8, 1, 3}, {4, 8, 2, 2}, {4, 8, 1, 2},
-      {2, 8, 1, 4}, {2, 8, 2, 2}, {2, 8, 1, 2}, {2, 4, 1, 2}, {2, 4, 1, 1}};
-  int force_stages = 0, force_teams = 0;
+      {2, 8, 1, 4}, {2, 8, 2, 2}, {2, 8, 1, 2}, {8, 4, 1, 4}, {8, 4, 1, 2}, {4, 4, 1, 4}, {4, 4, 1, 2},
+      {2, 4, 1, 4}, {2, 4, 1, 2}, {2, 4, 1, 1}};
+  int force_stages = 0, force_teams = 0, force_units = 0;
   if (const char* e = std::getenv("BFQ_STAGES")) force_stages = std::atoi(e);
   if (const char* e = std::getenv("BFQ_TEAMS")) force_teams = std::atoi(e);
+  if (const char* e = std::getenv("BFQ_UNITS")) force_units = std::atoi(e);
+  // Two CTAs per SM (4 units x 2 warps each, <= 128 registers) when their
+  // shared memory fits twice per SM: a CTA's prologue and tail then overlap
+  // the other CTA's work (measured +2.6% at N=L=8 and N=L=10).
+  static const int popts2[][4] = {{8, 4, 1, 4}, {8, 4, 1, 3}, {8, 4, 1, 2}, {4, 4, 1, 4}, {4, 4, 1, 3}, {4, 4, 1, 2}};
+  const long half_sm = (233472L - 2 * 1024) / 2;  // 228 KB per SM, 1 KB reserved per CTA
+  if (kernel == 2 && !force_stages && (!force_units || force_units == 4) && nk != 17 &&
+      !std::getenv("BFQ_ONE_CTA")) {
+    for (auto o0 : popts2) {
+      int o[4] = {o0[0], o0[1], o0[2], force_teams ? force_teams : o0[3]};
+      if (force_cells && o[0] != force_cells) continue;
+      if (o[0] > max_cells || o[3] > MAX_TEAMS) continue;
+      const long smem = smem_bytes(nk, qs, k2s, nf, o[0], o[1], o[2], c.hdr, o[3]);
+      if (smem > std::min<long>(half_sm, smem_limit)) continue;
+      c.cells = o[0];
+      c.m1t = 8 / o[0];
+      c.upc = o[1];
+      c.nw = 2 * o[1];
+      c.nstage = o[2];
+      c.nteams = o[3];
+      c.smem = (int)smem;
+      c.cg = c.cells;
+      c.pairsplit = 1;
+      return true;
+    }
+  }
   if (kernel == 2) {
     for (auto o0 : popts) {
       int o[4] = {o0[0], o0[1], force_stages ? force_stages : o0[2], force_teams ? force_teams : o0[3]};
       if (force_cells && o[0] != force_cells) continue;
+      if (force_units && o[1] != force_units) continue;
       if (o[0] > max_cells || o[0] < 2) continue;
       if (o[2] * o[3] > 2 * MAX_TEAMS || o[3] > MAX_TEAMS || o[2] > 2) continue;
       const long smem = smem_bytes(nk, qs, k2s, nf, o[0], o[1], o[2], c.hdr, o[3]);
