@@ -272,8 +272,35 @@ static void build_items(const HostPlan& hp, Program& pg) {
   if (std::getenv("BFQ_PLAN_STATS")) {  // packing efficiency: unit work / (slots x slowest unit)
     double cap = 0.0;
     for (const Cta& cta : ctas) cap += cta.work * c.upc;
-    std::fprintf(stderr, "plan: %zu CTAs per tile, %zu units, packing efficiency %.3f\n", ctas.size(),
-                 units_all.size(), total / cap);
+    // lockstep model: a team (one R ring) advances channel by channel at the
+    // pace of its slowest unit in that channel
+    double cap2 = 0.0;
+    for (const Cta& cta : ctas) {
+      double worst = 0.0;
+      for (size_t t = 0; t < cta.team_l1.size(); ++t) {
+        const Group& gr = pg.groups[cta.team_l1[t]];
+        double tt = 0.0;
+        for (int e = 0; e < gr.n_chan; ++e) {
+          const ChanEntry& ce = pg.chans[gr.chan_off + e];
+          double mx = 0.0;
+          for (int old : cta.team_units[t]) {
+            double w = stage2;
+            for (int ml = 0; ml < c.m1t; ++ml) {
+              const int m1 = new_m1[(size_t)(gr.unit_off + old) * c.m1t + ml];  // old ids (swapped out)
+              if (m1 < 0) continue;
+              w += (double)c.cells * c.mt * c.mt * 256.0 *
+                   ((hp.sstart[ce.slice_base + m1 + 1] - hp.sstart[ce.slice_base + m1] + 3) / 4);
+            }
+            mx = std::max(mx, w);
+          }
+          tt += mx;
+        }
+        worst = std::max(worst, tt);
+      }
+      cap2 += worst * c.upc;
+    }
+    std::fprintf(stderr, "plan: %zu CTAs per tile, %zu units, packing efficiency %.3f, with team lockstep %.3f\n",
+                 ctas.size(), units_all.size(), total / cap, total / cap2);
   }
 }
 
