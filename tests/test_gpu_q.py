@@ -299,3 +299,33 @@ def test_n16_path_synthetic_operator():
         assert q_oracle.rel_err(q[i], q_oracle.q_angular_first(oop, cells[i])) <= TOL, i
     q12 = run(op, cells[:3], cells[3:6])  # bilinear path at n_k = 17
     assert q_oracle.rel_err(q12[1], q_oracle.q_angular_first(oop, cells[1], cells[4])) <= TOL
+
+
+def test_n16_config4_on_gpu_built_operator():
+    """Config 4 (hard spheres N=L=16, n_k = 17: two DMMA tiles + the DFMA X1
+    row/column per axis, DUAL row groups) with the real Gaunt table and an R
+    tensor assembled on this GPU (bfr_assemble) -- the reference's own N=16
+    cache is a multi-hour CPU build that is not always shipped.
+      * kernel parity: GPU Q vs the oracle on the SAME operator, 1e-12;
+      * end-to-end parity vs the reference's evaluate() goldens (tests/golden/
+        hs_n16.npz, reference operator): bounded by the GPU-built R's distance
+        to the reference R (<= 4e-10 relative, test_gpu_rbuild.py BARS), which
+        the high-k rows amplify to 2.1e-9 in Q (measured), so the bar here is
+        5e-9 -- the 1e-12 bar against the reference's own N=16 operator is
+        test_golden_parity[hs_n16], run whenever operators/hs_n16.bfct is shipped;
+      * invariant slots bitwise zero; bilinear path against its golden."""
+    from paper_2605_28475_b200 import rbuild
+    from paper_2605_28475_b200.operator import SpectralConfig
+
+    d = golden("hs_n16")
+    op = rbuild.build_operator(SpectralConfig(16, 16, 1.0))
+    cells = d["cells"]
+    q = run(op, cells)
+    assert_invariants_zero(q)
+    oop = q_oracle.OracleOperator.from_operator(op)
+    assert q_oracle.rel_err(q[0], q_oracle.q_angular_first(oop, cells[0])) <= TOL
+    for i in range(cells.shape[0]):
+        assert q_oracle.rel_err(q[i], d["q"][i]) <= 5e-9, i
+    q12 = run(op, d["c1"][None], d["c2"][None])[0]
+    assert q_oracle.rel_err(q12, q_oracle.q_angular_first(oop, d["c1"], d["c2"])) <= TOL
+    assert q_oracle.rel_err(q12, d["q12"]) <= 5e-9
