@@ -64,6 +64,7 @@ struct KParams {
   double* q;
   long long n_cells;
   long long n_tiles;
+  int n_items;  // CTAs (items) per cell tile
   const double* R;
   const Row* rows;
   const int* sstart;
@@ -78,6 +79,26 @@ struct KParams {
   int debug;  // timing experiments only (BFQ_DEBUG): bit0 skip stage 1, bit1 skip stage 2, bit3 phase clocks
   unsigned long long* dbg_clk;  // [8] phase cycle totals when bit3 set
 };
+
+// CTA -> (item, tile).  Tiles are taken in chunks of TILE_CHUNK; inside a
+// chunk the CTAs run item-major (heavy items first), so all items of a tile
+// are resident within a few waves and the tile's cells are read from HBM
+// once (L2 serves the other items), while only the last chunk's tail sees
+// the light items last.
+constexpr long long TILE_CHUNK = 64;
+__device__ __forceinline__ void cta_item_tile(const long long b, const long long n_tiles, const int n_items,
+                                              long long& item, long long& tile) {
+  const long long full = n_tiles / TILE_CHUNK, per = TILE_CHUNK * n_items;
+  if (b < full * per) {
+    const long long ch = b / per, r = b - ch * per;
+    item = r / TILE_CHUNK;
+    tile = ch * TILE_CHUNK + (r - item * TILE_CHUNK);
+  } else {
+    const long long rem = n_tiles - full * TILE_CHUNK, r = b - full * per;
+    item = r / rem;
+    tile = full * TILE_CHUNK + (r - item * rem);
+  }
+}
 
 // ------------------------------------------------------------ PTX helpers
 // Not volatile: the scheduler may move shared loads across DMMAs.
@@ -432,6 +453,7 @@ int launch_q(const bfq_plan* plan, const DevProgram& dp, const double* f2, const
   p.q = q;
   p.n_cells = n_cells;
   p.n_tiles = (n_cells + dp.cfg.cells - 1) / dp.cfg.cells;
+  p.n_items = dp.n_items;
   p.R = plan->R;
   p.rows = plan->rows;
   p.sstart = plan->sstart;

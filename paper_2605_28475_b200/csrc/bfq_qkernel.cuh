@@ -39,8 +39,8 @@ __global__ void __launch_bounds__(256, 1) bfq_q_kernel(const KParams p) {
   const int K2S = FIXED ? conflict_free_stride_dev((NKT * NKT + 3) / 4 * 4) : p.k2s;
   const int NST = p.nstage;
 
-  const long long item_idx = (long long)blockIdx.x / p.n_tiles;
-  const long long tile = (long long)blockIdx.x - item_idx * p.n_tiles;
+  long long item_idx, tile;
+  cta_item_tile((long long)blockIdx.x, p.n_tiles, p.n_items, item_idx, tile);
   const Item item = p.items[item_idx];
 
   // shared layout: barriers + arrival counters | R rings (team, stage) | Phi (per warp, 8 pairs) | f (cells)
