@@ -64,7 +64,8 @@ struct KParams {
   double* q;
   long long n_cells;
   long long n_tiles;
-  int n_items;  // CTAs (items) per cell tile
+  int n_items;     // CTAs (items) per cell tile
+  int tile_chunk;  // tiles per item-major chunk of the grid
   const double* R;
   const Row* rows;
   const int* sstart;
@@ -85,18 +86,18 @@ struct KParams {
 // are resident within a few waves and the tile's cells are read from HBM
 // once (L2 serves the other items), while only the last chunk's tail sees
 // the light items last.
-constexpr long long TILE_CHUNK = 64;
+constexpr int TILE_CHUNK = 64;  // minimum; BFQ_TILE_CHUNK overrides (experiments)
 __device__ __forceinline__ void cta_item_tile(const long long b, const long long n_tiles, const int n_items,
-                                              long long& item, long long& tile) {
-  const long long full = n_tiles / TILE_CHUNK, per = TILE_CHUNK * n_items;
+                                              const int chunk, long long& item, long long& tile) {
+  const long long full = n_tiles / chunk, per = (long long)chunk * n_items;
   if (b < full * per) {
     const long long ch = b / per, r = b - ch * per;
-    item = r / TILE_CHUNK;
-    tile = ch * TILE_CHUNK + (r - item * TILE_CHUNK);
+    item = r / chunk;
+    tile = ch * chunk + (r - item * chunk);
   } else {
-    const long long rem = n_tiles - full * TILE_CHUNK, r = b - full * per;
+    const long long rem = n_tiles - full * chunk, r = b - full * per;
     item = r / rem;
-    tile = full * TILE_CHUNK + (r - item * rem);
+    tile = full * chunk + (r - item * rem);
   }
 }
 
@@ -454,6 +455,13 @@ int launch_q(const bfq_plan* plan, const DevProgram& dp, const double* f2, const
   p.n_cells = n_cells;
   p.n_tiles = (n_cells + dp.cfg.cells - 1) / dp.cfg.cells;
   p.n_items = dp.n_items;
+  {
+    // as many tiles per item-major chunk as keep their cells (f2 and f3)
+    // within ~32 MB of L2: small batches stay fully heavy-first
+    static const int forced = std::getenv("BFQ_TILE_CHUNK") ? std::max(1, std::atoi(std::getenv("BFQ_TILE_CHUNK"))) : 0;
+    const long long tile_bytes = (long long)dp.cfg.cells * hp.n_k * hp.n_q * 8 * (dp.bilinear ? 2 : 1);
+    p.tile_chunk = forced ? forced : (int)std::max<long long>(TILE_CHUNK, (32LL << 20) / std::max(tile_bytes, 1LL));
+  }
   p.R = plan->R;
   p.rows = plan->rows;
   p.sstart = plan->sstart;

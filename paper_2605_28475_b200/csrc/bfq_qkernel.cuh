@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(256, 1) bfq_q_kernel(const KParams p) {
   const int NST = p.nstage;
 
   long long item_idx, tile;
-  cta_item_tile((long long)blockIdx.x, p.n_tiles, p.n_items, item_idx, tile);
+  cta_item_tile((long long)blockIdx.x, p.n_tiles, p.n_items, p.tile_chunk, item_idx, tile);
   const Item item = p.items[item_idx];
 
   // shared layout: barriers + arrival counters | R rings (team, stage) | Phi (per warp, 8 pairs) | f (cells)

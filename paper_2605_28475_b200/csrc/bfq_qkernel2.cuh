@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
   const int NU = p.nw / 2;  // units (Phi buffers) per CTA
 
   long long item_idx, tile;
-  cta_item_tile((long long)blockIdx.x, p.n_tiles, p.n_items, item_idx, tile);
+  cta_item_tile((long long)blockIdx.x, p.n_tiles, p.n_items, p.tile_chunk, item_idx, tile);
   const Item item = p.items[item_idx];
 
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);  // [team*2 + stage]
