@@ -1,8 +1,11 @@
-OUT=gpurun_out
-python -m pytest tests -m gpu -x -q > $OUT/pytest.log 2>&1
-for spec in hs_n12:65536 mm_n10:32768 hs_n8:32768 hs_n16:16384; do
-  op=${spec%%:*}; n=${spec##*:}
-  echo "== $op $n" >> $OUT/q.txt
-  timeout 300 python tools/prof_q.py --op $op --cells $n --iters 3 2>&1 | grep -v "^iter 0" | tail -2 >> $OUT/q.txt
-  timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:bfq_q_kernel -s 1 -c 1 python tools/prof_q.py --op $op --cells $n --iters 2 2>&1 | grep -E "dram__|gpu__time" >> $OUT/q.txt
+OUT=gpurun_out/hostchunk2.txt; : > $OUT
+for ch in 256 512 1024; do
+  echo "== hs12 chunk $ch" >> $OUT
+  BFQ_HOST_CHUNK=$ch timeout 600 python bench.py --no-cpu --steps 3 --warmup 3 --e2e-steps 5 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['value']), round(d['e2e']['value']))" >> $OUT
+done
+for ch in 128 256 512; do
+  for c in hs8 mm10; do
+  echo "== $c chunk $ch" >> $OUT
+  BFQ_HOST_CHUNK=$ch timeout 600 python bench.py --config $c --no-cpu --steps 3 --warmup 3 --e2e-steps 5 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['value']), round(d['e2e']['value']))" >> $OUT
+  done
 done
