@@ -416,8 +416,8 @@ def run_ours(args, rank, world, local_rank):
     import numpy as np
     import torch
 
+    from paper_2605_28475_b200 import dist as bdist
     from paper_2605_28475_b200 import engine
-    from paper_2605_28475_b200.operator import load_cache
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -483,13 +483,10 @@ def run_ours(args, rank, world, local_rank):
         wall = time.perf_counter() - t0
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     total_ms = sum(step_ms) if flush is not None else starts[0].elapsed_time(ends[-1])
-    t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
-    if dist is not None:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t.item())
-    ms_per_step = total_ms / args.steps
     q_per_step = 4 if rk4 else 1
-    value = n_cells * world * args.steps * q_per_step / (total_ms / 1e3)
+    # whole-job rate: cells of all ranks / the slowest rank's device time
+    value, total_ms = bdist.weak_scaling_rate(n_cells, args.steps * q_per_step, total_ms, device=dev)
+    ms_per_step = total_ms / args.steps
 
     # conservation diagnostics of the last step, all-reduced (max |production|,
     # or for RK4 the max drift of the invariants from the initial state)

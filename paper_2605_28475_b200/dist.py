@@ -14,7 +14,8 @@ import os
 
 import numpy as np
 
-__all__ = ["shard_range", "diagnostics_vector", "allreduce_diagnostics", "init_from_env"]
+__all__ = ["shard_range", "diagnostics_vector", "allreduce_diagnostics", "init_from_env", "max_over_ranks",
+           "weak_scaling_rate"]
 
 DIAG_FIELDS = ("max_mass", "max_px", "max_py", "max_pz", "max_energy", "cells", "checksum")
 
@@ -60,6 +61,30 @@ def allreduce_diagnostics(vec, group=None):
     dist.all_reduce(mx, op=dist.ReduceOp.MAX, group=group)
     dist.all_reduce(sm, op=dist.ReduceOp.SUM, group=group)
     return torch.cat([mx, sm])
+
+
+def max_over_ranks(value: float, device=None) -> float:
+    """MAX of a per-rank scalar (a device-timed step time) over all ranks; the
+    bench's step time is the slowest rank's (the job ends with it)."""
+    import torch
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()):
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def weak_scaling_rate(cells_per_rank: int, evals_per_cell: int, local_ms: float, device=None) -> tuple[float, float]:
+    """Whole-job cell-evaluations/s of a weak-scaling run: every rank evaluates
+    ``cells_per_rank`` cells ``evals_per_cell`` times in ``local_ms`` of its own
+    device time; the job's time is the max over ranks.  Returns (rate, max_ms)."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size() if dist.is_available() and dist.is_initialized() else 1
+    ms = max_over_ranks(local_ms, device)
+    return cells_per_rank * world * evals_per_cell / (ms / 1e3), ms
 
 
 def init_from_env(backend: str = "nccl"):

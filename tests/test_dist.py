@@ -56,3 +56,24 @@ def test_diagnostics_allreduce_gloo_world2():
         assert abs(r[6] - ref[6]) <= 1e-12 * np.abs(q_all).sum()
     d = bdist.as_dict(res[0])
     assert d["cells"] == 13.0
+
+
+def _timing_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    local_ms = [100.0, 125.0][rank]  # rank 1 is the slow one
+    out[rank] = bdist.weak_scaling_rate(65536, 10, local_ms)
+    dist.destroy_process_group()
+
+
+def test_weak_scaling_rate_is_max_over_ranks_gloo_world2():
+    """bench.py's aggregation: every rank reports the job rate over the slowest
+    rank's time, cells counted over all ranks."""
+    with mp.Manager() as mgr:
+        out = mgr.dict()
+        mp.spawn(_timing_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+        res = [out[0], out[1]]
+    for rate, ms in res:
+        assert ms == 125.0
+        assert rate == 65536 * 2 * 10 / 0.125
+    assert bdist.weak_scaling_rate(100, 1, 50.0) == (2000.0, 50.0)  # no process group: one rank
