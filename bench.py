@@ -88,13 +88,13 @@ def _cpu_worker(args):
     except ImportError:  # pragma: no cover
         threadpool_limits = None
     op = q_oracle.OracleOperator.from_operator(load_cache(path))
-    rs = op.r[:, :, :, op.slice_tau]
+    ws = q_oracle.angular_workspace(op)  # cached per operator, as the reference does
     ctx = threadpool_limits(limits=1) if threadpool_limits else None
     if ctx:
         ctx.__enter__()
     t0 = time.perf_counter()
     for c in cells:
-        q_oracle.q_angular_first(op, c, r_slices=rs)
+        q_oracle.q_angular_first(op, c, workspace=ws)
     dt = time.perf_counter() - t0
     if ctx:
         ctx.__exit__(None, None, None)

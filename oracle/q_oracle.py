@@ -73,21 +73,43 @@ def _sort_guard(op: OracleOperator) -> None:
         raise ValueError("COO rows must be sorted and grouped by (tau, q1)")
 
 
+def angular_workspace(op: OracleOperator):
+    """The static pieces the reference caches per operator (contraction.py:110-130):
+    the row -> slice segment-sum operator as a CSR 0/1 matrix (N_G x N_S) and
+    the per-slice gather of R, contiguous as (n_k, n_k^2, N_S)."""
+    import scipy.sparse as sp
+
+    n_g = op.g.size
+    n_s = op.slice_starts.size - 1
+    ids = np.repeat(np.arange(n_s), np.diff(op.slice_starts))
+    seg = sp.csr_matrix((np.ones(n_g), ids, np.arange(n_g + 1)), shape=(n_g, n_s))
+    r_slices = np.ascontiguousarray(op.r[:, :, :, op.slice_tau].reshape(op.n_k, op.n_k * op.n_k, n_s))
+    return seg, r_slices
+
+
 def q_angular_first(op: OracleOperator, f2: np.ndarray, f3: np.ndarray | None = None,
-                    r_slices: np.ndarray | None = None) -> np.ndarray:
-    """Q(f2, f3) of one cell, (n_k, n_q) -> (n_k, n_q)."""
+                    r_slices: np.ndarray | None = None, workspace=None) -> np.ndarray:
+    """Q(f2, f3) of one cell, (n_k, n_q) -> (n_k, n_q), contraction.py:293-317.
+
+    Same operations as the reference (gather, CSR segment-sum matmul, einsum
+    against the contiguous per-slice R, bincount scatter), so it is also the
+    reference's CPU speed on the GPU box (tools/cpu_ref_vs_port.py).  Pass
+    ``workspace=angular_workspace(op)`` to reuse the static pieces across
+    cells, as the reference does; ``r_slices`` (n_k, n_k, n_k, N_S) is the
+    older form of the R half of it."""
     _sort_guard(op)
     f3 = f2 if f3 is None else f3
     n_k, n_q = op.n_k, op.n_q
+    if workspace is None:
+        workspace = angular_workspace(op) if r_slices is None else (
+            angular_workspace(op)[0], np.ascontiguousarray(r_slices.reshape(n_k, n_k * n_k, -1)))
+    seg, rs = workspace
     # operand columns of every row, the g weight folded into the slot-2 side
-    left = f2[:, op.q2] * op.g  # (n_k, N_G)
-    right = f3[:, op.q3]  # (n_k, N_G)
-    outer = left[:, None, :] * right[None, :, :]  # (n_k, n_k, N_G)
-    phi = np.add.reduceat(outer, op.slice_starts[:-1], axis=2)  # (n_k, n_k, N_S)
-    if r_slices is None:
-        r_slices = op.r[:, :, :, op.slice_tau]  # (n_k, n_k, n_k, N_S)
-    out = np.einsum("kabs,abs->ks", r_slices, phi, optimize=True)
-    q = np.zeros((n_k, n_q))
+    left = op.g * f2[:, op.q2]  # (n_k, N_G)
+    outer = left[:, None, :] * f3[None, :, op.q3]  # (n_k, n_k, N_G)
+    phi = np.asarray(outer.reshape(n_k * n_k, -1) @ seg)  # (n_k^2, N_S) segment sums
+    out = np.einsum("kaS,aS->kS", rs, phi, optimize=True)
+    q = np.empty((n_k, n_q))
     for k1 in range(n_k):
         q[k1] = np.bincount(op.slice_q1, weights=out[k1], minlength=n_q)
     return q
@@ -110,10 +132,10 @@ def q_naive(op: OracleOperator, f2: np.ndarray, f3: np.ndarray | None = None) ->
 
 def q_batch(op: OracleOperator, cells: np.ndarray, cells3: np.ndarray | None = None) -> np.ndarray:
     """Angular-first over a batch (B, n_k, n_q), one cell at a time."""
-    rs = op.r[:, :, :, op.slice_tau]
+    ws = angular_workspace(op)
     out = np.empty_like(cells)
     for i in range(cells.shape[0]):
-        out[i] = q_angular_first(op, cells[i], None if cells3 is None else cells3[i], r_slices=rs)
+        out[i] = q_angular_first(op, cells[i], None if cells3 is None else cells3[i], workspace=ws)
     return out
 
 

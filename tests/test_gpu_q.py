@@ -256,9 +256,9 @@ def test_hs12_headline_operator():
     q = run(op, cells)
     assert_invariants_zero(q)
     oop = q_oracle.OracleOperator.from_operator(op)
-    rs = oop.r[:, :, :, oop.slice_tau]
+    ws = q_oracle.angular_workspace(oop)
     for i in (0, 1, 511, 1024, 2047):
-        ref = q_oracle.q_angular_first(oop, cells[i], r_slices=rs)
+        ref = q_oracle.q_angular_first(oop, cells[i], workspace=ws)
         assert q_oracle.rel_err(q[i], ref) <= TOL, i
 
 

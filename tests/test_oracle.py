@@ -44,3 +44,24 @@ def test_sort_guard():
                                   op.g[perm], op.slice_starts, op.slice_tau, op.slice_q1, op.r)
     with pytest.raises(ValueError):
         q_oracle.q_angular_first(bad, np.zeros((op.n_k, op.n_q)))
+
+
+@pytest.mark.parametrize("name", ["hs_n4", "mm_k4l6", "hs_n8"])
+def test_oracle_bitwise_equals_live_reference(reference, name):
+    """The restatement performs the reference's own operations in the same
+    order (gather, CSR segment-sum matmul, einsum, bincount), so on the same
+    numpy/scipy it is bit-identical to contraction.q_angular_first -- which is
+    why bench.py may time it as the reference's CPU path on the GPU box
+    (profiles/r01_cpu_ref_vs_port.txt: same speed per cell)."""
+    import os
+
+    from boltzfact import basis
+
+    from conftest import OPERATORS
+
+    ref_op = reference.cache.load_cache(os.path.join(OPERATORS, f"{name}.bfct"))
+    op = q_oracle.OracleOperator.from_operator(load_op(name))
+    ws = q_oracle.angular_workspace(op)
+    for c in golden(name)["cells"]:
+        ref = reference.contraction.q_angular_first(ref_op, basis.CoefficientField(c.copy(), ref_op.cfg)).values
+        assert np.array_equal(q_oracle.q_angular_first(op, c, workspace=ws), ref)
