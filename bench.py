@@ -581,7 +581,8 @@ def run_ours(args, rank, world, local_rank):
         cpu = cpu_port_rate(args.config, host[:256], budget_s=args.cpu_budget, path=oppath)
         line["cpu_baseline"] = {"value": cpu["value"], "unit": "cells/s", "cores": cpu["cores"], "kind": "port",
                                 "sample": f"{cpu['cells']} cells of the same batch, ~{args.cpu_budget:.0f} s per core "
-                                          "(numpy restatement of q_angular_first, 1 thread per process)"}
+                                          "(oracle/q_oracle.py: the reference's q_angular_first operations, bit-identical to it and "
+                                          "the same speed per cell, profiles/r01_cpu_ref_vs_port.txt; 1 thread per process)"}
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
