@@ -129,9 +129,10 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
 #ifdef BFQ_PHASE_CLOCKS
   const bool clk_on = (p.debug & 8) != 0;
   const bool skip1 = (p.debug & 1) != 0, skip2 = (p.debug & 2) != 0;  // timing experiments
+  const bool nowait = (p.debug & 4) != 0;  // do not wait for the R ring (stale R: timing only)
 #else
   constexpr bool clk_on = false;  // build with -DBFQ_PHASE_CLOCKS for per-phase cycle counts
-  constexpr bool skip1 = false, skip2 = false;
+  constexpr bool skip1 = false, skip2 = false, nowait = false;
 #endif
   long long ck_s1 = 0, ck_b1 = 0, ck_w = 0, ck_s2 = 0, ck_b2 = 0, ck0 = clock64(), ckt = ck0;
   auto tick = [&](long long& acc) {
@@ -377,7 +378,7 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
     // ring slot and phase of channel i (NST is 1 or 2: no integer division)
     const int s = NST == 1 ? 0 : (i & 1);
     const unsigned par = NST == 1 ? (unsigned)(i & 1) : (unsigned)((i >> 1) & 1);
-    mbar_wait(&tfull[s], par);
+    if (!nowait || i == 0) mbar_wait(&tfull[s], par);
     tick(ck_w);
     const uint32_t rb = ring_u32 + (uint32_t)(s * rblk) * 8u;
     const uint32_t pa = phu_u32 + (uint32_t)(r0 * K2S + kq) * 8u;

@@ -1,11 +1,5 @@
-OUT=gpurun_out/hostchunk2.txt; : > $OUT
-for ch in 256 512 1024; do
-  echo "== hs12 chunk $ch" >> $OUT
-  BFQ_HOST_CHUNK=$ch timeout 600 python bench.py --no-cpu --steps 3 --warmup 3 --e2e-steps 5 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['value']), round(d['e2e']['value']))" >> $OUT
-done
-for ch in 128 256 512; do
-  for c in hs8 mm10; do
-  echo "== $c chunk $ch" >> $OUT
-  BFQ_HOST_CHUNK=$ch timeout 600 python bench.py --config $c --no-cpu --steps 3 --warmup 3 --e2e-steps 5 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['value']), round(d['e2e']['value']))" >> $OUT
-  done
+OUT=gpurun_out/sweep5.txt; : > $OUT
+for env in "" "BFQ_KERNEL=1" "BFQ_ONE_CTA=1 BFQ_TEAMS=2" "BFQ_TEAMS=2" "BFQ_TEAMS=3" "BFQ_NO_X1_CELLS8=1"; do
+  echo "== hs_n8 [$env]" >> $OUT
+  env $env timeout 120 python tools/prof_q.py --op hs_n8 --cells 4096 --iters 5 2>&1 | grep -E "^\{|^iter 4" >> $OUT
 done
