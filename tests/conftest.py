@@ -38,7 +38,8 @@ def golden(name: str):
 
 def golden_names():
     return sorted(f[:-4] for f in os.listdir(GOLDEN)
-                  if f.endswith(".npz") and f not in ("project.npz", "maxwell_rates.npz", "rtensor_quadconv.npz"))
+                  if f.endswith(".npz") and not f.startswith("rk4_")
+                  and f not in ("project.npz", "maxwell_rates.npz", "rtensor_quadconv.npz"))
 
 
 def reference_available() -> bool:

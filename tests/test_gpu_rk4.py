@@ -73,3 +73,31 @@ def test_rk4_config5_operator():
     tr = harness.rk4_integrate_batch(op, c0, 0.01, 3, record_every=3, watch=[17])
     assert tr.moment_drift() == 0.0
     assert q_oracle.rel_err(tr.snapshots[-1, 0], oracle_rk4(op, c0[17], 0.01, 3)) <= 1e-12
+
+
+def test_rk4_config5_full_trajectory_matches_reference():
+    """Config 5 as BASELINE.json states it: Maxwell molecules N=L=10, bimodal
+    cells, RK4 dt = 0.01 for 1,000 steps.  Two cells of a 16-cell batch are
+    compared at every 100th step with the reference's own rk4_integrate
+    trajectory (tests/golden/make_rk4_golden.py, harness.py:79-120); the
+    invariants of every cell stay bitwise constant."""
+    import os
+
+    from conftest import GOLDEN
+
+    path = os.path.join(GOLDEN, "rk4_mm_n10.npz")
+    if not os.path.exists(path):
+        pytest.skip("reference RK4 trajectory not generated")
+    d = np.load(path)
+    op = load_op("mm_n10")
+    cfg = op.cfg
+    c0 = inputs.bimodal(cfg.n_k, cfg.l_max, int(d["n_cells"]), seed=int(d["seed"]))
+    watch = [int(i) for i in d["cells"]]
+    tr = harness.rk4_integrate_batch(op, c0, float(d["dt"]), int(d["n_steps"]), record_every=100, watch=watch)
+    assert tr.moment_drift() == 0.0
+    assert np.allclose(tr.times, d["times"])
+    ref = d["snapshots"]  # (records, cells, n_k, n_q)
+    assert tr.snapshots.shape == ref.shape
+    for r in range(ref.shape[0]):
+        for j in range(len(watch)):
+            assert q_oracle.rel_err(tr.snapshots[r, j], ref[r, j]) <= 1e-12, (r, j)
