@@ -130,9 +130,10 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
   const bool clk_on = (p.debug & 8) != 0;
   const bool skip1 = (p.debug & 1) != 0, skip2 = (p.debug & 2) != 0;  // timing experiments
   const bool nowait = (p.debug & 4) != 0;  // do not wait for the R ring (stale R: timing only)
+  const bool rowhit = (p.debug & 16) != 0;  // fetch table rows 0..15 only (always L1 hits: timing only)
 #else
   constexpr bool clk_on = false;  // build with -DBFQ_PHASE_CLOCKS for per-phase cycle counts
-  constexpr bool skip1 = false, skip2 = false, nowait = false;
+  constexpr bool skip1 = false, skip2 = false, nowait = false, rowhit = false;
 #endif
   long long ck_s1 = 0, ck_b1 = 0, ck_w = 0, ck_s2 = 0, ck_b2 = 0, ck0 = clock64(), ckt = ck0;
   auto tick = [&](long long& acc) {
@@ -218,11 +219,12 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
   slice_bounds(0, zs_n, ze_n);
   if (nch > 1) slice_bounds(1, zs_nn, ze_nn);
   prefetch_rows_l1(zs_n, ze_n);
-  Row nxt_row = fetch_row_bf(p.rows, zs_n[0] + kq, ze_n[0]);
+  auto fetch_rb = [&](int z, int ze) { return fetch_row_bf(p.rows, rowhit ? (z & 15) : z, ze); };
+  Row nxt_row = fetch_rb(zs_n[0] + kq, ze_n[0]);
   // DUAL: the second row group of the next iteration, also one iteration ahead
   // (rows of a 600k-row table miss L1; ncu showed long-scoreboard stalls on it)
   constexpr bool DUALK = NKT == 17;
-  Row nxt_b = DUALK ? fetch_row_bf(p.rows, zs_n[0] + 4 + kq, ze_n[0]) : nxt_row;
+  Row nxt_b = DUALK ? fetch_rb(zs_n[0] + 4 + kq, ze_n[0]) : nxt_row;
 
   for (int i = 0; i < nch; ++i) {
     int zs[M1T], ze[M1T];
@@ -302,8 +304,8 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
             const Row rwa = nxt_row;
             const Row rwb = nxt_b;  // g = 0 past the slice end
             const bool same = z0 + 8 < ze[ml];
-            nxt_row = fetch_row_bf(p.rows, (same ? z0 + 8 : zn) + kq, same ? ze[ml] : en);
-            nxt_b = fetch_row_bf(p.rows, (same ? z0 + 12 : zn + 4) + kq, same ? ze[ml] : en);
+            nxt_row = fetch_rb((same ? z0 + 8 : zn) + kq, same ? ze[ml] : en);
+            nxt_b = fetch_rb((same ? z0 + 12 : zn + 4) + kq, same ? ze[ml] : en);
             group(rwa, acc);
             group(rwb, acc2);
           }
@@ -320,16 +322,16 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
           for (int z0 = zs[ml]; z0 < (skip1 ? zs[ml] : ze[ml]); z0 += 4) {
             const Row rw = nxt_row;
             const bool same = z0 + 4 < ze[ml];
-            nxt_row = fetch_row_bf(p.rows, (same ? z0 + 4 : zn) + kq, same ? ze[ml] : en);
+            nxt_row = fetch_rb((same ? z0 + 4 : zn) + kq, same ? ze[ml] : en);
             group(rw, acc);
           }
         }
         if (zs[ml] >= ze[ml]) {
-          if (ml + 1 < M1T) nxt_row = fetch_row_bf(p.rows, zs[ml + 1 < M1T ? ml + 1 : ml] + kq, ze[ml + 1 < M1T ? ml + 1 : ml]);
-          else nxt_row = fetch_row_bf(p.rows, zs_n[0] + kq, i + 1 < nch ? ze_n[0] : 0);
+          if (ml + 1 < M1T) nxt_row = fetch_rb(zs[ml + 1 < M1T ? ml + 1 : ml] + kq, ze[ml + 1 < M1T ? ml + 1 : ml]);
+          else nxt_row = fetch_rb(zs_n[0] + kq, i + 1 < nch ? ze_n[0] : 0);
           if constexpr (DUALK) {
-            if (ml + 1 < M1T) nxt_b = fetch_row_bf(p.rows, zs[ml + 1 < M1T ? ml + 1 : ml] + 4 + kq, ze[ml + 1 < M1T ? ml + 1 : ml]);
-            else nxt_b = fetch_row_bf(p.rows, zs_n[0] + 4 + kq, i + 1 < nch ? ze_n[0] : 0);
+            if (ml + 1 < M1T) nxt_b = fetch_rb(zs[ml + 1 < M1T ? ml + 1 : ml] + 4 + kq, ze[ml + 1 < M1T ? ml + 1 : ml]);
+            else nxt_b = fetch_rb(zs_n[0] + 4 + kq, i + 1 < nch ? ze_n[0] : 0);
           }
         }
         store_phi(ml, acc, DGC);
