@@ -186,13 +186,6 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
       ze[ml] = ok ? __ldg(p.sstart + ce.slice_base + m1 + 1) : 0;
     }
   };
-  auto prefetch_rows_l1 = [&](const int* zs, const int* ze) {
-    if (h) return;  // one warp of the pair is enough
-#pragma unroll
-    for (int ml = 0; ml < M1T; ++ml)
-      for (int z = (zs[ml] & ~7) + lane * 8; z < ze[ml]; z += 256)
-        asm volatile("prefetch.global.L1 [%0];\n" ::"l"(p.rows + z));
-  };
   auto store_phi = [&](int ml, double (&acc)[HC][MT][MT][2], bool dg) {
 #pragma unroll
     for (int cc = 0; cc < HC; ++cc) {
@@ -218,7 +211,6 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
   int zs_n[M1T], ze_n[M1T], zs_nn[M1T], ze_nn[M1T];
   slice_bounds(0, zs_n, ze_n);
   if (nch > 1) slice_bounds(1, zs_nn, ze_nn);
-  prefetch_rows_l1(zs_n, ze_n);
   auto fetch_rb = [&](int z, int ze) { return fetch_row_bf(p.rows, rowhit ? (z & 15) : z, ze); };
   Row nxt_row = fetch_rb(zs_n[0] + kq, ze_n[0]);
   // DUAL: the second row group of the next iteration, also one iteration ahead
@@ -240,7 +232,6 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
         ze_n[ml] = ze_nn[ml];
       }
       if (i + 2 < nch) slice_bounds(i + 2, zs_nn, ze_nn);
-      prefetch_rows_l1(zs_n, ze_n);
     }
     const bool dg = (ctau[team * p.max_chan + i] & 1) != 0;
     auto stage1 = [&](auto dgtag) {

@@ -1,5 +1,7 @@
-OUT=gpurun_out/sweep5.txt; : > $OUT
-for env in "" "BFQ_KERNEL=1" "BFQ_ONE_CTA=1 BFQ_TEAMS=2" "BFQ_TEAMS=2" "BFQ_TEAMS=3" "BFQ_NO_X1_CELLS8=1"; do
-  echo "== hs_n8 [$env]" >> $OUT
-  env $env timeout 120 python tools/prof_q.py --op hs_n8 --cells 4096 --iters 5 2>&1 | grep -E "^\{|^iter 4" >> $OUT
+OUT=gpurun_out/q.txt; : > $OUT
+python -m pytest tests -m gpu -x -q > gpurun_out/pytest.log 2>&1
+for spec in hs_n12:65536 hs_n16:16384 mm_n10:32768 hs_n8:4096; do
+  op=${spec%%:*}; n=${spec##*:}
+  echo "== $op $n" >> $OUT
+  timeout 300 python tools/prof_q.py --op $op --cells $n --iters 4 2>&1 | grep "^iter 3" >> $OUT
 done
