@@ -11,10 +11,10 @@ for c in ${CONFIGS:-hs8 mm10 hs16 rk4 rbuild12}; do
   timeout 900 python bench.py --config $c > $OUT/bench_$c.json 2> $OUT/bench_$c.err
 done
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > $OUT/bench_ref.json 2> $OUT/bench_ref.err
-timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/launches_default.csv \
+timeout 1200 ncu --target-processes application-only --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/launches_default.csv \
    python bench.py > $OUT/ncu_launches.log 2>&1
 timeout 300 python tools/prof_q.py --op hs_n12 --cells 2048 > $OUT/prof_hs_n12.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:bfq_q_kernel -s 2 -c 1 \
+timeout 900 ncu --target-processes application-only --set full --clock-control none --import-source on -k regex:bfq_q_kernel -s 2 -c 1 \
    -o /tmp/ncurep/prof_hs_n12 python tools/prof_q.py --op hs_n12 --cells 2048 > $OUT/ncu_hs_n12.log 2>&1
 if [ -f /tmp/ncurep/prof_hs_n12.ncu-rep ]; then
   python tools/ncu_summary.py /tmp/ncurep/prof_hs_n12.ncu-rep > $OUT/ncu_sum_hs_n12.txt 2>&1
