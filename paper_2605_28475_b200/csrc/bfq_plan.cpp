@@ -443,6 +443,25 @@ int build_host_plan(const bfq_desc& d, int smem_limit, HostPlan& hp) {
     }
     hp.sstart.push_back((int32_t)d.n_g);
   }
+  // Pad every slice to a whole number of k-steps with g = 0 rows (q2 = q3 = 0),
+  // so the stage-1 row stream needs no clamp / zero-weight select: 4 rows, or
+  // 8 at n_k = 17 where the DUAL loop consumes two row groups per iteration.
+  {
+    const int padm = nk == 17 ? 8 : 4;
+    std::vector<Row> padded;
+    padded.reserve(hp.rows.size() + (size_t)padm * hp.sstart.size());
+    std::vector<int32_t> ns(hp.sstart.size());
+    for (size_t i = 0; i + 1 < hp.sstart.size(); ++i) {
+      ns[i] = (int32_t)padded.size();
+      const int32_t a = hp.sstart[i], b = hp.sstart[i + 1];
+      for (int32_t z = a; z < b; ++z) padded.push_back(hp.rows[z]);
+      while ((padded.size() - ns[i]) % padm) padded.push_back(Row{0, 0, 0.0});
+    }
+    ns.back() = (int32_t)padded.size();
+    while (padded.size() < (size_t)padm) padded.push_back(Row{0, 0, 0.0});  // rows 0..padm-1 always exist
+    hp.rows.swap(padded);
+    hp.sstart.swap(ns);
+  }
 
   // R blocks: rblocks[t][k1][a*nk+b] = R[k1,a,b,t]; zero padding to k2s
   const size_t blk = (size_t)nk * hp.k2s;

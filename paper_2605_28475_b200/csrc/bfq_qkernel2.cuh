@@ -211,7 +211,9 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
   int zs_n[M1T], ze_n[M1T], zs_nn[M1T], ze_nn[M1T];
   slice_bounds(0, zs_n, ze_n);
   if (nch > 1) slice_bounds(1, zs_nn, ze_nn);
-  auto fetch_rb = [&](int z, int ze) { return fetch_row_bf(p.rows, rowhit ? (z & 15) : z, ze); };
+  // slices are padded to whole k-steps with g = 0 rows (bfq_plan.cpp), and a
+  // fetch past the last slice reads a valid row that is never used: no clamp
+  auto fetch_rb = [&](int z, int ze) { (void)ze; return load_row(p.rows, rowhit ? (z & 15) : z); };
   Row nxt_row = fetch_rb(zs_n[0] + kq, ze_n[0]);
   // DUAL: the second row group of the next iteration, also one iteration ahead
   // (rows of a 600k-row table miss L1; ncu showed long-scoreboard stalls on it)
