@@ -131,9 +131,10 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
   const bool skip1 = (p.debug & 1) != 0, skip2 = (p.debug & 2) != 0;  // timing experiments
   const bool nowait = (p.debug & 4) != 0;  // do not wait for the R ring (stale R: timing only)
   const bool rowhit = (p.debug & 16) != 0;  // fetch table rows 0..15 only (always L1 hits: timing only)
+  const bool nostore = (p.debug & 64) != 0;  // skip the per-slice Phi stores (timing only)
 #else
   constexpr bool clk_on = false;  // build with -DBFQ_PHASE_CLOCKS for per-phase cycle counts
-  constexpr bool skip1 = false, skip2 = false, nowait = false, rowhit = false;
+  constexpr bool skip1 = false, skip2 = false, nowait = false, rowhit = false, nostore = false;
 #endif
   long long ck_s1 = 0, ck_b1 = 0, ck_w = 0, ck_s2 = 0, ck_b2 = 0, ck0 = clock64(), ckt = ck0;
   auto tick = [&](long long& acc) {
@@ -327,7 +328,7 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
             else nxt_b = fetch_rb(zs_n[0] + 4 + kq, i + 1 < nch ? ze_n[0] : 0);
           }
         }
-        store_phi(ml, acc, DGC);
+        if (!nostore) store_phi(ml, acc, DGC);
         if constexpr (X1) {
           // lanes kq = 0..3 hold partial sums over their own rows: reduce, then
           // the kq == 0 lanes store row / column n_k-1 of Phi
