@@ -105,12 +105,16 @@ int bfq_plan_work(const bfq_plan* plan, double* flops_per_cell, double* bytes_pe
 /* Q(f2, f3) for n_cells cells.  DEVICE pointers on the plan's device, layout
  * (n_cells, n_k, n_q) fp64 C-contiguous.  f3 == f2 (or f3 == NULL) selects
  * Q(f,f).  Stream-ordered on `stream` (a cudaStream_t, NULL = legacy default),
- * no host synchronisation, no allocation. */
+ * no host synchronisation, no allocation.  q must not overlap f2 or f3: CTAs
+ * of one cell tile still read its cells while others already write Q (BFQ_EINVAL). */
 int bfq_eval(const bfq_plan* plan, const double* f2, const double* f3, double* q,
              int64_t n_cells, void* stream);
 
 /* Same contract on HOST buffers: H2D, evaluate, D2H in pipelined chunks.
- * Blocks until q is written.  Host buffers may be pageable or pinned. */
+ * Blocks until q is written.  Pinned host buffers are copied asynchronously;
+ * pageable ones are staged chunk by chunk through pinned buffers owned by the
+ * plan (the host memcpy overlaps the device work of the chunks in flight).
+ * q must not overlap f2 or f3 (BFQ_EINVAL). */
 int bfq_eval_host(const bfq_plan* plan, const double* f2, const double* f3, double* q,
                   int64_t n_cells);
 
@@ -145,6 +149,9 @@ int bfq_host_plan_info(const bfq_desc* desc, int smem_limit, bfq_plan_info* info
 
 const char* bfq_strerror(int code);
 const char* bfq_last_error(void);
+/* Provenance: hash of the sources, headers and flags this library was built
+ * from (paper_2605_28475_b200/_build.py); the loader compares it with the tree. */
+const char* bfq_build_id(void);
 
 #ifdef __cplusplus
 }

@@ -11,8 +11,12 @@ import ctypes
 import os
 import threading
 
+from . import _build
+
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbfq.so")
+# BFQ_LIB=checked selects the self-checking build (libbfq_checked.so)
+CHECKED = os.environ.get("BFQ_LIB", "") == "checked"
+LIB_PATH = _build.lib_path(CHECKED)
 
 BFQ_OK = 0
 BFQ_EINVAL = -1
@@ -40,6 +44,7 @@ EXPORTED_SYMBOLS = (
     "bfq_project_maxwellians",
     "bfq_strerror",
     "bfq_last_error",
+    "bfq_build_id",
 )
 # every symbol include/bfr.h declares
 EXPORTED_SYMBOLS_BFR = ("bfr_assemble",)
@@ -159,12 +164,39 @@ def _declare(lib):
     lib.bfq_strerror.restype = ctypes.c_char_p
     lib.bfq_last_error.argtypes = []
     lib.bfq_last_error.restype = ctypes.c_char_p
+    lib.bfq_build_id.argtypes = []
+    lib.bfq_build_id.restype = ctypes.c_char_p
     lib.bfq_project_maxwellians.argtypes = [ctypes.c_int32, ctypes.c_int32, _f64p, _f64p, ctypes.c_int32, vp, vp, vp,
                                             vp, ctypes.c_int64, vp]
     lib.bfr_assemble.argtypes = [ctypes.POINTER(BfrDesc), ctypes.c_int, vp, vp, ctypes.POINTER(BfrStats)]
     for name in EXPORTED_SYMBOLS + EXPORTED_SYMBOLS_BFR:
-        if name not in ("bfq_strerror", "bfq_last_error"):
+        if name not in ("bfq_strerror", "bfq_last_error", "bfq_build_id"):
             getattr(lib, name).restype = ctypes.c_int
+
+
+def _ensure_current(path: str) -> None:
+    """The library must be built from the sources next to it (provenance).
+    A stale or missing binary is rebuilt in place (nvcc is part of the image);
+    BFQ_NO_AUTOBUILD=1 turns that into an error instead."""
+    if _build.is_current(CHECKED):
+        return
+    if os.environ.get("BFQ_NO_AUTOBUILD"):
+        raise EngineUnavailable(
+            f"{path} is missing or was not built from these sources "
+            f"(embedded {_build.embedded_hash(path)}, sources {_build.source_hash(CHECKED)}): "
+            "rebuild with `python -c 'import __graft_entry__ as g; g.build()'`")
+    import fcntl
+    import sys
+
+    os.makedirs(_build.BUILD, exist_ok=True)
+    with open(os.path.join(_build.BUILD, ".lock"), "w") as lk:
+        fcntl.flock(lk, fcntl.LOCK_EX)
+        if not _build.is_current(CHECKED):
+            sys.stderr.write(f"[bfq] {os.path.basename(path)} stale or missing: rebuilding from source\n")
+            try:
+                _build.build(checked=CHECKED)
+            except (RuntimeError, OSError) as exc:
+                raise EngineUnavailable(f"cannot build {path}: {exc}") from exc
 
 
 def lib():
@@ -173,6 +205,7 @@ def lib():
     if _lib is None:
         with _lock:
             if _lib is None:
+                _ensure_current(LIB_PATH)
                 if not os.path.exists(LIB_PATH):
                     raise EngineUnavailable(
                         f"{LIB_PATH} is missing: build the CUDA engine with "
@@ -183,6 +216,9 @@ def lib():
                 except OSError as exc:  # pragma: no cover - environment specific
                     raise EngineUnavailable(f"cannot load {LIB_PATH}: {exc}") from exc
                 _declare(handle)
+                got = handle.bfq_build_id().decode()
+                if got != _build.source_hash(CHECKED):
+                    raise EngineUnavailable(f"{LIB_PATH} build id {got} does not match the sources")
                 _lib = handle
     return _lib
 

@@ -29,7 +29,19 @@
 #include <vector>
 #include <type_traits>
 
+#include "bfq_device.cuh"
 #include "bfq_internal.h"
+
+namespace bfq {
+typedef void (*QKernel)(const KParams);
+// per-size instantiation units (bfq_inst_*.cu)
+QKernel pick_n5(bool, int, int);
+QKernel pick_n9(bool, int, int);
+QKernel pick_n11(bool, int, int);
+QKernel pick_n13(bool, int, int);
+QKernel pick_n17(bool, int, int);
+QKernel pick_generic(bool, int, int);
+}  // namespace bfq
 
 using namespace bfq;
 
@@ -53,276 +65,22 @@ struct DevProgram {
   Item* items = nullptr;
   int n_items = 0;
   double exec_macs_per_cell = 0.0;
-  void (*kernel)(const struct KParams) = nullptr;
+  QKernel kernel = nullptr;
 };
 
 unsigned long long* bfq_dbg_clk_ptr = nullptr;  // BFQ_DEBUG bit 3 only
 
-struct KParams {
-  const double* f2;
-  const double* f3;
-  double* q;
-  long long n_cells;
-  long long n_tiles;
-  int n_items;     // CTAs (items) per cell tile
-  int tile_chunk;  // tiles per item-major chunk of the grid
-  const double* R;
-  const Row* rows;
-  const int* sstart;
-  const ChanEntry* chans;
-  const Group* groups;
-  const int16_t* unit_m1;
-  const Item* items;
-  int nk, nq, qs, k2s, k2p, k2sd, k2pd;
-  int cells, m1t, nw, nstage;
-  int conservation;
-  int hdr, max_chan, nteams;
-  int debug;  // timing experiments only (BFQ_DEBUG): bit0 skip stage 1, bit1 skip stage 2, bit3 phase clocks
-  unsigned long long* dbg_clk;  // [8] phase cycle totals when bit3 set
-};
-
-// CTA -> (item, tile).  Tiles are taken in chunks of TILE_CHUNK; inside a
-// chunk the CTAs run item-major (heavy items first), so all items of a tile
-// are resident within a few waves and the tile's cells are read from HBM
-// once (L2 serves the other items), while only the last chunk's tail sees
-// the light items last.
-constexpr int TILE_CHUNK = 64;  // minimum; BFQ_TILE_CHUNK overrides (experiments)
-__device__ __forceinline__ void cta_item_tile(const long long b, const long long n_tiles, const int n_items,
-                                              const int chunk, long long& item, long long& tile) {
-  const long long full = n_tiles / chunk, per = (long long)chunk * n_items;
-  if (b < full * per) {
-    const long long ch = b / per, r = b - ch * per;
-    item = r / chunk;
-    tile = ch * chunk + (r - item * chunk);
-  } else {
-    const long long rem = n_tiles - full * chunk, r = b - full * per;
-    item = r / rem;
-    tile = full * chunk + (r - item * rem);
-  }
-}
-
-// ------------------------------------------------------------ PTX helpers
-// Not volatile: the scheduler may move shared loads across DMMAs.
-__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
-  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-      : "+d"(d0), "+d"(d1)
-      : "d"(a), "d"(b));
-}
-
-// Gather from the staged cells: read-only after the staging barrier, so a
-// plain (non-volatile) asm the compiler may schedule freely.
-__device__ __forceinline__ double lds_ro(uint32_t addr) {
-  double v;
-  asm("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(addr));
-  return v;
-}
-
-// Loads/stores of buffers rewritten inside the kernel (Phi, R ring): volatile
-// so they stay ordered with the warp syncs and mbarrier waits.
-__device__ __forceinline__ double lds_v(uint32_t addr) {
-  double v;
-  asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(addr) : "memory");
-  return v;
-}
-
-__device__ __forceinline__ void named_bar_sync(unsigned id, unsigned count) {
-  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void sts_v(uint32_t addr, double v) {
-  asm volatile("st.shared.f64 [%0], %1;\n" ::"r"(addr), "d"(v) : "memory");
-}
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(smem_u32(bar))
-               : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n" ::"r"(
-                   smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-
-// try_wait with a suspend-time hint: the waiting warp sleeps in hardware
-// until the phase flips (or the hint expires) instead of spinning on issue slots.
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-  asm volatile(
-      "{\n"
-      " .reg .pred p;\n"
-      "WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n"
-      " @!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
-// Non-blocking probe of an mbarrier phase.
-__device__ __forceinline__ bool mbar_test(uint64_t* bar, unsigned parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n"
-      " .reg .pred p;\n"
-      " mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-      " selp.u32 %0, 1, 0, p;\n"
-      "}\n"
-      : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
-// volatile: the compiler must issue the table-row load where it is written
-// (early, as a prefetch), not sink it next to its first use.
-__device__ __forceinline__ Row load_row(const Row* rows, int z) {
-  int4 v;
-  asm volatile("ld.global.nc.v4.s32 {%0,%1,%2,%3}, [%4];\n"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-               : "l"(reinterpret_cast<const int4*>(rows) + z));
-  Row r;
-  r.q2 = v.x;
-  r.q3 = v.y;
-  r.g = __hiloint2double(v.w, v.z);
-  return r;
-}
-
-__device__ __forceinline__ Row fetch_row(const Row* rows, int z, int ze) {
-  if (z < ze) return load_row(rows, z);
-  Row r;
-  r.q2 = 0;
-  r.q3 = 0;
-  r.g = 0.0;
-  return r;
-}
-
-// Branch-free fetch of row z of a range ending at ze: always loads a valid
-// row (clamped into [0, ze-1], row 0 for an empty range) and zeroes g when z
-// is past the end, so padding lanes and exhausted streams contribute 0.
-__device__ __forceinline__ Row fetch_row_bf(const Row* rows, int z, int ze) {
-  Row r = load_row(rows, max(min(z, ze - 1), 0));
-  r.g = z < ze ? r.g : 0.0;
-  return r;
-}
-
-__device__ __forceinline__ Row fetch_row_clamped(const Row* rows, int z, int ze) {
-  Row r = load_row(rows, min(z, ze - 1));
-  if (z >= ze) r.g = 0.0;  // padding lane of the last k-step: contributes 0
-  return r;
-}
-
-// ------------------------------------------------------------ the Q kernel
-#include "bfq_qkernel.cuh"
-#include "bfq_qkernel2.cuh"
-
-typedef void (*QKernel)(const KParams);
-
-// Compile-time-size instantiations for the BASELINE configurations (all
-// gathers then use immediate offsets); anything else runs the generic kernel.
-template <bool BILIN, int NK, int QS>
-QKernel pick_fixed(int mt, int cells) {
-  constexpr int MT = (NK + 7) / 8;
-  if (mt != MT) return nullptr;
-  if constexpr (MT == 1) {
-    if (cells == 8) return bfq_q_kernel<1, 8, BILIN, NK, QS>;
-    if (cells == 4) return bfq_q_kernel<1, 4, BILIN, NK, QS>;
-  } else if constexpr (MT == 2) {
-    if (cells == 4) return bfq_q_kernel<2, 4, BILIN, NK, QS>;
-    if (cells == 2) return bfq_q_kernel<2, 2, BILIN, NK, QS>;
-  } else {
-    if (cells == 2) return bfq_q_kernel<MT, 2, BILIN, NK, QS>;
-    if (cells == 1) return bfq_q_kernel<MT, 1, BILIN, NK, QS>;
-  }
-  return nullptr;
-}
-
-template <bool BILIN>
-QKernel pick_kernel(int mt, int cells, int nk, int qs) {
+QKernel pick_kernel(bool bilin, int mt, int cells, int nk, int qs) {
   QKernel k = nullptr;
   if (!std::getenv("BFQ_GENERIC")) {
-    if (nk == 13 && qs == 172) k = pick_fixed<BILIN, 13, 172>(mt, cells);
-    else if (nk == 9 && qs == 84) k = pick_fixed<BILIN, 9, 84>(mt, cells);
-    else if (nk == 11 && qs == 124) k = pick_fixed<BILIN, 11, 124>(mt, cells);
-    else if (nk == 5 && qs == 28) k = pick_fixed<BILIN, 5, 28>(mt, cells);
-    else if (nk == 17 && qs == 292) k = pick_fixed<BILIN, 17, 292>(mt, cells);
+    if (nk == 13 && qs == 172) k = pick_n13(bilin, mt, cells);
+    else if (nk == 9 && qs == 84) k = pick_n9(bilin, mt, cells);
+    else if (nk == 11 && qs == 124) k = pick_n11(bilin, mt, cells);
+    else if (nk == 5 && qs == 28) k = pick_n5(bilin, mt, cells);
+    else if (nk == 17 && qs == 292) k = pick_n17(bilin, mt, cells);
     if (k) return k;
   }
-  if (mt == 1) {
-    if (cells == 8) return bfq_q_kernel<1, 8, BILIN, 0, 0>;
-    if (cells == 4) return bfq_q_kernel<1, 4, BILIN, 0, 0>;
-    if (cells == 2) return bfq_q_kernel<1, 2, BILIN, 0, 0>;
-    if (cells == 1) return bfq_q_kernel<1, 1, BILIN, 0, 0>;
-  }
-  if (mt == 2) {
-    if (cells == 4) return bfq_q_kernel<2, 4, BILIN, 0, 0>;
-    if (cells == 2) return bfq_q_kernel<2, 2, BILIN, 0, 0>;
-    if (cells == 1) return bfq_q_kernel<2, 1, BILIN, 0, 0>;
-  }
-  if (mt == 3) {
-    if (cells == 2) return bfq_q_kernel<3, 2, BILIN, 0, 0>;
-    if (cells == 1) return bfq_q_kernel<3, 1, BILIN, 0, 0>;
-  }
-  return nullptr;
-}
-
-template <bool BILIN, int NK, int QS>
-QKernel pick_fixed2(int mt, int cells) {
-  constexpr int MT = (NK + 7) / 8;
-  if (mt != MT) return nullptr;
-  if constexpr (MT == 1) {
-    if (cells == 8) return bfq_q_kernel2<1, 8, BILIN, NK, QS>;
-    if (cells == 4) return bfq_q_kernel2<1, 4, BILIN, NK, QS>;
-  } else if constexpr (MT == 2) {
-    if constexpr (NK == 9) {
-      if (cells == 8) return bfq_q_kernel2<2, 8, BILIN, NK, QS>;  // X1: one DMMA tile per cell
-    }
-    if (cells == 4) return bfq_q_kernel2<2, 4, BILIN, NK, QS>;
-    if (cells == 2) return bfq_q_kernel2<2, 2, BILIN, NK, QS>;
-  } else {
-    if (cells == 2) return bfq_q_kernel2<MT, 2, BILIN, NK, QS>;
-  }
-  return nullptr;
-}
-
-template <bool BILIN>
-QKernel pick_kernel2(int mt, int cells, int nk, int qs) {
-  QKernel k = nullptr;
-  if (!std::getenv("BFQ_GENERIC")) {
-    if (nk == 13 && qs == 172) k = pick_fixed2<BILIN, 13, 172>(mt, cells);
-    else if (nk == 9 && qs == 84) k = pick_fixed2<BILIN, 9, 84>(mt, cells);
-    else if (nk == 11 && qs == 124) k = pick_fixed2<BILIN, 11, 124>(mt, cells);
-    else if (nk == 5 && qs == 28) k = pick_fixed2<BILIN, 5, 28>(mt, cells);
-    else if (nk == 17 && qs == 292) k = pick_fixed2<BILIN, 17, 292>(mt, cells);
-    if (k) return k;
-  }
-  if (mt == 1) {
-    if (cells == 8) return bfq_q_kernel2<1, 8, BILIN, 0, 0>;
-    if (cells == 4) return bfq_q_kernel2<1, 4, BILIN, 0, 0>;
-    if (cells == 2) return bfq_q_kernel2<1, 2, BILIN, 0, 0>;
-  }
-  if (mt == 2) {
-    if (cells == 4) return bfq_q_kernel2<2, 4, BILIN, 0, 0>;
-    if (cells == 2) return bfq_q_kernel2<2, 2, BILIN, 0, 0>;
-  }
-  if (mt == 3 && cells == 2) return bfq_q_kernel2<3, 2, BILIN, 0, 0>;
-  return nullptr;
+  return pick_generic(bilin, mt, cells);
 }
 
 // ------------------------------------------------------------ small kernels
@@ -380,6 +138,8 @@ struct HostPathScratch {
   cudaStream_t st[NB] = {nullptr, nullptr, nullptr};
   double* buf[NB] = {nullptr, nullptr, nullptr};
   size_t cap = 0;  // doubles per buffer
+  double* pin[NB] = {nullptr, nullptr, nullptr};  // pinned staging for pageable host buffers
+  size_t pin_cap = 0;
 };
 
 struct bfq_plan {
@@ -417,11 +177,7 @@ int upload_program(const Program& pg, DevProgram& dp, size_t& total, int smem_op
   if ((rc = upload(pg.groups, &dp.groups, total))) return rc;
   if ((rc = upload(pg.unit_m1, &dp.unit_m1, total))) return rc;
   if ((rc = upload(pg.items, &dp.items, total))) return rc;
-  QKernel k = pg.cfg.pairsplit
-                  ? (pg.bilinear ? pick_kernel2<true>(pg.cfg.mt, pg.cfg.cells, nk, qs)
-                                 : pick_kernel2<false>(pg.cfg.mt, pg.cfg.cells, nk, qs))
-                  : (pg.bilinear ? pick_kernel<true>(pg.cfg.mt, pg.cfg.cells, nk, qs)
-                                 : pick_kernel<false>(pg.cfg.mt, pg.cfg.cells, nk, qs));
+  QKernel k = pick_kernel(pg.bilinear, pg.cfg.mt, pg.cfg.cells, nk, qs);
   if (!k) {
     set_error("no kernel instantiation for this tiling");
     return BFQ_EINVAL;
@@ -519,6 +275,23 @@ struct DeviceGuard {
   }
 };
 
+// The output may not share bytes with an input: CTAs of one cell tile still
+// read its cells while other CTAs of the tile already write Q.
+bool io_overlap(const bfq_plan* plan, const double* f2, const double* f3, const double* q, int64_t n_cells) {
+  if (n_cells <= 0) return false;
+  const uintptr_t span = (uintptr_t)n_cells * plan->hp.n_k * plan->hp.n_q * sizeof(double);
+  auto hit = [&](const double* in) {
+    if (!in) return false;
+    const uintptr_t a = (uintptr_t)in, b = (uintptr_t)q;
+    return a < b + span && b < a + span;
+  };
+  if (hit(f2) || hit(f3)) {
+    set_error("q must not overlap f2 or f3 (in-place evaluation is not supported)");
+    return true;
+  }
+  return false;
+}
+
 int plan_from_desc(const bfq_desc* desc, int device, bfq_plan** out) {
   if (!desc || !out) {
     set_error("null argument");
@@ -587,6 +360,7 @@ int bfq_plan_destroy(bfq_plan* plan) {
     if (plan->host) {
       for (int b = 0; b < HostPathScratch::NB; ++b) {
         cudaFree(plan->host->buf[b]);
+        cudaFreeHost(plan->host->pin[b]);
         if (plan->host->st[b]) cudaStreamDestroy(plan->host->st[b]);
       }
       delete plan->host;
@@ -637,6 +411,7 @@ int bfq_eval(const bfq_plan* plan, const double* f2, const double* f3, double* q
     set_error("null buffer");
     return BFQ_EINVAL;
   }
+  if (io_overlap(plan, f2, f3, q, n_cells)) return BFQ_EINVAL;
   DeviceGuard guard(plan->device);
   const bool same = (f3 == nullptr || f3 == f2);
   return launch_q(plan, same ? plan->sym : plan->full, f2, same ? f2 : f3, q, n_cells, (cudaStream_t)stream);
@@ -648,6 +423,7 @@ int bfq_eval_host(const bfq_plan* plan, const double* f2, const double* f3, doub
     return BFQ_EINVAL;
   }
   if (n_cells == 0) return BFQ_OK;
+  if (io_overlap(plan, f2, f3, q, n_cells)) return BFQ_EINVAL;
   DeviceGuard guard(plan->device);
   const bool same = (f3 == nullptr || f3 == f2);
   const size_t ndof = (size_t)plan->hp.n_k * plan->hp.n_q;
@@ -689,7 +465,46 @@ int bfq_eval_host(const bfq_plan* plan, const double* f2, const double* f3, doub
       set_error("stream creation failed");
       return BFQ_ECUDA;
     }
+  // Pageable host buffers cannot be copied asynchronously: stage them through
+  // pinned buffers owned by the plan, so the host memcpy of chunk i+1 (and the
+  // copy-out of chunk i-NB) overlaps the device work of the chunks in flight.
+  auto pinned = [](const void* p) {
+    if (!p) return true;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+  };
+  const bool stage_in = !pinned(f2) || (!same && !pinned(f3));
+  const bool stage_out = !pinned(q);
+  if ((stage_in || stage_out) && hs->pin_cap < need) {
+    for (int b = 0; b < NB; ++b) {
+      cudaFreeHost(hs->pin[b]);
+      hs->pin[b] = nullptr;
+    }
+    hs->pin_cap = 0;
+    for (int b = 0; b < NB; ++b)
+      if (cudaMallocHost(&hs->pin[b], need * sizeof(double)) != cudaSuccess) {
+        set_error("pinned host allocation failed");
+        return BFQ_ENOMEM;
+      }
+    hs->pin_cap = need;
+  }
   int rc = BFQ_OK;
+  std::vector<int64_t> pending(NB, -1);  // chunk start whose staged Q is still in pin[b]
+  auto drain = [&](int b) {
+    if (pending[b] < 0) return;
+    if (cudaStreamSynchronize(hs->st[b]) != cudaSuccess) {
+      set_error(cudaGetErrorString(cudaGetLastError()));
+      rc = BFQ_ECUDA;
+    } else {
+      const int64_t n = std::min<int64_t>(chunk, n_cells - pending[b]);
+      std::memcpy(q + pending[b] * ndof, hs->pin[b] + 2 * per, n * ndof * sizeof(double));
+    }
+    pending[b] = -1;
+  };
   for (int64_t c0 = 0, i = 0; c0 < n_cells && rc == BFQ_OK; c0 += chunk, ++i) {
     const int b = (int)(i % NB);
     cudaStream_t st = hs->st[b];
@@ -698,24 +513,42 @@ int bfq_eval_host(const bfq_plan* plan, const double* f2, const double* f3, doub
     double* dq = d2 + per;
     double* d3 = same ? d2 : dq + per;
     const size_t bytes = n * ndof * sizeof(double);
-    if (cudaMemcpyAsync(d2, f2 + c0 * ndof, bytes, cudaMemcpyHostToDevice, st) != cudaSuccess ||
-        (!same && cudaMemcpyAsync(d3, f3 + c0 * ndof, bytes, cudaMemcpyHostToDevice, st) != cudaSuccess)) {
+    if (stage_out) drain(b);
+    else if (stage_in && i >= NB && cudaStreamSynchronize(st) != cudaSuccess) {  // pin[b] still being read
+      set_error(cudaGetErrorString(cudaGetLastError()));
+      rc = BFQ_ECUDA;
+    }
+    if (rc) break;
+    const double* s2 = f2 + c0 * ndof;
+    const double* s3 = same ? s2 : f3 + c0 * ndof;
+    if (stage_in) {  // pin[b] = [f2 chunk | f3 chunk | Q chunk]
+      std::memcpy(hs->pin[b], s2, bytes);
+      if (!same) std::memcpy(hs->pin[b] + per, s3, bytes);
+      s2 = hs->pin[b];
+      s3 = same ? s2 : hs->pin[b] + per;
+    }
+    if (cudaMemcpyAsync(d2, s2, bytes, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+        (!same && cudaMemcpyAsync(d3, s3, bytes, cudaMemcpyHostToDevice, st) != cudaSuccess)) {
       set_error("host-to-device copy failed");
       rc = BFQ_ECUDA;
       break;
     }
     rc = launch_q(plan, same ? plan->sym : plan->full, d2, d3, dq, n, st);
     if (rc) break;
-    if (cudaMemcpyAsync(q + c0 * ndof, dq, bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess) {
+    double* dst = stage_out ? hs->pin[b] + 2 * per : q + c0 * ndof;
+    if (cudaMemcpyAsync(dst, dq, bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess) {
       set_error("device-to-host copy failed");
       rc = BFQ_ECUDA;
     }
+    if (stage_out) pending[b] = c0;
   }
-  for (int b = 0; b < NB; ++b)
+  for (int b = 0; b < NB; ++b) {
+    if (stage_out && rc == BFQ_OK) drain(b);
     if (cudaStreamSynchronize(hs->st[b]) != cudaSuccess && rc == BFQ_OK) {
       set_error(cudaGetErrorString(cudaGetLastError()));
       rc = BFQ_ECUDA;
     }
+  }
   return rc;
 }
 

@@ -819,7 +819,19 @@ int assemble(const bfr_desc& d, int device, double* r_out, double* halves_out, b
     set_error("device ordinal out of range");
     return BFQ_EINVAL;
   }
-  BFR_TRY(cudaSetDevice(device));
+  // restore the caller's current device on every exit path (torch keeps its own)
+  struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+      cudaGetDevice(&prev);
+      if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+      int cur = -1;
+      cudaGetDevice(&cur);
+      if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+  } guard(device);
   int rc;
   if ((rc = set_ybar_constants())) return rc;
   DevBuf db;

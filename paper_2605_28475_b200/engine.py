@@ -222,6 +222,14 @@ def _check_batch(plan: GpuPlan, t, name: str):
         raise ValueError(f"{name} must be C-contiguous")
 
 
+def _overlaps(a, b) -> bool:
+    """True when the byte ranges of two tensors intersect."""
+    a0, b0 = a.data_ptr(), b.data_ptr()
+    a1 = a0 + a.numel() * a.element_size()
+    b1 = b0 + b.numel() * b.element_size()
+    return a.numel() > 0 and b.numel() > 0 and a0 < b1 and b0 < a1
+
+
 def evaluate_batch(op, f, f3=None, out=None, stream=None):
     """Q(f, f3) for every cell of ``f`` (B, n_k, n_q) on the GPU.
 
@@ -242,6 +250,11 @@ def evaluate_batch(op, f, f3=None, out=None, stream=None):
         _check_batch(plan, out, "out")
         if out.shape != f.shape:
             raise ValueError("out must have the shape of f")
+        # CTAs of one tile read its cells while other CTAs already write Q:
+        # an output that overlaps an input would be read back half-written
+        for name, t in (("f", f), ("f3", f3)):
+            if t is not None and _overlaps(out, t):
+                raise ValueError(f"out must not overlap {name} (in-place evaluation is not supported)")
     st = (stream or torch.cuda.current_stream(plan.device)).cuda_stream
     p3 = None if f3 is None or f3 is f else f3.data_ptr()
     plan.eval_device(f.data_ptr(), p3, out.data_ptr(), f.shape[0], st)

@@ -266,7 +266,7 @@ def _f64(a):
 
 
 def assemble_r_tensor(cfg: SpectralConfig, grid: GridSpec | None = None, *, kernel_scale: float = 1.0,
-                      threads: int = 1, device: int = 0, return_halves: bool = False):
+                      threads: int = 1, device: int | None = None, return_halves: bool = False):
     """Integrate the physical tensor for every channel on the GPU.
 
     Same result as kinematic.assemble_r_tensor (kinematic.py:521-570): gain +
@@ -275,6 +275,10 @@ def assemble_r_tensor(cfg: SpectralConfig, grid: GridSpec | None = None, *, kern
     accepted for signature compatibility (the device does the work).
     """
     del threads
+    if device is None:  # the caller's current CUDA device, as torch sees it
+        from .engine import _default_device
+
+        device = _default_device()
     if grid is None:
         grid = grid_sizes(cfg.k_max, cfg.l_max)
     check_grid(grid, cfg.k_max, cfg.l_max)
@@ -421,7 +425,7 @@ def build_gaunt_coo(l_max: int) -> GauntCOO:
 def build_operator(cfg: SpectralConfig, pad_rad: int = 16, pad_ang: int = 16, *,
                    grid: GridSpec | None = None, threads: int = 1, conservation: bool = True,
                    detailed_balance: bool = True, kernel_scale: float = 1.0,
-                   device: int = 0) -> FactorizedOperator:
+                   device: int | None = None) -> FactorizedOperator:
     """Assemble the factorized operator with the null-space corrections
     (contraction.py:158-177), R integrals on the GPU."""
     if grid is None:
