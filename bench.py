@@ -1,12 +1,21 @@
 """Benchmark of the Q(f,f) hot path (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config hs12|hs8|mm10|hs4]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config hs12|hs8|hs16|mm10|rk4|hs4|rbuild12|...] [--scaling strong|weak]
 
-One step = one Q(f,f) evaluation of every cell of the rank's batch (one
-``bfq_eval`` launch).  Default workload = BASELINE config 3 (hard spheres,
-N=L=12, 65,536 cells per GPU; weak scaling: each rank evaluates its own
-65,536-cell shard of a 65,536*N-cell global batch, no data-path collective).
-Rank 0 prints one JSON line.  See DESIGN.md §Measurement.
+One step = one Q(f,f) evaluation of every cell of the rank's shard (one
+``bfq_eval`` launch).  Default workload = BASELINE config 3: hard spheres,
+N=L=12, a fixed 65,536-cell global batch sharded evenly over the GPUs
+(strong scaling, as BASELINE config 3 states; ``--scaling weak`` gives every
+GPU the full batch instead).  ``--gpus N`` without torchrun's environment
+re-launches this script through ``torch.distributed.run`` with N ranks; under
+torchrun the rank layout comes from RANK / WORLD_SIZE / LOCAL_RANK.  No
+collective runs inside the timed region (cells are independent); the step
+time is the max over ranks and NCCL is used only for the diagnostics
+all-reduce after it.  After the timed region the run checks its OWN outputs:
+a stratified sample of the timed batch (every cell for config 2) against the
+CPU oracle, which is also the timed CPU baseline.  Rank 0 prints one JSON
+line.  See DESIGN.md §4.
 """
 
 from __future__ import annotations
@@ -15,6 +24,8 @@ import argparse
 import json
 import math
 import os
+import platform
+import socket
 import statistics
 import subprocess
 import sys
@@ -24,16 +35,16 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 CONFIGS = {
-    # name: (operator file, cells per GPU, generator, description)
-    "hs12": ("hs_n12", 65536, "pm", "config3: hard spheres N=L=12, perturbed Maxwellians"),
-    "hs8": ("hs_n8", 4096, "pm", "config2: hard spheres N=L=8, perturbed Maxwellians"),
-    "mm10": ("mm_n10", 32768, "bimodal", "config5 operator: Maxwell N=L=10, bimodal cells (single Q eval)"),
-    "hs4": ("hs_n4", 65536, "pm", "hard spheres N=L=4 (small)"),
-    "hs16": ("hs_n16", 16384, "pm", "config4: hard spheres N=L=16, perturbed Maxwellians"),
+    # name: (operator file, global cells, generator, description, parity sample (0 = every cell))
+    "hs12": ("hs_n12", 65536, "pm", "config3: hard spheres N=L=12, perturbed Maxwellians", 256),
+    "hs8": ("hs_n8", 4096, "pm", "config2: hard spheres N=L=8, perturbed Maxwellians", 0),
+    "mm10": ("mm_n10", 32768, "bimodal", "config5 operator: Maxwell N=L=10, bimodal cells (single Q eval)", 256),
+    "hs4": ("hs_n4", 65536, "pm", "hard spheres N=L=4 (small)", 256),
+    "hs16": ("hs_n16", 16384, "pm", "config4: hard spheres N=L=16, perturbed Maxwellians", 256),
     "syn16": ("synth_n16", 16384, "pm", "config4 shape N=L=16 with a SYNTHETIC R (real Gaunt table, random "
-                                        "slot-symmetric R with the reference's null-space zeroing): timing only"),
+                                        "slot-symmetric R with the reference's null-space zeroing): timing only", 64),
     "rk4": ("mm_n10", 32768, "bimodal", "config5: Maxwell N=L=10, bimodal cells, GPU-resident RK4 dt=0.01 "
-                                         "(one step = one RK4 step = 4 Q(f,f) per cell)"),
+                                         "(one step = one RK4 step = 4 Q(f,f) per cell)", 0),
 }
 # the operator build.  One step = one full R-tensor
 # assembly (every channel's gain / loss integrals over both Duffy patches).
@@ -45,6 +56,9 @@ RBUILD = {
 METRIC = "Q(f,f) cell-evals/s (fp64, hard spheres L=N=12) and FP64/HBM roofline frac"
 RBUILD_METRIC = "R-tensor assembly channel integrals/s (fp64, hard spheres, pad 16/16)"
 FP64_PEAK_TFLOPS = 37.1  # DMMA.8x8x4 sustained, measured on this pool (profiles/fp64_peak.txt)
+# SURVEY §8d "datasheet ~37 TF": 148 SMs x 128 FP64 tensor flop/clk/SM x 1.965 GHz max boost
+FP64_NOMINAL_TFLOPS = 148 * 128 * 1.965e9 / 1e12
+L2_BYTES = 132644864
 
 
 def env_int(name, default):
@@ -62,6 +76,17 @@ def measured_peaks():
         return {}
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return platform.processor() or "unknown"
+
+
 def make_cells(cfg_name, n_k, l_max, n, seed, start, device=None):
     """Seeded cells (host numpy); with ``device`` the Maxwellian projection runs
     on the GPU (bfq_project_maxwellians, same draws, equal to rounding)."""
@@ -77,9 +102,28 @@ def make_cells(cfg_name, n_k, l_max, n, seed, start, device=None):
     return inputs.bimodal(n_k, l_max, n, seed=seed, start=start)
 
 
+def stratified_indices(n, k):
+    """``k`` cell indices spread evenly over [0, n): first and last cell, every
+    stretch of the batch (hence every tile chunk of the grid), and the ragged
+    last tile; ``k = 0`` or ``k >= n`` selects every cell."""
+    import numpy as np
+
+    if n == 0:
+        return np.zeros(0, dtype=np.int64)
+    if k <= 0 or k >= n:
+        return np.arange(n, dtype=np.int64)
+    idx = np.unique(np.round(np.linspace(0, n - 1, k)).astype(np.int64))
+    tail = np.arange(max(0, n - 3), n, dtype=np.int64)  # the last (possibly partial) tile
+    return np.unique(np.concatenate([idx, tail]))
+
+
 # ------------------------------------------------------------------ CPU legs
 def _cpu_worker(args):
+    """Oracle Q of a block of cells in one process, one BLAS thread: the
+    reference's q_angular_first operations (oracle/q_oracle.py)."""
     path, cells = args
+    import numpy as np
+
     from oracle import q_oracle
     from paper_2605_28475_b200.operator import load_cache
 
@@ -92,35 +136,42 @@ def _cpu_worker(args):
     ctx = threadpool_limits(limits=1) if threadpool_limits else None
     if ctx:
         ctx.__enter__()
+    out = np.empty_like(cells)
     t0 = time.perf_counter()
-    for c in cells:
-        q_oracle.q_angular_first(op, c, workspace=ws)
+    for i, c in enumerate(cells):
+        out[i] = q_oracle.q_angular_first(op, c, workspace=ws)
     dt = time.perf_counter() - t0
     if ctx:
         ctx.__exit__(None, None, None)
-    return len(cells), dt
+    return out, dt
 
 
-def cpu_port_rate(cfg_name, cells, budget_s=15.0, cores=None, path=None):
-    """Oracle port (numpy restatement of q_angular_first) on host cores: cells/s."""
+def oracle_pool(path, cells, cores=None):
+    """Oracle Q of ``cells`` on ``cores`` host processes (one thread each),
+    contiguous blocks, the pattern of cli.py:406-410.  Returns (q, info):
+    cells/s over the slowest worker's busy time, plus the 1-core rate."""
     import multiprocessing as mp
 
-    path = path or os.path.join(ROOT, "operators", CONFIGS[cfg_name][0] + ".bfct")
-    cores = cores or os.cpu_count() or 1
-    # calibrate on one cell, then give every worker ~budget_s of work
-    n1, dt1 = _cpu_worker((path, cells[:1]))
-    per_worker = max(1, int(budget_s / max(dt1, 1e-6)))
-    n = min(cells.shape[0], per_worker * cores)
-    chunks = [(path, cells[i::cores][: per_worker]) for i in range(cores)]
-    chunks = [c for c in chunks if len(c[1])]
+    import numpy as np
+
+    cores = max(1, min(cores or os.cpu_count() or 1, cells.shape[0]))
+    _, t1 = _cpu_worker((path, cells[:2]))  # 1-core rate (operator load + workspace excluded)
+    bounds = np.linspace(0, cells.shape[0], cores + 1).round().astype(int)
+    chunks = [(path, cells[bounds[i]:bounds[i + 1]]) for i in range(cores) if bounds[i + 1] > bounds[i]]
     t0 = time.perf_counter()
     with mp.get_context("spawn").Pool(len(chunks)) as pool:
         res = pool.map(_cpu_worker, chunks)
     wall = time.perf_counter() - t0
-    done = sum(r[0] for r in res)
+    q = np.concatenate([r[0] for r in res])
     busy = max(r[1] for r in res)
-    return {"value": done / busy, "cells": done, "cores": len(chunks), "wall_s": wall, "busy_s": busy,
-            "single_cell_s": dt1}
+    return q, {"value": cells.shape[0] / busy, "cells": int(cells.shape[0]), "cores": len(chunks),
+               "busy_s": busy, "wall_s": wall, "single_core_cells_per_s": 2.0 / t1}
+
+
+def free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
 
 
 def _rbuild_cpu_worker(args):
@@ -268,7 +319,8 @@ class ClockSampler:
 # ------------------------------------------------------------------ arms
 def run_reference(args, rank, world):
     """--impl reference: the reference's CPU path (oracle port of
-    contraction.q_angular_first) on all host cores, rank 0 only."""
+    contraction.q_angular_first, the same operations and the same speed per
+    cell, profiles/r01_cpu_ref_vs_port.txt) on all host cores, rank 0 only."""
     if rank != 0:
         return
     if args.config in RBUILD:
@@ -286,11 +338,11 @@ def run_reference(args, rank, world):
             "config": {"workload": f"R-tensor assembly N={k} L={l} gamma={gam}",
                        "step": "one channel per host core (random sample), oracle port of channel_half"},
             "cpu_baseline": {"value": v, "unit": "channels/s", "cores": r["cores"], "kind": "port",
-                             "sample": f"{r['channels']} random channels, one per core"},
+                             "sample": f"{r['channels']} random channels, one per core", "cpu": cpu_model()},
             "e2e": {"value": v, "unit": "channels/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         }), flush=True)
         return
-    opfile, n_cells, _, desc = CONFIGS[args.config]
+    opfile, n_global, _, desc, _ = CONFIGS[args.config]
     from paper_2605_28475_b200.operator import load_cache
 
     path = os.path.join(ROOT, "operators", opfile + ".bfct")
@@ -299,25 +351,36 @@ def run_reference(args, rank, world):
                           "CPU build) is not shipped with this snapshot"}), flush=True)
         return
     op = load_cache(path)
-    cells = make_cells(args.config, op.cfg.n_k, op.cfg.l_max, 256, seed=args.seed, start=0)
-    rates, walls = [], []
+    cores = os.cpu_count() or 1
+    # calibrate one cell, then size each step's sample to ~cpu_budget s per core
+    probe = make_cells(args.config, op.cfg.n_k, op.cfg.l_max, 2, seed=args.seed, start=0)
+    _, t2 = _cpu_worker((path, probe))
+    per_core = max(1, int(args.cpu_budget / max(t2 / 2, 1e-6)))
+    n_sample = min(n_global, per_core * cores)
+    # the leading cells of the batch (per-cell CPU cost does not depend on the values;
+    # generating the whole 65,536-cell batch on the host would take ~40 s)
+    cells = make_cells(args.config, op.cfg.n_k, op.cfg.l_max, n_sample, seed=args.seed, start=0)
     for _ in range(args.warmup):
-        cpu_port_rate(args.config, cells, budget_s=2.0)
+        oracle_pool(path, cells[:cores], cores)
+    rates, walls = [], []
     for _ in range(args.steps):
-        r = cpu_port_rate(args.config, cells, budget_s=args.cpu_budget)
+        _, r = oracle_pool(path, cells, cores)
         rates.append(r["value"])
         walls.append(r["wall_s"])
         last = r
     v = statistics.median(rates)
+    sample = (f"the first {n_sample} cells of the {n_global}-cell batch per step "
+              f"({math.ceil(n_sample / last['cores'])} per core, ~{last['busy_s']:.1f} s of work per core); "
+              "rate = sample / slowest worker's busy time")
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "cells/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(walls),
-        "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.json distributions)",
-        "config": {"workload": desc, "cells_per_gpu": n_cells, "operator": opfile,
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded, BASELINE.json distributions)",
+        "config": {"workload": desc, "global_cells": n_global, "operator": opfile, "seed": args.seed,
                    "step": "one bounded sample of the workload on all host cores (multiprocessing pool)"},
-        "cpu_baseline": {"value": v, "unit": "cells/s", "cores": last["cores"], "kind": "port",
-                         "sample": f"~{args.cpu_budget:.0f} s of per-core work per step, cells of {desc}"},
+        "cpu_baseline": {"value": v, "unit": "cells/s", "cores": last["cores"], "kind": "port", "sample": sample,
+                         "cpu": cpu_model(), "single_core_cells_per_s": last["single_core_cells_per_s"]},
         "e2e": {"value": v, "unit": "cells/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -325,7 +388,7 @@ def run_reference(args, rank, world):
 
 def load_operator(opfile, device=0):
     """The reference-built cache; for config 4 (N=L=16, a multi-hour CPU build
-    that is not shipped) fall back to assembling it on the GPU (rbuild)."""
+    that is not always shipped) fall back to assembling it on the GPU (rbuild)."""
     from paper_2605_28475_b200.operator import SpectralConfig, load_cache
 
     path = os.path.join(ROOT, "operators", opfile + ".bfct")
@@ -417,25 +480,62 @@ def run_ours(args, rank, world, local_rank):
     import torch
 
     from paper_2605_28475_b200 import dist as bdist
-    from paper_2605_28475_b200 import engine
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    dry = args.dry_run
+    dev = torch.device("cpu") if dry else torch.device("cuda", local_rank)
+    if not dry:
+        torch.cuda.set_device(local_rank)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
-    opfile, n_cells, _, desc = CONFIGS[args.config]
+        if args.backend == "nccl":
+            # the communicator lines (nranks, NVLS/NVLink transport) go to stderr
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
+    opfile, n_global, _, desc, psample = CONFIGS[args.config]
     if args.cells:
-        n_cells = args.cells
+        n_global = args.cells
+    strong = args.scaling == "strong"
+    if strong:  # one fixed global batch, contiguous equal shards
+        start, n_cells = bdist.shard_range(n_global, world, rank)
+        total_cells = n_global
+    else:  # every rank evaluates its own n_global cells
+        start, n_cells = rank * n_global, n_global
+        total_cells = n_global * world
+
+    def gather(vals):
+        """Per-rank float values -> list over ranks (all ranks)."""
+        t = torch.tensor([float(v) for v in vals], dtype=torch.float64, device=dev)
+        if dist is None:
+            return [t.tolist()]
+        out = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(out, t)
+        return [o.tolist() for o in out]
+
+    if dry:  # launcher / sharding / collective plumbing only (CPU test): no kernels, no timing
+        shards = gather([start, n_cells])
+        diag = bdist.allreduce_diagnostics(torch.tensor([0.0] * 5 + [float(n_cells), float(start)],
+                                                        dtype=torch.float64))
+        if rank == 0:
+            print(json.dumps({"dry_run": True, "n_gpus": world, "scaling": args.scaling, "backend": args.backend,
+                              "global_cells": total_cells, "shards": [[int(a), int(b)] for a, b in shards],
+                              "diag_cells": float(diag[5])}), flush=True)
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+
+    from paper_2605_28475_b200 import engine
+
     op = load_operator(opfile, local_rank)
     if getattr(op, "_built_on_gpu", False):
         desc += " [operator assembled on this GPU by bfr_assemble: reference build not present]"
     plan = engine.plan_for(op, local_rank)
     cfg = op.cfg
-    host = make_cells(args.config, cfg.n_k, cfg.l_max, n_cells, seed=args.seed, start=rank * n_cells,
-                      device=local_rank)
+    host = make_cells(args.config, cfg.n_k, cfg.l_max, n_cells, seed=args.seed, start=start, device=local_rank)
     f = torch.from_numpy(host).to(dev)
     q = torch.empty_like(f)
     stream = torch.cuda.current_stream(dev)
@@ -462,9 +562,8 @@ def run_ours(args, rank, world, local_rank):
     # Inputs (+ outputs) smaller than L2: flush L2 between timed steps by
     # writing a 256 MB buffer outside the per-step events; the step time is
     # then the sum of the per-step event intervals.
-    l2_bytes = 132644864
     flush = None
-    if 2 * host.nbytes < 2 * l2_bytes and not rk4:
+    if 2 * host.nbytes < 2 * L2_BYTES and not rk4:
         flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -482,59 +581,104 @@ def run_ours(args, rank, world, local_rank):
         barrier()
         wall = time.perf_counter() - t0
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    total_ms = sum(step_ms) if flush is not None else starts[0].elapsed_time(ends[-1])
+    local_ms = sum(step_ms) if flush is not None else starts[0].elapsed_time(ends[-1])
     q_per_step = 4 if rk4 else 1
-    # whole-job rate: cells of all ranks / the slowest rank's device time
-    value, total_ms = bdist.weak_scaling_rate(n_cells, args.steps * q_per_step, total_ms, device=dev)
+    per_rank = gather([local_ms, n_cells, start])
+    total_ms = max(r[0] for r in per_rank)  # the job ends with the slowest rank
+    value = total_cells * args.steps * q_per_step / (total_ms / 1e3)
     ms_per_step = total_ms / args.steps
 
-    # conservation diagnostics of the last step, all-reduced (max |production|,
-    # or for RK4 the max drift of the invariants from the initial state)
+    # conservation diagnostics, all-reduced over NCCL after the timed region
     mom = torch.empty((n_cells, 5), dtype=torch.float64, device=dev)
     if rk4:
         mom0 = torch.empty_like(mom)
         plan.moments_device(f.data_ptr(), mom0.data_ptr(), n_cells, stream.cuda_stream)
         plan.moments_device(y.data_ptr(), mom.data_ptr(), n_cells, stream.cuda_stream)
-        mom = mom - mom0
+        mom = mom - mom0  # drift of the invariants over the run
         if int(flag.item()):
             raise RuntimeError("RK4 diverged")
+        out_t = y
     else:
         plan.moments_device(q.data_ptr(), mom.data_ptr(), n_cells, stream.cuda_stream)
-    diag = mom.abs().amax(dim=0)
+        out_t = q
+    diag = bdist.as_dict(bdist.allreduce_diagnostics(bdist.diagnostics_vector(mom, out_t)))
+    slots_exact = bool((q[:, 0, : min(4, cfg.n_q)] == 0).all() and (cfg.n_k < 2 or (q[:, 1, 0] == 0).all())) \
+        if not rk4 else None
+    ok = torch.tensor([1.0 if (slots_exact is None or slots_exact) else 0.0], dtype=torch.float64, device=dev)
     if dist is not None:
-        dist.all_reduce(diag, op=dist.ReduceOp.MAX)
-    conservation_max = float(diag.max().item())
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
 
-    # end-to-end through the C ABI with host buffers (pinned), copies timed
+    # end to end through the C ABI with host buffers, copies inside the timed region
     e2e = None
-    if args.e2e_steps > 0 and not rk4:
-        hin = torch.from_numpy(host).pin_memory()
-        hout = torch.empty_like(hin).pin_memory()
+    if args.e2e_steps != 0 and not rk4:
         from paper_2605_28475_b200 import _lib
 
         lib = _lib.lib()
-        lib.bfq_eval_host(plan.handle, hin.data_ptr(), None, hout.data_ptr(), n_cells)  # warm
+        e2e_steps = args.steps if args.e2e_steps < 0 else args.e2e_steps
+        hin = torch.from_numpy(host).pin_memory()
+        hout = torch.empty_like(hin).pin_memory()
+        _lib.check(lib.bfq_eval_host(plan.handle, hin.data_ptr(), None, hout.data_ptr(), n_cells))  # warm
         barrier()
-        walls = []
-        for _ in range(args.e2e_steps):
-            t0 = time.perf_counter()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
             _lib.check(lib.bfq_eval_host(plan.handle, hin.data_ptr(), None, hout.data_ptr(), n_cells))
-            walls.append(time.perf_counter() - t0)
-        # wall clock of the blocking host call (copies in the timed region), median step
-        el = torch.tensor([statistics.median(walls) * args.e2e_steps], dtype=torch.float64, device=dev)
-        if dist is not None:
-            dist.all_reduce(el, op=dist.ReduceOp.MAX)
+        el = time.perf_counter() - t0
+        # pageable numpy buffers (staged through the plan's pinned chunks)
+        pout = np.empty_like(host)
+        n_pg = min(3, e2e_steps)
+        t0 = time.perf_counter()
+        for _ in range(n_pg):
+            _lib.check(lib.bfq_eval_host(plan.handle, host.ctypes.data, None, pout.ctypes.data, n_cells))
+        el_pg = time.perf_counter() - t0
+        same_bits = bool(np.array_equal(pout, hout.numpy()))
+        els = gather([el, el_pg])
+        el, el_pg = max(r[0] for r in els), max(r[1] for r in els)
         bytes_ = n_cells * cfg.n_dof * 8
-        e2e = {"value": n_cells * world * args.e2e_steps / float(el.item()), "unit": "cells/s",
-               "h2d_bytes_per_step": bytes_, "d2h_bytes_per_step": bytes_, "steps": args.e2e_steps,
-               "path": "bfq_eval_host (C ABI, pinned host buffers, chunked H2D/Q/D2H pipeline)"}
+        e2e = {"value": total_cells * e2e_steps / el, "unit": "cells/s",
+               "h2d_bytes_per_step": bytes_, "d2h_bytes_per_step": bytes_, "steps": e2e_steps,
+               "path": "bfq_eval_host (C ABI, pinned host buffers, chunked H2D/Q/D2H pipeline over 3 streams)",
+               "pageable": {"value": total_cells * n_pg / el_pg, "steps": n_pg, "bitwise_equal_to_pinned": same_bits,
+                            "path": "bfq_eval_host on pageable numpy buffers (staged through pinned chunks)"}}
+
+    # parity of the timed batch's own outputs against the CPU oracle (rank 0's shard)
+    parity, cpu = None, None
+    if rank == 0 and not args.no_parity and not rk4:
+        from oracle import q_oracle
+        from paper_2605_28475_b200.operator import save_cache
+
+        oppath = os.path.join(ROOT, "operators", opfile + ".bfct")
+        if getattr(op, "_built_on_gpu", False):  # the CPU port reads the same (GPU-built) operator
+            import tempfile
+
+            oppath = os.path.join(tempfile.mkdtemp(), opfile + ".bfct")
+            save_cache(oppath, op)
+        k = psample if args.parity_cells < 0 else args.parity_cells
+        idx = stratified_indices(n_cells, k)
+        qs = q[torch.from_numpy(idx).to(dev)].cpu().numpy()
+        ref, cpu = oracle_pool(oppath, host[idx])
+        errs = np.array([q_oracle.rel_err(qs[i], ref[i]) for i in range(len(idx))])
+        worst = int(np.argmax(errs)) if len(idx) else 0
+        parity = {"cells": int(len(idx)), "of": int(n_cells), "max_rel_err": float(errs.max()) if len(idx) else None,
+                  "worst_cell": int(idx[worst]) if len(idx) else None, "bar": 1e-12,
+                  "pass": bool(len(idx) and errs.max() <= 1e-12),
+                  "selection": "every cell" if len(idx) == n_cells else
+                  "stratified: evenly spread over the shard incl. first/last cell and the last tile",
+                  "metric": "max|Q_gpu - Q_oracle| / max|Q_oracle| per cell (test_contraction.py:63-65)",
+                  "invariant_slots_exact": bool(ok.item() == 1.0)}
+    elif rk4:
+        parity = {"skipped": "RK4 trajectory parity is tests/test_gpu_rk4.py (reference golden, every 100th step)",
+                  "moment_drift_max": max(diag[k] for k in ("max_mass", "max_px", "max_py", "max_pz", "max_energy"))}
+    if dist is not None:
+        dist.barrier()
 
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
         return
     flops_cell, bytes_cell = plan.flops_per_cell, plan.bytes_per_cell
-    achieved = flops_cell * n_cells * q_per_step / (statistics.mean(step_ms) / 1e3) / 1e12
+    kern_s = statistics.mean(step_ms) / 1e3
+    achieved = flops_cell * n_cells * q_per_step / kern_s / 1e12
+    exec_tf = 2.0 * plan.info["exec_macs_per_cell"] * n_cells * q_per_step / kern_s / 1e12
     traffic = None
     tpath = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
     if os.path.exists(tpath):
@@ -544,48 +688,55 @@ def run_ours(args, rank, world, local_rank):
             traffic = None
     line = {
         "metric": METRIC, "value": value, "unit": "cells/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.json distributions)",
-        "config": {"workload": desc, "operator": opfile, "cells_per_gpu": n_cells, "global_cells": n_cells * world,
-                   "parallelism": f"cells sharded over {world} GPU(s), no data-path collective",
+        "config": {"workload": desc, "operator": opfile, "global_cells": total_cells, "cells_per_rank": n_cells,
+                   "parallelism": f"{'one fixed batch' if strong else 'one batch per GPU'} sharded over {world} "
+                                  "GPU(s), contiguous blocks, no data-path collective",
                    "l2": ("L2 flushed between timed steps (256 MB write outside the step events; inputs "
                           "%.3f GB per GPU < 126 MB L2)" % (host.nbytes / 1e9)) if flush is not None else
                          ("inputs larger than L2 (%.2f GB per GPU vs 126 MB)" % (host.nbytes / 1e9)),
                    "seed": args.seed},
+        "rank_ms": [r[0] for r in per_rank],
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
+                     "kernel": "bfq_q_kernel2 (fused stages 1-3, DMMA.8x8x4)",
                      "peak_source": "measured FP64 DMMA.8x8x4 sustained (profiles/fp64_peak.txt); "
                                     "MEASURED_PEAKS.json has no fp64 entry",
-                     "flops_per_cell": flops_cell, "exec_dmma_macs_per_cell": plan.info["exec_macs_per_cell"],
-                     "hbm_frac": bytes_cell * n_cells / (statistics.mean(step_ms) / 1e3) / 1e9
-                     / measured_peaks().get("hbm_gbs", 6456.5)},
+                     "nominal_peak": FP64_NOMINAL_TFLOPS, "nominal_frac": achieved / FP64_NOMINAL_TFLOPS,
+                     "flops_per_cell": flops_cell,
+                     "exec_dmma_macs_per_cell": plan.info["exec_macs_per_cell"],
+                     "exec_tflops": exec_tf, "exec_frac": exec_tf / FP64_PEAK_TFLOPS,
+                     "hbm_frac": bytes_cell * n_cells / kern_s / 1e9 / measured_peaks().get("hbm_gbs", 6548.2)},
         "e2e": e2e,
-        "gpu_launches": args.steps * (7 if rk4 else 1),
+        "gpu_launches": args.steps * (11 if rk4 else 1),
         "clocks": clk.summary(),
-        "conservation_max_abs": conservation_max,
+        "parity": parity,
+        "conservation": {"invariant_slots_exact": bool(ok.item() == 1.0), **diag},
         "wall_s": wall,
     }
     if rk4:
         line["rk4"] = {"dt": 0.01, "steps_per_s": args.steps / (total_ms / 1e3),
-                       "full_run_estimate_s": 1000 * ms_per_step / 1e3,
-                       "moment_drift_max": conservation_max}
-    if world == 1 and not args.no_cpu:
-        oppath = None
-        if getattr(op, "_built_on_gpu", False):  # the CPU port reads the same (GPU-built) operator
-            import tempfile
-
-            from paper_2605_28475_b200.operator import save_cache
-
-            oppath = os.path.join(tempfile.mkdtemp(), opfile + ".bfct")
-            save_cache(oppath, op)
-        cpu = cpu_port_rate(args.config, host[:256], budget_s=args.cpu_budget, path=oppath)
-        line["cpu_baseline"] = {"value": cpu["value"], "unit": "cells/s", "cores": cpu["cores"], "kind": "port",
-                                "sample": f"{cpu['cells']} cells of the same batch, ~{args.cpu_budget:.0f} s per core "
-                                          "(oracle/q_oracle.py: the reference's q_angular_first operations, bit-identical to it and "
-                                          "the same speed per cell, profiles/r01_cpu_ref_vs_port.txt; 1 thread per process)"}
+                       "full_run_estimate_s": 1000 * ms_per_step / 1e3}
+    if world == 1 and cpu is not None:
+        line["cpu_baseline"] = {
+            "value": cpu["value"], "unit": "cells/s", "cores": cpu["cores"], "kind": "port",
+            "sample": f"the {cpu['cells']} parity cells of the timed batch, contiguous blocks over {cpu['cores']} "
+                      f"processes (1 thread each), ~{cpu['busy_s']:.1f} s per process (oracle/q_oracle.py: the "
+                      "reference's q_angular_first operations, bit-identical to it and the same speed per cell, "
+                      "profiles/r01_cpu_ref_vs_port.txt)",
+            "cpu": cpu_model(), "single_core_cells_per_s": cpu["single_core_cells_per_s"]}
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+
+
+def launch_ranks(args):
+    """``--gpus N`` outside torchrun: re-run this script under
+    torch.distributed.run with N local ranks; rank 0 prints the line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd, env=dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1")))
 
 
 def main():
@@ -595,12 +746,23 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="hs12", choices=sorted(CONFIGS) + sorted(RBUILD))
-    ap.add_argument("--cells", type=int, default=0, help="override cells per GPU")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: one fixed global batch sharded over the GPUs (BASELINE config 3); "
+                         "weak: the batch per GPU")
+    ap.add_argument("--cells", type=int, default=0, help="override the global batch (strong) / per-GPU batch (weak)")
     ap.add_argument("--seed", type=int, default=20260520)
-    ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--cpu-budget", type=float, default=10.0, help="seconds of per-core CPU work per sample")
-    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=-1, help="-1: as many as --steps; 0: skip")
+    ap.add_argument("--parity-cells", type=int, default=-1, help="-1: the config's default sample; 0: every cell")
+    ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=3.0, help="reference arm: seconds of work per core per step")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle leg (parity and cpu_baseline)")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--dry-run", action="store_true", help="launcher/sharding/collective plumbing only (no GPU)")
     args = ap.parse_args()
+    if args.no_cpu:
+        args.no_parity = True
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(launch_ranks(args))
     world = env_int("WORLD_SIZE", 1)
     rank = env_int("RANK", 0)
     local_rank = env_int("LOCAL_RANK", 0)

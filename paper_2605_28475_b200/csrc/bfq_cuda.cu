@@ -98,7 +98,8 @@ __global__ void moments_kernel(const double* c, double* out, long long n_cells, 
   o[1] = px;
   o[2] = py;
   o[3] = pz;
-  o[4] = 0.5 * (3.0 * mass + (-2.449489742783178) * e2);
+  // separately rounded, in the reference's order (no FMA contraction): bitwise equal
+  o[4] = __dmul_rn(0.5, __dadd_rn(__dmul_rn(3.0, mass), __dmul_rn(-2.449489742783178, e2)));
 }
 
 // RK4 stage helpers (harness.py:97-102).  Stage argument y + a*k is formed

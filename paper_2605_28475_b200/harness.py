@@ -7,10 +7,12 @@ an ``EvolutionTrace`` whose ``moment_drift()`` is the largest deviation of
 mass/momentum/energy from the start (harness.py:55-76).
 
 The batched form keeps the whole (B, n_k, n_q) state on the device; one step is
-four Q launches plus three fused stage kernels (``bfq_rk4_step``).  The
-divergence flag is read back only at record steps (and at the end), so the
-step loop never synchronises; a non-finite state is reported at the first
-record step after it appears, with the step index of that check.
+four Q launches plus the stage kernels (``bfq_rk4_step``).  Every step's
+divergence check runs on the device into its own flag slot (one int32 per
+step between records), and the flags are read back at record steps (and at the
+end), so the step loop never synchronises; the ``RuntimeError`` then names the
+exact first step whose state was not finite, with the reference's message
+(harness.py:103-107).
 """
 
 from __future__ import annotations
@@ -76,7 +78,7 @@ def rk4_integrate_batch(op, c0, dt: float, n_steps: int, record_every: int = 1, 
         raise ValueError(f"state must have shape (B, {plan.n_k}, {plan.n_q})")
     b = y.shape[0]
     work = torch.empty((3,) + tuple(y.shape), dtype=torch.float64, device=dev)
-    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    flags = torch.zeros(max(1, int(record_every)), dtype=torch.int32, device=dev)  # one slot per step
     mom = torch.empty((b, 5), dtype=torch.float64, device=dev)
     watch = np.arange(min(b, 4)) if watch is None else np.asarray(watch, dtype=np.int64)
     widx = torch.as_tensor(watch, device=dev)
@@ -91,12 +93,18 @@ def rk4_integrate_batch(op, c0, dt: float, n_steps: int, record_every: int = 1, 
         snaps.append(y.index_select(0, widx).cpu().numpy())
 
     record(0.0)
+    last = 0  # step of the previous record
     for step in range(1, n_steps + 1):
-        plan.rk4_step_device(y.data_ptr(), work.data_ptr(), b, dt, flag.data_ptr(), stream)
+        slot = flags.data_ptr() + 4 * (step - last - 1)
+        plan.rk4_step_device(y.data_ptr(), work.data_ptr(), b, dt, slot, stream)
         if step % record_every == 0 or step == n_steps:
-            if int(flag.item()):
-                raise RuntimeError(f"integration diverged by step {step} (t={step * dt:.4g}); "
+            bad = torch.nonzero(flags[:step - last]).flatten()
+            if bad.numel():
+                first = last + 1 + int(bad[0])
+                raise RuntimeError(f"integration diverged at step {first} (t={first * dt:.4g}); "
                                    "reduce dt below the stability bound")
+            flags.zero_()
+            last = step
             record(step * dt)
     return BatchTrace(np.array(times), np.stack(moms), watch, np.stack(snaps), y)
 

@@ -329,3 +329,53 @@ def test_n16_config4_on_gpu_built_operator():
     q12 = run(op, d["c1"][None], d["c2"][None])[0]
     assert q_oracle.rel_err(q12, q_oracle.q_angular_first(oop, d["c1"], d["c2"])) <= TOL
     assert q_oracle.rel_err(q12, d["q12"]) <= 5e-9
+
+
+def test_output_overlapping_input_is_rejected():
+    """CTAs of a tile still read its cells while others write Q, so
+    in-place / overlapping outputs are refused (wrapper and C ABI)."""
+    from paper_2605_28475_b200 import _lib
+
+    op = load_op("hs_n4")
+    cfg = op.cfg
+    f = gpu(inputs.perturbed_maxwellians(cfg.n_k, cfg.l_max, 16, seed=2))
+    with pytest.raises(ValueError, match="overlap"):
+        engine.evaluate_batch(op, f, out=f)
+    big = torch.zeros((17, cfg.n_k, cfg.n_q), dtype=torch.float64, device="cuda")
+    big[:16] = f
+    with pytest.raises(ValueError, match="overlap"):
+        engine.evaluate_batch(op, big[:16], out=big[1:])
+    f3 = f.clone()
+    with pytest.raises(ValueError, match="overlap"):
+        engine.evaluate_batch(op, f, f3, out=f3)
+    plan = engine.plan_for(op)
+    lib = _lib.lib()
+    st = torch.cuda.current_stream().cuda_stream
+    assert lib.bfq_eval(plan.handle, f.data_ptr(), None, f.data_ptr() + 8 * cfg.n_dof, 16, st) == _lib.BFQ_EINVAL
+    assert b"overlap" in lib.bfq_last_error()
+    h = np.zeros((16, cfg.n_k, cfg.n_q))
+    assert lib.bfq_eval_host(plan.handle, h.ctypes.data, None, h.ctypes.data, 16) == _lib.BFQ_EINVAL
+    # disjoint buffers still work, and the result did not change
+    out = engine.evaluate_batch(op, f)
+    assert np.array_equal(out.cpu().numpy(), run(op, f.cpu().numpy()))
+
+
+def test_host_path_pinned_and_pageable_agree():
+    """bfq_eval_host: pinned buffers are copied asynchronously, pageable ones
+    staged through the plan's pinned chunks; both equal the device path."""
+    op = load_op("hs_n8")
+    cfg = op.cfg
+    cells = inputs.perturbed_maxwellians(cfg.n_k, cfg.l_max, 1000, seed=13)
+    dev = run(op, cells)
+    pageable = engine.evaluate_host(op, cells)
+    assert np.array_equal(pageable, dev)
+    from paper_2605_28475_b200 import _lib
+
+    hin = torch.from_numpy(cells).pin_memory()
+    hout = torch.empty_like(hin).pin_memory()
+    _lib.check(_lib.lib().bfq_eval_host(engine.plan_for(op).handle, hin.data_ptr(), None, hout.data_ptr(), 1000))
+    assert np.array_equal(hout.numpy(), dev)
+    # mixed: pinned input, pageable output
+    out = np.empty_like(cells)
+    _lib.check(_lib.lib().bfq_eval_host(engine.plan_for(op).handle, hin.data_ptr(), None, out.ctypes.data, 1000))
+    assert np.array_equal(out, dev)

@@ -20,6 +20,15 @@ from paper_2605_28475_b200 import harness, inputs  # noqa: E402
 from paper_2605_28475_b200.operator import CoefficientField  # noqa: E402
 
 
+def oracle_rk4_step(oop, y, dt):
+    rhs = lambda v: q_oracle.q_angular_first(oop, v)  # noqa: E731
+    k1 = rhs(y)
+    k2 = rhs(y + 0.5 * dt * k1)
+    k3 = rhs(y + 0.5 * dt * k2)
+    k4 = rhs(y + dt * k3)
+    return y + (dt / 6.0) * (k1 + 2.0 * k2 + 2.0 * k3 + k4)
+
+
 def oracle_rk4(op, y, dt, n):
     oop = q_oracle.OracleOperator.from_operator(op)
     rhs = lambda v: q_oracle.q_angular_first(oop, v)  # noqa: E731
@@ -63,6 +72,21 @@ def test_rk4_divergence_raises():
     c0[2] *= 1e150
     with pytest.raises(RuntimeError, match="diverged"):
         harness.rk4_integrate_batch(op, c0, 1.0, 3)
+    # the exact first non-finite step, as the reference reports it
+    # (harness.py:103-107): cell 2 scaled by 1e20 overflows in step 2 (oracle RK4)
+    c0 = inputs.perturbed_maxwellians(op.cfg.n_k, op.cfg.l_max, 4, seed=1)
+    c0[2] *= 1e20
+    oop = q_oracle.OracleOperator.from_operator(op)
+    y, first = c0[2].copy(), None
+    with np.errstate(all="ignore"):
+        for step in range(1, 8):
+            y = oracle_rk4_step(oop, y, 1.0)
+            if not np.all(np.isfinite(y)):
+                first = step
+                break
+    assert first == 2
+    with pytest.raises(RuntimeError, match=f"diverged at step {first} "):
+        harness.rk4_integrate_batch(op, c0, 1.0, 7, record_every=5)
 
 
 def test_rk4_config5_operator():
