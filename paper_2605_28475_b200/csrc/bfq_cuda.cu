@@ -35,12 +35,12 @@
 namespace bfq {
 typedef void (*QKernel)(const KParams);
 // per-size instantiation units (bfq_inst_*.cu)
-QKernel pick_n5(bool, int, int);
-QKernel pick_n9(bool, int, int);
-QKernel pick_n11(bool, int, int);
-QKernel pick_n13(bool, int, int);
-QKernel pick_n17(bool, int, int);
-QKernel pick_generic(bool, int, int);
+QKernel pick_n5(bool, bool, int, int);
+QKernel pick_n9(bool, bool, int, int);
+QKernel pick_n11(bool, bool, int, int);
+QKernel pick_n13(bool, bool, int, int);
+QKernel pick_n17(bool, bool, int, int);
+QKernel pick_generic(bool, bool, int, int);
 }  // namespace bfq
 
 using namespace bfq;
@@ -70,17 +70,17 @@ struct DevProgram {
 
 unsigned long long* bfq_dbg_clk_ptr = nullptr;  // BFQ_DEBUG bit 3 only
 
-QKernel pick_kernel(bool bilin, int mt, int cells, int nk, int qs) {
+QKernel pick_kernel(bool bilin, bool ps, int mt, int cells, int nk, int qs) {
   QKernel k = nullptr;
   if (!std::getenv("BFQ_GENERIC")) {
-    if (nk == 13 && qs == 172) k = pick_n13(bilin, mt, cells);
-    else if (nk == 9 && qs == 84) k = pick_n9(bilin, mt, cells);
-    else if (nk == 11 && qs == 124) k = pick_n11(bilin, mt, cells);
-    else if (nk == 5 && qs == 28) k = pick_n5(bilin, mt, cells);
-    else if (nk == 17 && qs == 292) k = pick_n17(bilin, mt, cells);
+    if (nk == 13 && qs == 172) k = pick_n13(bilin, ps, mt, cells);
+    else if (nk == 9 && qs == 84) k = pick_n9(bilin, ps, mt, cells);
+    else if (nk == 11 && qs == 124) k = pick_n11(bilin, ps, mt, cells);
+    else if (nk == 5 && qs == 28) k = pick_n5(bilin, ps, mt, cells);
+    else if (nk == 17 && qs == 292) k = pick_n17(bilin, ps, mt, cells);
     if (k) return k;
   }
-  return pick_generic(bilin, mt, cells);
+  return pick_generic(bilin, ps, mt, cells);
 }
 
 // ------------------------------------------------------------ small kernels
@@ -152,6 +152,7 @@ struct bfq_plan {
   int* sstart = nullptr;
   DevProgram sym, full;
   size_t operator_bytes = 0;
+  int* chk = nullptr;  // checked builds: violation record (KParams::chk)
 };
 
 namespace {
@@ -178,7 +179,7 @@ int upload_program(const Program& pg, DevProgram& dp, size_t& total, int smem_op
   if ((rc = upload(pg.groups, &dp.groups, total))) return rc;
   if ((rc = upload(pg.unit_m1, &dp.unit_m1, total))) return rc;
   if ((rc = upload(pg.items, &dp.items, total))) return rc;
-  QKernel k = pick_kernel(pg.bilinear, pg.cfg.mt, pg.cfg.cells, nk, qs);
+  QKernel k = pick_kernel(pg.bilinear, pg.cfg.pairsplit != 0, pg.cfg.mt, pg.cfg.cells, nk, qs);
   if (!k) {
     set_error("no kernel instantiation for this tiling");
     return BFQ_EINVAL;
@@ -221,6 +222,8 @@ int launch_q(const bfq_plan* plan, const DevProgram& dp, const double* f2, const
   }
   p.R = plan->R;
   p.rows = plan->rows;
+  p.n_rows = (long long)hp.rows.size();
+  p.chk = plan->chk;
   p.sstart = plan->sstart;
   p.chans = dp.chans;
   p.groups = dp.groups;
@@ -325,6 +328,10 @@ int plan_from_desc(const bfq_desc* desc, int device, bfq_plan** out) {
     return rc;
   }
   plan->operator_bytes = total;
+  if (kChecked) {
+    BFQ_CUDA_TRY(cudaMalloc(&plan->chk, 8 * sizeof(int)));
+    BFQ_CUDA_TRY(cudaMemset(plan->chk, 0, 8 * sizeof(int)));
+  }
   // host copies of the bulk data are no longer needed
   std::vector<double>().swap(plan->hp.rblocks);
   *out = plan.release();
@@ -356,6 +363,7 @@ int bfq_plan_destroy(bfq_plan* plan) {
     cudaFree(plan->R);
     cudaFree(plan->rows);
     cudaFree(plan->sstart);
+    cudaFree(plan->chk);
     free_program(plan->sym);
     free_program(plan->full);
     if (plan->host) {
@@ -644,6 +652,19 @@ const char* bfq_strerror(int code) {
 }
 
 const char* bfq_last_error(void) { return get_error().c_str(); }
+
+// Checked builds only (libbfq_checked.so): copy out and reset the first
+// recorded violation {code, block, thread, aux, count}; returns BFQ_EINVAL in
+// an unchecked build.  Synchronises the plan's device.
+extern "C" int bfq_debug_check_status(const bfq_plan* plan, int* out5);
+int bfq_debug_check_status(const bfq_plan* plan, int* out5) {
+  if (!plan || !out5 || !plan->chk) return BFQ_EINVAL;
+  DeviceGuard guard(plan->device);
+  BFQ_CUDA_TRY(cudaDeviceSynchronize());
+  BFQ_CUDA_TRY(cudaMemcpy(out5, plan->chk, 5 * sizeof(int), cudaMemcpyDeviceToHost));
+  BFQ_CUDA_TRY(cudaMemset(plan->chk, 0, 8 * sizeof(int)));
+  return BFQ_OK;
+}
 
 // Debug only (BFQ_DEBUG bit 3): copy out and reset the per-phase cycle totals.
 extern "C" int bfq_debug_phase_clocks(unsigned long long* out8);

@@ -33,7 +33,73 @@ struct KParams {
   int hdr, max_chan, nteams;
   int debug;  // timing experiments only (BFQ_DEBUG): bit0 skip stage 1, bit1 skip stage 2, bit3 phase clocks
   unsigned long long* dbg_clk;  // [8] phase cycle totals when bit3 set
+  long long n_rows;  // table rows (incl. padding) -- bounds of the row stream
+  int* chk;          // BFQ_CHECKED builds: first violation {code, block, thread, aux, count}
 };
+
+// ------------------------------------------------------------ checked build
+// -DBFQ_CHECKED (libbfq_checked.so, tests/test_gpu_checked.py): every shared
+// memory access of the Q kernel is checked against the sub-buffer it belongs
+// to (staged cells of this warp, this unit's Phi rows, this team's R slot),
+// every table row index against the table, every Q store against the
+// output; mbarrier waits time out instead of hanging; the first violation is
+// recorded in p.chk (and the access clamped into its buffer, so the kernel
+// finishes and the host can read the record).  The race canaries (R-slot and
+// Phi poisoning, randomized delays) live in the kernel itself.
+enum CheckCode {
+  CHK_F2 = 1,      // stage-1 gather of g f2[a, q2] outside this warp's staged cells
+  CHK_F3 = 2,      // stage-1 gather of f3[b, q3]
+  CHK_PHI_ST = 3,  // Phi store outside this warp's Phi row
+  CHK_PHI_LD = 4,  // stage-2 Phi load outside this unit's Phi buffer
+  CHK_RING = 5,    // stage-2 R load outside this team's ring slot
+  CHK_XCH = 6,     // epilogue exchange outside this unit's buffer
+  CHK_ROW = 7,     // table row index outside the table
+  CHK_Q = 8,       // Q store outside the output
+  CHK_ZERO = 9,    // an invariant slot computed non-zero before the epilogue forced it
+  CHK_HANG = 10,   // mbarrier wait timed out (ring never filled)
+};
+
+#ifdef BFQ_CHECKED
+static __device__ __noinline__ void chk_fail(const KParams& p, int code, long long aux) {
+  if (atomicAdd(p.chk + 4, 1) == 0) {
+    p.chk[0] = code;
+    p.chk[1] = (int)blockIdx.x;
+    p.chk[2] = (int)threadIdx.x;
+    p.chk[3] = (int)aux;
+  }
+}
+__device__ __forceinline__ uint32_t chk_range(const KParams& p, uint32_t addr, uint32_t lo, uint32_t hi, int code) {
+  if (addr < lo || addr + 8u > hi || (addr & 7u)) {
+    chk_fail(p, code, (long long)addr);
+    return lo;
+  }
+  return addr;
+}
+__device__ __forceinline__ long long chk_index(const KParams& p, long long i, long long n, int code) {
+  if (i < 0 || i >= n) {
+    chk_fail(p, code, i);
+    return 0;
+  }
+  return i;
+}
+// pseudo-random delay (0..1023 ns) of a warp at a schedule point
+__device__ __forceinline__ void chk_jitter(unsigned salt) {
+  unsigned h = (blockIdx.x * 0x9E3779B9u) ^ ((threadIdx.x >> 5) * 0x85EBCA6Bu) ^ (salt * 0xC2B2AE35u);
+  h ^= h >> 15;
+  h *= 0x2C1B3C6Du;
+  h ^= h >> 12;
+  __nanosleep(h & 1023u);
+}
+#define BFQ_CHK(addr, lo, hi, code) chk_range(p, (addr), (lo), (hi), (code))
+#define BFQ_CHK_IDX(i, n, code) chk_index(p, (i), (n), (code))
+#define BFQ_JITTER(salt) chk_jitter(salt)
+constexpr bool kChecked = true;
+#else
+#define BFQ_CHK(addr, lo, hi, code) (addr)
+#define BFQ_CHK_IDX(i, n, code) (i)
+#define BFQ_JITTER(salt) ((void)0)
+constexpr bool kChecked = false;
+#endif
 
 // CTA -> (item, tile).  Tiles are taken in chunks of TILE_CHUNK; inside a
 // chunk the CTAs run item-major (heavy items first), so all items of a tile
@@ -119,6 +185,33 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       "}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+}
+
+// Checked builds: a bounded wait (~seconds) that records CHK_HANG instead of
+// hanging the GPU when a ring slot is never filled.
+__device__ __forceinline__ void mbar_wait_chk(const KParams& p, uint64_t* bar, unsigned parity) {
+#ifdef BFQ_CHECKED
+  for (long long it = 0;; ++it) {
+    uint32_t ok;
+    asm volatile(
+        "{\n"
+        " .reg .pred q;\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2, 100000;\n"
+        " selp.u32 %0, 1, 0, q;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if (it > (1LL << 22)) {
+      chk_fail(p, CHK_HANG, (long long)parity);
+      return;
+    }
+  }
+#else
+  (void)p;
+  mbar_wait(bar, parity);
+#endif
 }
 
 // Non-blocking probe of an mbarrier phase.

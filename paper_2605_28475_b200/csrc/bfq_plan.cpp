@@ -56,8 +56,9 @@ static bool choose_config(int nk, int qs, int k2s, int nf, int smem_limit, int m
   // bfq_qkernel2.cuh), leaving one 8x8 tile per cell, so it takes 8 cells per tile
   int max_cells = c.mt == 1 ? 8 : (c.mt == 2 ? 4 : 2);
   if (nk == 9 && qs == 84 && !std::getenv("BFQ_GENERIC") && !std::getenv("BFQ_NO_X1_CELLS8")) max_cells = 8;
-  int force_cells = 0;
+  int force_cells = 0, kernel = 2;
   if (const char* e = std::getenv("BFQ_CELLS")) force_cells = std::atoi(e);
+  if (const char* e = std::getenv("BFQ_KERNEL")) kernel = std::atoi(e);
   c.hdr = header_bytes(max_chan);
   c.max_chan = max_chan;
   // Pair-split kernel first: 8 units x 2 warps (4 compute warps per
@@ -77,7 +78,7 @@ static bool choose_config(int nk, int qs, int k2s, int nf, int smem_limit, int m
   // the other CTA's work (measured +2.6% at N=L=8 and N=L=10).
   static const int popts2[][4] = {{8, 4, 1, 4}, {8, 4, 1, 3}, {8, 4, 1, 2}, {4, 4, 1, 4}, {4, 4, 1, 3}, {4, 4, 1, 2}};
   const long half_sm = (233472L - 2 * 1024) / 2;  // 228 KB per SM, 1 KB reserved per CTA
-  if (!force_stages && (!force_units || force_units == 4) && nk != 17 &&
+  if (kernel == 2 && !force_stages && (!force_units || force_units == 4) && nk != 17 &&
       !std::getenv("BFQ_ONE_CTA")) {
     for (auto o0 : popts2) {
       int o[4] = {o0[0], o0[1], o0[2], force_teams ? force_teams : o0[3]};
@@ -97,7 +98,7 @@ static bool choose_config(int nk, int qs, int k2s, int nf, int smem_limit, int m
       return true;
     }
   }
-  {
+  if (kernel == 2) {
     for (auto o0 : popts) {
       int o[4] = {o0[0], o0[1], force_stages ? force_stages : o0[2], force_teams ? force_teams : o0[3]};
       if (force_cells && o[0] != force_cells) continue;
@@ -117,6 +118,28 @@ static bool choose_config(int nk, int qs, int k2s, int nf, int smem_limit, int m
       c.pairsplit = 1;
       return true;
     }
+  }
+  // Single-warp-per-unit kernel (bfq_qkernel.cuh): only when no pair-split
+  // shape fits (e.g. the bilinear Q(f2,f3) program at n_k = 17, whose two
+  // staged arrays leave no room for two cells), or forced by BFQ_KERNEL=1.
+  static const int opts[][3] = {  // cells, compute warps (= units), ring stages
+      {8, 8, 2}, {4, 8, 2}, {4, 8, 1}, {2, 8, 2}, {2, 8, 1}, {8, 4, 2}, {4, 4, 2}, {4, 4, 1},
+      {2, 4, 2}, {2, 4, 1}, {1, 8, 1}, {1, 4, 1}, {1, 2, 1}, {1, 1, 1}};
+  for (auto& o : opts) {
+    if (force_cells && o[0] != force_cells) continue;
+    if (o[0] > max_cells) continue;
+    const long smem = smem_bytes(nk, qs, k2s, nf, o[0], o[1], o[2], c.hdr, 2);
+    if (smem > smem_limit) continue;
+    c.cells = o[0];
+    c.m1t = 8 / o[0];
+    c.nw = o[1];
+    c.upc = o[1];
+    c.nteams = 2;
+    c.nstage = o[2];
+    c.smem = (int)smem;
+    c.cg = c.cells;
+    c.pairsplit = 0;
+    return true;
   }
   return false;
 }

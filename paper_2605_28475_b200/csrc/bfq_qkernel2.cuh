@@ -155,6 +155,9 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
   const uint32_t phu_u32 = smem_u32(phis + u * 8 * K2S);
   const uint32_t cell_bytes = (uint32_t)cell_elems * 8u;
   uint32_t fa[MT], fb[MT], rrow[MT], rrowd[MT], fx_a = 0, fx_b = 0, rx = 0, rxd = 0;
+  uint32_t fa_lo = 0, fb_lo = 0;  // checked builds: this warp's staged cells (f2 / f3)
+  const uint32_t fspan = (uint32_t)HC * cell_bytes;
+  const uint32_t phu_hi = phu_u32 + (uint32_t)(8 * K2S) * 8u;  // end of this unit's Phi buffer
   {
     const uint32_t f0 = smem_u32(fs) + (uint32_t)(h * HC) * cell_bytes;  // this warp's first cell
     const uint32_t f3off = BILIN ? (uint32_t)(CELLS * cell_elems) * 8u : 0u;
@@ -168,6 +171,8 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
     }
     fx_a = f0 + (uint32_t)((NK - 1) * QS) * 8u;
     fx_b = fx_a + f3off;
+    fa_lo = f0;
+    fb_lo = f0 + f3off;
     rx = (uint32_t)((NK - 1) * K2S + kq) * 8u;   // R row k1 = n_k-1 (X1 stage 2)
     rxd = (uint32_t)((NK - 1) * K2SD + kq) * 8u;
   }
@@ -199,11 +204,13 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
           for (int e = 0; e < 2; ++e) {
             const int ia = 8 * a + r0, ib = 8 * b + 2 * kq + e;
             if (!dg) {
-              if (ia < NK && ib < NK) sts_v(ph + (uint32_t)(ia * NK + ib) * 8u, acc[cc][a][b][e]);
+              if (ia < NK && ib < NK)
+                sts_v(BFQ_CHK(ph + (uint32_t)(ia * NK + ib) * 8u, ph, ph + (uint32_t)K2S * 8u, CHK_PHI_ST),
+                      acc[cc][a][b][e]);
             } else if (a <= b && ia <= ib && ib < NK) {
               // packed upper triangle p(a,b) = a*NK - a(a-1)/2 + (b - a)
               const int pidx = ia * NK - (ia * (ia - 1)) / 2 + (ib - ia);
-              sts_v(ph + (uint32_t)pidx * 8u, acc[cc][a][b][e]);
+              sts_v(BFQ_CHK(ph + (uint32_t)pidx * 8u, ph, ph + (uint32_t)K2S * 8u, CHK_PHI_ST), acc[cc][a][b][e]);
             }
           }
     }
@@ -214,7 +221,10 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
   if (nch > 1) slice_bounds(1, zs_nn, ze_nn);
   // slices are padded to whole k-steps with g = 0 rows (bfq_plan.cpp), and a
   // fetch past the last slice reads a valid row that is never used: no clamp
-  auto fetch_rb = [&](int z, int ze) { (void)ze; return load_row(p.rows, rowhit ? (z & 15) : z); };
+  auto fetch_rb = [&](int z, int ze) {
+    (void)ze;
+    return load_row(p.rows, (int)BFQ_CHK_IDX((long long)(rowhit ? (z & 15) : z), p.n_rows, CHK_ROW));
+  };
   Row nxt_row = fetch_rb(zs_n[0] + kq, ze_n[0]);
   // DUAL: the second row group of the next iteration, also one iteration ahead
   // (rows of a 600k-row table miss L1; ncu showed long-scoreboard stalls on it)
@@ -271,8 +281,8 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
             double av[MT], bv[MT];
 #pragma unroll
             for (int t = 0; t < MTM; ++t) {
-              av[t] = rw.g * lds_ro(fa[t] + qa + cc * cell_bytes);
-              bv[t] = lds_ro(fb[t] + qb + cc * cell_bytes);
+              av[t] = rw.g * lds_ro(BFQ_CHK(fa[t] + qa + cc * cell_bytes, fa_lo, fa_lo + fspan, CHK_F2));
+              bv[t] = lds_ro(BFQ_CHK(fb[t] + qb + cc * cell_bytes, fb_lo, fb_lo + fspan, CHK_F3));
             }
 #pragma unroll
             for (int a = 0; a < MTM; ++a)
@@ -280,8 +290,9 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
               for (int b = 0; b < MTM; ++b)
                 if (b >= a || !DGC) dmma884(ac[cc][a][b][0], ac[cc][a][b][1], av[a], bv[b]);
             if constexpr (X1) {
-              const double ea = rw.g * lds_ro(fx_a + qa + cc * cell_bytes);  // g f2[n_k-1, q2]
-              const double eb = lds_ro(fx_b + qb + cc * cell_bytes);         // f3[n_k-1, q3]
+              const double ea =
+                  rw.g * lds_ro(BFQ_CHK(fx_a + qa + cc * cell_bytes, fa_lo, fa_lo + fspan, CHK_F2));  // g f2[n_k-1, q2]
+              const double eb = lds_ro(BFQ_CHK(fx_b + qb + cc * cell_bytes, fb_lo, fb_lo + fspan, CHK_F3));  // f3[n_k-1, q3]
 #pragma unroll
               for (int t = 0; t < MTM; ++t) {
                 if (!DGC) xr[cc][t] = fma(ea, bv[t], xr[cc][t]);
@@ -350,15 +361,19 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
               for (int t = 0; t < MTM; ++t) {
                 const int ab = r0 + 8 * t;
                 if (!DGC) {
-                  sts_v(ph + (uint32_t)(L * NKT + ab) * 8u, xr[cc][t]);  // Phi[L][b]
-                  sts_v(ph + (uint32_t)(ab * NKT + L) * 8u, xc[cc][t]);  // Phi[a][L]
+                  sts_v(BFQ_CHK(ph + (uint32_t)(L * NKT + ab) * 8u, ph, ph + (uint32_t)K2S * 8u, CHK_PHI_ST),
+                        xr[cc][t]);  // Phi[L][b]
+                  sts_v(BFQ_CHK(ph + (uint32_t)(ab * NKT + L) * 8u, ph, ph + (uint32_t)K2S * 8u, CHK_PHI_ST),
+                        xc[cc][t]);  // Phi[a][L]
                 } else {
-                  sts_v(ph + (uint32_t)(ab * NKT - (ab * (ab - 1)) / 2 + (L - ab)) * 8u, xc[cc][t]);
+                  sts_v(BFQ_CHK(ph + (uint32_t)(ab * NKT - (ab * (ab - 1)) / 2 + (L - ab)) * 8u, ph,
+                                ph + (uint32_t)K2S * 8u, CHK_PHI_ST),
+                        xc[cc][t]);
                 }
               }
               if (r0 == 0) {
                 const int pl = DGC ? (L * NKT - (L * (L - 1)) / 2) : (L * NKT + L);
-                sts_v(ph + (uint32_t)pl * 8u, xd[cc]);
+                sts_v(BFQ_CHK(ph + (uint32_t)pl * 8u, ph, ph + (uint32_t)K2S * 8u, CHK_PHI_ST), xd[cc]);
               }
             }
           }
@@ -368,15 +383,19 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
     if (dg) stage1(std::true_type{});
     else stage1(std::false_type{});
     tick(ck_s1);
+    BFQ_JITTER(4 * i + 1);
     named_bar_sync(bar_id, 64);  // Phi of all 8 pairs written
     tick(ck_b1);
     // ---- stage 2: this warp's half of K for all 8 pairs
     // ring slot and phase of channel i (NST is 1 or 2: no integer division)
     const int s = NST == 1 ? 0 : (i & 1);
     const unsigned par = NST == 1 ? (unsigned)(i & 1) : (unsigned)((i >> 1) & 1);
-    if (!nowait || i == 0) mbar_wait(&tfull[s], par);
+    BFQ_JITTER(4 * i + 2);
+    if (!nowait || i == 0) mbar_wait_chk(p, &tfull[s], par);
     tick(ck_w);
     const uint32_t rb = ring_u32 + (uint32_t)(s * rblk) * 8u;
+    const uint32_t rb_hi = rb + (uint32_t)rblk * 8u;  // end of this ring slot
+    (void)rb_hi;
     const uint32_t pa = phu_u32 + (uint32_t)(r0 * K2S + kq) * 8u;
     auto stage2 = [&](auto dgtag) {
       constexpr bool DGC = decltype(dgtag)::value;
@@ -391,12 +410,13 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
 #pragma unroll 2
       for (; ks + 2 <= ks1; ks += 2) {
         const int k0 = ks * 4;
-        const double av0 = lds_v(pa + k0 * 8), av1 = lds_v(pa + (k0 + 4) * 8);
+        const double av0 = lds_v(BFQ_CHK(pa + k0 * 8, phu_u32, phu_hi, CHK_PHI_LD));
+        const double av1 = lds_v(BFQ_CHK(pa + (k0 + 4) * 8, phu_u32, phu_hi, CHK_PHI_LD));
         double bv0[MT], bv1[MT];
 #pragma unroll
         for (int j = 0; j < MTM; ++j) {
-          bv0[j] = lds_v(rb + rr[j] + k0 * 8);
-          bv1[j] = lds_v(rb + rr[j] + (k0 + 4) * 8);
+          bv0[j] = lds_v(BFQ_CHK(rb + rr[j] + k0 * 8, rb, rb_hi, CHK_RING));
+          bv1[j] = lds_v(BFQ_CHK(rb + rr[j] + (k0 + 4) * 8, rb, rb_hi, CHK_RING));
         }
 #pragma unroll
         for (int j = 0; j < MTM; ++j) {
@@ -404,24 +424,55 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
           dmma884(accb[j][0], accb[j][1], av1, bv1[j]);
         }
         if constexpr (X1) {
-          x2 = fma(av0, lds_v(rb + rrx + k0 * 8), x2);
-          x2 = fma(av1, lds_v(rb + rrx + (k0 + 4) * 8), x2);
+          x2 = fma(av0, lds_v(BFQ_CHK(rb + rrx + k0 * 8, rb, rb_hi, CHK_RING)), x2);
+          x2 = fma(av1, lds_v(BFQ_CHK(rb + rrx + (k0 + 4) * 8, rb, rb_hi, CHK_RING)), x2);
         }
       }
       if (ks < ks1) {
         const int k0 = ks * 4;
-        const double av = lds_v(pa + k0 * 8);
+        const double av = lds_v(BFQ_CHK(pa + k0 * 8, phu_u32, phu_hi, CHK_PHI_LD));
 #pragma unroll
-        for (int j = 0; j < MTM; ++j) dmma884(acc2[j][0], acc2[j][1], av, lds_v(rb + rr[j] + k0 * 8));
-        if constexpr (X1) x2 = fma(av, lds_v(rb + rrx + k0 * 8), x2);
+        for (int j = 0; j < MTM; ++j)
+          dmma884(acc2[j][0], acc2[j][1], av, lds_v(BFQ_CHK(rb + rr[j] + k0 * 8, rb, rb_hi, CHK_RING)));
+        if constexpr (X1) x2 = fma(av, lds_v(BFQ_CHK(rb + rrx + k0 * 8, rb, rb_hi, CHK_RING)), x2);
       }
     };
     if (dg) stage2(std::true_type{});
     else stage2(std::false_type{});
     tick(ck_s2);
+    BFQ_JITTER(4 * i + 3);
     named_bar_sync(bar_id, 64);  // Phi consumed by both warps
     tick(ck_b2);
-    if (lane == 0) {
+    if constexpr (kChecked) {
+      // Race canaries: this warp's Phi rows are poisoned with 1e300 until its
+      // next stage 1 rewrites them (a stage-2 read of a stale or early Phi
+      // entry blows Q up), and the last warp to release an R slot poisons it
+      // before the refill (a read of a released or not-yet-landed slot does
+      // the same).  Unused K padding keeps its zeros, so a correct schedule
+      // is unaffected: 1e300 x 0 = 0.
+#pragma unroll 1
+      for (int ml = 0; ml < (i + 1 < nch ? M1T : 0); ++ml)  // not after the last channel: the
+#pragma unroll 1                                           // epilogue reuses the buffer
+        for (int cc = 0; cc < HC; ++cc) {
+          const uint32_t ph = phu_u32 + (uint32_t)((ml * CELLS + h * HC + cc) * K2S) * 8u;
+          for (int e = lane; e < NK * NK; e += 32) sts_v(ph + (uint32_t)e * 8u, 1e300);
+        }
+      __syncwarp();
+      BFQ_JITTER(4 * i);
+      int last = 0;
+      if (lane == 0) {
+        __threadfence_block();
+        last = atomicAdd(&tarr[s], 1) == 2 * t_nunits - 1;
+        if (last) tarr[s] = 0;
+      }
+      last = __shfl_sync(0xffffffffu, last, 0);
+      if (last) {
+        for (int e = lane; e < NK * K2S; e += 32) sts_v(rb + (uint32_t)e * 8u, 1e300);
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        __syncwarp();
+        if (lane == 0 && i + NST < nch) issue_r(team, i + NST, ctau[team * p.max_chan + i + NST]);
+      }
+    } else if (lane == 0) {
       __threadfence_block();
       if (atomicAdd(&tarr[s], 1) == 2 * t_nunits - 1) {
         tarr[s] = 0;
@@ -448,10 +499,10 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
   if (h == 1) {
 #pragma unroll
     for (int j = 0; j < MTM; ++j) {
-      sts_v(xch + (uint32_t)(2 * j) * 8u, acc2[j][0] + accb[j][0]);
-      sts_v(xch + (uint32_t)(2 * j + 1) * 8u, acc2[j][1] + accb[j][1]);
+      sts_v(BFQ_CHK(xch + (uint32_t)(2 * j) * 8u, phu_u32, phu_hi, CHK_XCH), acc2[j][0] + accb[j][0]);
+      sts_v(BFQ_CHK(xch + (uint32_t)(2 * j + 1) * 8u, phu_u32, phu_hi, CHK_XCH), acc2[j][1] + accb[j][1]);
     }
-    if constexpr (X1) sts_v(xch + (uint32_t)(2 * MT) * 8u, x2);
+    if constexpr (X1) sts_v(BFQ_CHK(xch + (uint32_t)(2 * MT) * 8u, phu_u32, phu_hi, CHK_XCH), x2);
   }
   named_bar_sync(bar_id, 64);
   if (h == 1) return;
@@ -465,17 +516,24 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
     const int l1 = grp.l1, q1 = l1 * l1 + m1;
     double* qc = p.q + cell * (long long)NK * p.nq + q1;
     auto put = [&](int k1, double v) {
-      if (p.conservation && ((k1 == 0 && l1 <= 1) || (k1 == 1 && l1 == 0))) v = 0.0;
-      qc[(size_t)k1 * p.nq] = v;
+      if (p.conservation && ((k1 == 0 && l1 <= 1) || (k1 == 1 && l1 == 0))) {
+        // the zeroed R rows (kinematic.py:594-610) already make these sums exactly 0
+        if (kChecked && v != 0.0) BFQ_CHK_IDX(1LL, 0LL, CHK_ZERO);
+        v = 0.0;
+      }
+      const long long off = (long long)(qc - p.q) + (long long)k1 * p.nq;
+      p.q[BFQ_CHK_IDX(off, p.n_cells * (long long)NK * p.nq, CHK_Q)] = v;
     };
 #pragma unroll
     for (int j = 0; j < MTM; ++j)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int k1 = 8 * j + 2 * kq + e;
-        if (k1 < NK) put(k1, (acc2[j][e] + accb[j][e]) + lds_v(xch + (uint32_t)(2 * j + e) * 8u));
+        if (k1 < NK)
+          put(k1, (acc2[j][e] + accb[j][e]) +
+                      lds_v(BFQ_CHK(xch + (uint32_t)(2 * j + e) * 8u, phu_u32, phu_hi, CHK_XCH)));
       }
     if constexpr (X1)
-      if (kq == 0) put(NK - 1, x2 + lds_v(xch + (uint32_t)(2 * MT) * 8u));
+      if (kq == 0) put(NK - 1, x2 + lds_v(BFQ_CHK(xch + (uint32_t)(2 * MT) * 8u, phu_u32, phu_hi, CHK_XCH)));
   }
 }

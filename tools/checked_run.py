@@ -1,0 +1,93 @@
+"""Self-checking run of the Q kernels (libbfq_checked.so, -DBFQ_CHECKED).
+
+    BFQ_LIB=checked python tools/checked_run.py [--ops hs_n4,hs_n8,...] [--cells N]
+
+For every operator: Q(f,f) (folded program), Q(f2,f3) (bilinear program) and
+one RK4 step on a small ragged batch, each followed by the kernel's violation
+record (bounds of every shared-memory / table / output access, mbarrier
+timeouts, computed-non-zero invariant slots) and a parity check against the
+oracle -- the R-slot / Phi poisoning of the checked build turns any race on
+those buffers into a Q error of ~1e290, which the 1e-12 parity bar catches.
+Prints one JSON line per case; exit code 1 on any violation or parity miss.
+"""
+import argparse
+import ctypes
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+os.environ.setdefault("BFQ_LIB", "checked")
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from oracle import q_oracle  # noqa: E402
+from paper_2605_28475_b200 import _lib, engine, inputs  # noqa: E402
+from paper_2605_28475_b200.operator import load_cache  # noqa: E402
+
+CODES = {1: "f2 gather", 2: "f3 gather", 3: "Phi store", 4: "Phi load", 5: "R ring load", 6: "epilogue exchange",
+         7: "table row", 8: "Q store", 9: "invariant slot computed non-zero", 10: "mbarrier wait timeout"}
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--ops", default="hs_n2,hs_n4,mm_k4l6,hs_n8,mm_n10,hs_n12,hs_n16")
+ap.add_argument("--cells", type=int, default=11)
+a = ap.parse_args()
+assert _lib.CHECKED, "run with BFQ_LIB=checked"
+lib = _lib.lib()
+lib.bfq_debug_check_status.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int)]
+bad = 0
+for name in a.ops.split(","):
+    path = os.path.join(ROOT, "operators", name + ".bfct")
+    if not os.path.exists(path):
+        print(json.dumps({"op": name, "skipped": "operator not shipped"}), flush=True)
+        continue
+    op = load_cache(path)
+    cfg = op.cfg
+    plan = engine.plan_for(op)
+    n = a.cells
+    c2 = inputs.perturbed_maxwellians(cfg.n_k, cfg.l_max, n, seed=5)
+    c3 = inputs.perturbed_maxwellians(cfg.n_k, cfg.l_max, n, seed=6)
+    f2, f3 = torch.from_numpy(c2).cuda(), torch.from_numpy(c3).cuda()
+    oop = q_oracle.OracleOperator.from_operator(op)
+    ws = q_oracle.angular_workspace(oop)
+    st = (ctypes.c_int * 5)()
+
+    def status():
+        _lib.check(lib.bfq_debug_check_status(plan.handle, st))
+        return list(st)
+
+    for case in ("ff", "f2f3", "rk4"):
+        if case == "ff":
+            q = engine.evaluate_batch(plan, f2).cpu().numpy()
+            refs = [q_oracle.q_angular_first(oop, c2[i], workspace=ws) for i in (0, n // 2, n - 1)]
+        elif case == "f2f3":
+            q = engine.evaluate_batch(plan, f2, f3).cpu().numpy()
+            refs = [q_oracle.q_angular_first(oop, c2[i], c3[i], workspace=ws) for i in (0, n // 2, n - 1)]
+        else:
+            y = f2.clone()
+            work = torch.empty((3,) + tuple(y.shape), dtype=torch.float64, device="cuda")
+            flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+            plan.rk4_step_device(y.data_ptr(), work.data_ptr(), n, 0.01, flag.data_ptr(),
+                                 torch.cuda.current_stream().cuda_stream)
+            q = y.cpu().numpy()
+            refs = []
+            for i in (0, n // 2, n - 1):
+                rhs = lambda v: q_oracle.q_angular_first(oop, v, workspace=ws)  # noqa: E731
+                yy, dt = c2[i], 0.01
+                k1 = rhs(yy)
+                k2 = rhs(yy + 0.5 * dt * k1)
+                k3 = rhs(yy + 0.5 * dt * k2)
+                k4 = rhs(yy + dt * k3)
+                refs.append(yy + (dt / 6.0) * (k1 + 2.0 * k2 + 2.0 * k3 + k4))
+        s = status()
+        errs = [q_oracle.rel_err(q[i], r) for i, r in zip((0, n // 2, n - 1), refs)]
+        ok = s[4] == 0 and max(errs) <= 1e-12 and bool(np.all(np.isfinite(q)))
+        bad += not ok
+        print(json.dumps({"op": name, "case": case, "kernel_info": {k: plan.info[k] for k in
+                          ("cells_per_cta", "warps_per_cta", "stages")},
+                          "violations": s[4], "first": {"code": s[0], "what": CODES.get(s[0]), "block": s[1],
+                                                        "thread": s[2], "aux": s[3]} if s[4] else None,
+                          "max_rel_err": max(errs), "ok": ok}), flush=True)
+sys.exit(1 if bad else 0)
