@@ -125,9 +125,10 @@ static bool choose_config(int nk, int qs, int k2s, int nf, int smem_limit, int m
   static const int opts[][3] = {  // cells, compute warps (= units), ring stages
       {8, 8, 2}, {4, 8, 2}, {4, 8, 1}, {2, 8, 2}, {2, 8, 1}, {8, 4, 2}, {4, 4, 2}, {4, 4, 1},
       {2, 4, 2}, {2, 4, 1}, {1, 8, 1}, {1, 4, 1}, {1, 2, 1}, {1, 1, 1}};
+  const int max_cells1 = c.mt == 1 ? 8 : (c.mt == 2 ? 4 : 2);  // no X1 variant of this kernel
   for (auto& o : opts) {
     if (force_cells && o[0] != force_cells) continue;
-    if (o[0] > max_cells) continue;
+    if (o[0] > max_cells1) continue;
     const long smem = smem_bytes(nk, qs, k2s, nf, o[0], o[1], o[2], c.hdr, 2);
     if (smem > smem_limit) continue;
     c.cells = o[0];
