@@ -25,6 +25,72 @@ BFQ_HD constexpr int conflict_free_stride_dev(int n) {
   return s;
 }
 
+// ---------------------------------------------------------------- K order
+// The K axis of stage 2 (an index over the radial pairs (a, b) of Phi) may be
+// numbered in any order as long as Phi and the R blocks agree.  It is numbered
+// in the order the stage-1 epilogue STORES Phi: DMMA tile (A, B) = (a/8, b/8),
+// accumulator half e = b&1, then lane (r0, kq) = (a&7, (b&7)>>1), skipping
+// entries outside n_k (and, for self-symmetric channels, entries below the
+// diagonal).  The valid lanes of each half-warp store then go to consecutive
+// doubles -- conflict-free -- while K stays compact (n_k^2, or n_k(n_k+1)/2).
+// phi_k / phid_k are used by the plan (R permutation) and by the kernels.
+BFQ_HD constexpr int kq_count(int nk, int b, int e) {  // kq in 0..3 with 8b + 2kq + e < nk
+  const int n = (nk - 8 * b - e + 1) / 2;
+  return n < 0 ? 0 : (n > 4 ? 4 : n);
+}
+BFQ_HD constexpr int row_count(int nk, int a) {  // r0 in 0..7 with 8a + r0 < nk
+  const int n = nk - 8 * a;
+  return n < 0 ? 0 : (n > 8 ? 8 : n);
+}
+// first kq of row r0 on or above the diagonal of a self-symmetric tile (r0 <= 2kq + e)
+BFQ_HD constexpr int kq_min_diag(int r0, int e) {
+  const int d = r0 - e;
+  return d <= 0 ? 0 : (d + 1) / 2;
+}
+// entries of the diagonal tile (A, A), half e, in rows before r0
+BFQ_HD constexpr int diag_rows_before(int nk, int a, int e, int r0) {
+  int s = 0;
+  const int n = kq_count(nk, a, e);
+  for (int r = 0; r < r0; ++r) {
+    const int c = n - kq_min_diag(r, e);
+    s += c > 0 ? c : 0;
+  }
+  return s;
+}
+// first K index of tile (A, B), half e
+BFQ_HD constexpr int phi_base(int nk, int a, int b, int e) {
+  const int mt = (nk + 7) / 8;
+  int s = 0;
+  for (int a2 = 0; a2 < mt; ++a2)
+    for (int b2 = 0; b2 < mt; ++b2)
+      for (int e2 = 0; e2 < 2; ++e2) {
+        if (a2 == a && b2 == b && e2 == e) return s;
+        s += row_count(nk, a2) * kq_count(nk, b2, e2);
+      }
+  return s;
+}
+BFQ_HD constexpr int phid_base(int nk, int a, int b, int e) {  // a <= b
+  const int mt = (nk + 7) / 8;
+  int s = 0;
+  for (int a2 = 0; a2 < mt; ++a2)
+    for (int b2 = a2; b2 < mt; ++b2)
+      for (int e2 = 0; e2 < 2; ++e2) {
+        if (a2 == a && b2 == b && e2 == e) return s;
+        s += a2 < b2 ? row_count(nk, a2) * kq_count(nk, b2, e2) : diag_rows_before(nk, a2, e2, 8);
+      }
+  return s;
+}
+// K index of Phi[ia][ib] (ia, ib < nk)
+BFQ_HD constexpr int phi_k(int nk, int ia, int ib) {
+  return phi_base(nk, ia / 8, ib / 8, ib & 1) + (ia & 7) * kq_count(nk, ib / 8, ib & 1) + ((ib & 7) >> 1);
+}
+// K index of Phi[ia][ib] of a self-symmetric channel (ia <= ib < nk)
+BFQ_HD constexpr int phid_k(int nk, int ia, int ib) {
+  const int a = ia / 8, b = ib / 8, e = ib & 1, r0 = ia & 7, kq = (ib & 7) >> 1;
+  if (a < b) return phid_base(nk, a, b, e) + r0 * kq_count(nk, b, e) + kq;
+  return phid_base(nk, a, a, e) + diag_rows_before(nk, a, e, r0) + kq - kq_min_diag(r0, e);
+}
+
 // One COO row as the kernel reads it: 16 bytes, one LDG.128 per row.
 struct alignas(16) Row {
   int32_t q2;

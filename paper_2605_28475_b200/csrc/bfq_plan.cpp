@@ -578,6 +578,32 @@ int build_host_plan(const bfq_desc& d, int smem_limit, HostPlan& hp) {
     }
   }
 
+  // K order of every R block = the order the kernels store Phi in
+  // (bfq_internal.h phi_k / phid_k: conflict-free Phi stores, compact K).
+  {
+    const size_t nb = hp.rblocks.size() / blk;
+    std::vector<char> packed(nb, 0);
+    for (const ChanEntry& ce : hp.sym.chans)
+      if (ce.diag) packed[ce.tau] = 1;
+    std::vector<double> src(blk);
+    for (size_t t = 0; t < nb; ++t) {
+      double* b = hp.rblocks.data() + t * blk;
+      std::copy(b, b + blk, src.begin());
+      std::fill(b, b + blk, 0.0);
+      for (int k1 = 0; k1 < nk; ++k1) {
+        if (packed[t]) {
+          int pidx = 0;
+          for (int a = 0; a < nk; ++a)
+            for (int c = a; c < nk; ++c, ++pidx)
+              b[(size_t)k1 * hp.k2sd + phid_k(nk, a, c)] = src[(size_t)k1 * hp.k2sd + pidx];
+        } else {
+          for (int a = 0; a < nk; ++a)
+            for (int c = 0; c < nk; ++c) b[(size_t)k1 * hp.k2s + phi_k(nk, a, c)] = src[(size_t)k1 * hp.k2s + a * nk + c];
+        }
+      }
+    }
+  }
+
   // executed DMMA MACs per cell of the Q(f,f) program (after the diag packing)
   {
     const Program& pg = hp.sym;

@@ -183,7 +183,9 @@ __global__ void __launch_bounds__(256, 1) bfq_q_kernel(const KParams p) {
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int ia = 8 * a + r0, ib = 8 * b + 2 * kq + e;
-            if (ia < NK && ib < NK) sts_v(ph + (uint32_t)(ia * NK + ib) * 8u, acc[cc][a][b][e]);
+            // K in store order (bfq_internal.h phi_k), as the R blocks
+            if (ia < NK && ib < NK)
+              sts_v(ph + (uint32_t)(phi_base(NK, a, b, e) + r0 * kq_count(NK, b, e) + kq) * 8u, acc[cc][a][b][e]);
           }
     }
   };

@@ -192,6 +192,16 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
       ze[ml] = ok ? __ldg(p.sstart + ce.slice_base + m1 + 1) : 0;
     }
   };
+  // Phi is stored in K "store order" (bfq_internal.h phi_k / phid_k): the
+  // valid lanes of each half-warp write consecutive doubles, conflict-free.
+  // Off-diagonal tiles: base(A,B,e) + r0 * kq_count + kq; diagonal tiles of
+  // self-symmetric channels: a per-lane offset computed once here.
+  int dpre[MT][2];
+#pragma unroll
+  for (int a = 0; a < MT; ++a)
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+      dpre[a][e] = phid_base(NK, a, a, e) + diag_rows_before(NK, a, e, r0) - kq_min_diag(r0, e) + kq;
   auto store_phi = [&](int ml, double (&acc)[HC][MT][MT][2], bool dg) {
 #pragma unroll
     for (int cc = 0; cc < HC; ++cc) {
@@ -204,13 +214,13 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
           for (int e = 0; e < 2; ++e) {
             const int ia = 8 * a + r0, ib = 8 * b + 2 * kq + e;
             if (!dg) {
-              if (ia < NK && ib < NK)
-                sts_v(BFQ_CHK(ph + (uint32_t)(ia * NK + ib) * 8u, ph, ph + (uint32_t)K2S * 8u, CHK_PHI_ST),
-                      acc[cc][a][b][e]);
+              if (ia < NK && ib < NK) {
+                const int k = phi_base(NK, a, b, e) + r0 * kq_count(NK, b, e) + kq;
+                sts_v(BFQ_CHK(ph + (uint32_t)k * 8u, ph, ph + (uint32_t)K2S * 8u, CHK_PHI_ST), acc[cc][a][b][e]);
+              }
             } else if (a <= b && ia <= ib && ib < NK) {
-              // packed upper triangle p(a,b) = a*NK - a(a-1)/2 + (b - a)
-              const int pidx = ia * NK - (ia * (ia - 1)) / 2 + (ib - ia);
-              sts_v(BFQ_CHK(ph + (uint32_t)pidx * 8u, ph, ph + (uint32_t)K2S * 8u, CHK_PHI_ST), acc[cc][a][b][e]);
+              const int k = a < b ? phid_base(NK, a, b, e) + r0 * kq_count(NK, b, e) + kq : dpre[a][e];
+              sts_v(BFQ_CHK(ph + (uint32_t)k * 8u, ph, ph + (uint32_t)K2S * 8u, CHK_PHI_ST), acc[cc][a][b][e]);
             }
           }
     }
@@ -355,24 +365,26 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
             xd[cc] += __shfl_xor_sync(0xffffffffu, xd[cc], 1);
             xd[cc] += __shfl_xor_sync(0xffffffffu, xd[cc], 2);
             const uint32_t ph = phu_u32 + (uint32_t)((ml * CELLS + h * HC + cc) * K2S) * 8u;
-            constexpr int L = NKT - 1;
+            // store-order K of row / column L = n_k - 1 = 8 (MT - 1): tile row or
+            // column MT - 1 holds one index (r0 = 0 or kq = e = 0)
+            constexpr int L = NKT - 1, TL = MT - 1;
             if (kq == 0) {
 #pragma unroll
               for (int t = 0; t < MTM; ++t) {
-                const int ab = r0 + 8 * t;
                 if (!DGC) {
-                  sts_v(BFQ_CHK(ph + (uint32_t)(L * NKT + ab) * 8u, ph, ph + (uint32_t)K2S * 8u, CHK_PHI_ST),
-                        xr[cc][t]);  // Phi[L][b]
-                  sts_v(BFQ_CHK(ph + (uint32_t)(ab * NKT + L) * 8u, ph, ph + (uint32_t)K2S * 8u, CHK_PHI_ST),
-                        xc[cc][t]);  // Phi[a][L]
+                  // Phi[L][8t + r0]: tile (TL, t), half r0 & 1, kq' = r0 >> 1
+                  const int kr = ((r0 & 1) ? phi_base(NKT, TL, t, 1) : phi_base(NKT, TL, t, 0)) + (r0 >> 1);
+                  sts_v(BFQ_CHK(ph + (uint32_t)kr * 8u, ph, ph + (uint32_t)K2S * 8u, CHK_PHI_ST), xr[cc][t]);
+                  // Phi[8t + r0][L]: tile (t, TL), half 0, kq' = 0 (one valid kq)
+                  const int kc = phi_base(NKT, t, TL, 0) + r0 * kq_count(NKT, TL, 0);
+                  sts_v(BFQ_CHK(ph + (uint32_t)kc * 8u, ph, ph + (uint32_t)K2S * 8u, CHK_PHI_ST), xc[cc][t]);
                 } else {
-                  sts_v(BFQ_CHK(ph + (uint32_t)(ab * NKT - (ab * (ab - 1)) / 2 + (L - ab)) * 8u, ph,
-                                ph + (uint32_t)K2S * 8u, CHK_PHI_ST),
-                        xc[cc][t]);
+                  const int kc = phid_base(NKT, t, TL, 0) + r0 * kq_count(NKT, TL, 0);
+                  sts_v(BFQ_CHK(ph + (uint32_t)kc * 8u, ph, ph + (uint32_t)K2S * 8u, CHK_PHI_ST), xc[cc][t]);
                 }
               }
               if (r0 == 0) {
-                const int pl = DGC ? (L * NKT - (L * (L - 1)) / 2) : (L * NKT + L);
+                const int pl = DGC ? phid_k(NKT, L, L) : phi_k(NKT, L, L);
                 sts_v(BFQ_CHK(ph + (uint32_t)pl * 8u, ph, ph + (uint32_t)K2S * 8u, CHK_PHI_ST), xd[cc]);
               }
             }
