@@ -679,6 +679,7 @@ def run_ours(args, rank, world, local_rank):
     kern_s = statistics.mean(step_ms) / 1e3
     achieved = flops_cell * n_cells * q_per_step / kern_s / 1e12
     exec_tf = 2.0 * plan.info["exec_macs_per_cell"] * n_cells * q_per_step / kern_s / 1e12
+    useful_tf = 2.0 * plan.info["useful_macs_per_cell"] * n_cells * q_per_step / kern_s / 1e12
     traffic = None
     tpath = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
     if os.path.exists(tpath):
@@ -707,6 +708,11 @@ def run_ours(args, rank, world, local_rank):
                      "flops_per_cell": flops_cell,
                      "exec_dmma_macs_per_cell": plan.info["exec_macs_per_cell"],
                      "exec_tflops": exec_tf, "exec_frac": exec_tf / FP64_PEAK_TFLOPS,
+                     "useful_macs_per_cell": plan.info["useful_macs_per_cell"],
+                     "useful_tflops": useful_tf, "useful_frac": useful_tf / FP64_PEAK_TFLOPS,
+                     "fracs_note": "frac: algorithmic FLOP (2(N_G n_k^2 + N_S n_k^3), SURVEY 8d) / peak; "
+                                   "exec_frac: DMMA MACs issued incl. tile and row padding; useful_frac: MACs "
+                                   "of the folded channels without padding (what the kernel must do)",
                      "hbm_frac": bytes_cell * n_cells / kern_s / 1e9 / measured_peaks().get("hbm_gbs", 6548.2)},
         "e2e": e2e,
         "gpu_launches": args.steps * (11 if rk4 else 1),

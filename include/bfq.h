@@ -90,6 +90,9 @@ typedef struct bfq_plan_info {
   int32_t items_per_tile;     /* CTAs per cell tile                                   */
   double exec_macs_per_cell;  /* DMMA MACs actually issued per cell, incl. padding    */
   double operator_bytes;      /* device bytes of the uploaded operator                */
+  double useful_macs_per_cell; /* MACs of the evaluated (folded) channels without tile
+                                  or row padding: stage 1 rows x n_k^2 (n_k(n_k+1)/2 on
+                                  self-symmetric channels) + stage 2 slices x n_k x K     */
 } bfq_plan_info;
 
 int bfq_plan_create(const bfq_desc* desc, int device, bfq_plan** out);

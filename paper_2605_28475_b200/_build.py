@@ -7,10 +7,13 @@ source tree (``bfq_build_id()``, and the marker string ``BFQ_BUILD_ID=<hash>``
 in the binary), so the loader (``_lib.py``) can refuse -- or rebuild -- a
 library that was not compiled from the sources next to it.
 
-``checked=True`` builds ``libbfq_checked.so``: the same sources with
-``-DBFQ_CHECKED`` (device-side bounds checks on every shared-memory and
-table access, mbarrier wait timeouts, R-ring / Phi poisoning), for the
-self-checking GPU tests (tests/test_gpu_checked.py).
+``checked=True`` (or ``"checked"``) builds ``libbfq_checked.so``: the same
+sources with ``-DBFQ_CHECKED`` (device-side bounds checks on every
+shared-memory and table access, mbarrier wait timeouts, R-ring / Phi
+poisoning), for the self-checking GPU tests (tests/test_gpu_checked.py).
+``"timing"`` builds ``libbfq_timing.so`` with ``-DBFQ_PHASE_CLOCKS``: per-phase
+cycle counters and the BFQ_DEBUG stage-skip switches of the timing
+experiments (results are wrong in the skip modes; never used by tests).
 """
 
 from __future__ import annotations
@@ -37,8 +40,25 @@ SOURCES = [
 HEADER_EXT = (".h", ".cuh", ".hpp")
 
 
-def lib_path(checked: bool = False) -> str:
-    return os.path.join(PKG, "libbfq_checked.so" if checked else "libbfq.so")
+VARIANTS = {"": [], "checked": ["-DBFQ_CHECKED=1"], "timing": ["-DBFQ_PHASE_CLOCKS=1"],
+            # A/B experiments: the timing build plus -DBFQ_EXPERIMENT (kernel code paths under test)
+            "exp": ["-DBFQ_PHASE_CLOCKS=1", "-DBFQ_EXPERIMENT=1"]}
+
+
+def _variant(checked) -> str:
+    """True / False (the checked build or not) or a variant name."""
+    if checked is True:
+        return "checked"
+    if not checked:
+        return ""
+    if checked not in VARIANTS:
+        raise ValueError(f"unknown library variant {checked!r}")
+    return checked
+
+
+def lib_path(checked=False) -> str:
+    v = _variant(checked)
+    return os.path.join(PKG, f"libbfq_{v}.so" if v else "libbfq.so")
 
 
 def _headers() -> list[str]:
@@ -56,11 +76,11 @@ def _digest(paths, extra: str) -> str:
     return h.hexdigest()[:24]
 
 
-def _defines(checked: bool) -> list[str]:
-    return ["-DBFQ_CHECKED=1"] if checked else []
+def _defines(checked) -> list[str]:
+    return VARIANTS[_variant(checked)]
 
 
-def source_hash(checked: bool = False) -> str:
+def source_hash(checked=False) -> str:
     """Hash of every source, header and flag the library is built from."""
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
     return _digest(srcs + _headers(), " ".join(NVCC_FLAGS + _defines(checked) + SOURCES))
@@ -80,11 +100,11 @@ def embedded_hash(path: str) -> str | None:
     return blob[j:j + 24].decode(errors="replace")
 
 
-def is_current(checked: bool = False) -> bool:
+def is_current(checked=False) -> bool:
     return embedded_hash(lib_path(checked)) == source_hash(checked)
 
 
-def build(checked: bool = False, verbose: bool = False, jobs: int | None = None) -> str:
+def build(checked=False, verbose: bool = False, jobs: int | None = None) -> str:
     """Compile (only what changed) and link; returns the library path."""
     path = lib_path(checked)
     want = source_hash(checked)
@@ -94,7 +114,7 @@ def build(checked: bool = False, verbose: bool = False, jobs: int | None = None)
         return path
     os.makedirs(BUILD, exist_ok=True)
     hdr_hash = _digest(_headers(), " ".join(NVCC_FLAGS + _defines(checked)))
-    tag = "chk" if checked else "opt"
+    tag = {"": "opt", "checked": "chk", "timing": "tim", "exp": "exp"}[_variant(checked)]
 
     def compile_one(src):
         full = os.path.join(CSRC, src)

@@ -14,9 +14,12 @@ import threading
 from . import _build
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# BFQ_LIB=checked selects the self-checking build (libbfq_checked.so)
-CHECKED = os.environ.get("BFQ_LIB", "") == "checked"
-LIB_PATH = _build.lib_path(CHECKED)
+# BFQ_LIB=checked selects the self-checking build (libbfq_checked.so),
+# BFQ_LIB=timing the timing-experiment build (libbfq_timing.so)
+VARIANT = os.environ.get("BFQ_LIB", "")
+CHECKED = VARIANT == "checked"
+LIB_SEL = VARIANT if VARIANT in ("checked", "timing", "exp") else False
+LIB_PATH = _build.lib_path(LIB_SEL)
 
 BFQ_OK = 0
 BFQ_EINVAL = -1
@@ -92,6 +95,7 @@ class BfqPlanInfo(ctypes.Structure):
         ("items_per_tile", ctypes.c_int32),
         ("exec_macs_per_cell", ctypes.c_double),
         ("operator_bytes", ctypes.c_double),
+        ("useful_macs_per_cell", ctypes.c_double),
     ]
 
 
@@ -178,12 +182,12 @@ def _ensure_current(path: str) -> None:
     """The library must be built from the sources next to it (provenance).
     A stale or missing binary is rebuilt in place (nvcc is part of the image);
     BFQ_NO_AUTOBUILD=1 turns that into an error instead."""
-    if _build.is_current(CHECKED):
+    if _build.is_current(LIB_SEL):
         return
     if os.environ.get("BFQ_NO_AUTOBUILD"):
         raise EngineUnavailable(
             f"{path} is missing or was not built from these sources "
-            f"(embedded {_build.embedded_hash(path)}, sources {_build.source_hash(CHECKED)}): "
+            f"(embedded {_build.embedded_hash(path)}, sources {_build.source_hash(LIB_SEL)}): "
             "rebuild with `python -c 'import __graft_entry__ as g; g.build()'`")
     import fcntl
     import sys
@@ -191,10 +195,10 @@ def _ensure_current(path: str) -> None:
     os.makedirs(_build.BUILD, exist_ok=True)
     with open(os.path.join(_build.BUILD, ".lock"), "w") as lk:
         fcntl.flock(lk, fcntl.LOCK_EX)
-        if not _build.is_current(CHECKED):
+        if not _build.is_current(LIB_SEL):
             sys.stderr.write(f"[bfq] {os.path.basename(path)} stale or missing: rebuilding from source\n")
             try:
-                _build.build(checked=CHECKED)
+                _build.build(checked=LIB_SEL)
             except (RuntimeError, OSError) as exc:
                 raise EngineUnavailable(f"cannot build {path}: {exc}") from exc
 
@@ -217,7 +221,7 @@ def lib():
                     raise EngineUnavailable(f"cannot load {LIB_PATH}: {exc}") from exc
                 _declare(handle)
                 got = handle.bfq_build_id().decode()
-                if got != _build.source_hash(CHECKED):
+                if got != _build.source_hash(LIB_SEL):
                     raise EngineUnavailable(f"{LIB_PATH} build id {got} does not match the sources")
                 _lib = handle
     return _lib

@@ -397,6 +397,7 @@ int bfq_plan_get_info(const bfq_plan* plan, bfq_plan_info* info) {
   info->smem_bytes = plan->sym.cfg.smem;
   info->items_per_tile = plan->sym.n_items;
   info->exec_macs_per_cell = plan->sym.exec_macs_per_cell;
+  info->useful_macs_per_cell = plan->hp.useful_macs_per_cell;
   info->operator_bytes = (double)plan->operator_bytes;
   return BFQ_OK;
 }
@@ -630,6 +631,7 @@ int bfq_host_plan_info(const bfq_desc* desc, int smem_limit, bfq_plan_info* info
   info->smem_bytes = hp.sym.cfg.smem;
   info->items_per_tile = (int)hp.sym.items.size();
   info->exec_macs_per_cell = hp.sym.exec_macs_per_cell;
+  info->useful_macs_per_cell = hp.useful_macs_per_cell;
   info->operator_bytes = (double)(hp.rblocks.size() * sizeof(double) + hp.rows.size() * sizeof(Row) +
                                   hp.sstart.size() * sizeof(int32_t));
   return BFQ_OK;

@@ -46,6 +46,9 @@ QKernel pick_fixed2(int mt, int cells) {
     if (cells == 2) return bfq_q_kernel2<2, 2, BILIN, NK, QS>;
   } else {
     if (cells == 2) return bfq_q_kernel2<MT, 2, BILIN, NK, QS>;
+    if constexpr (NK == 17) {
+      if (cells == 1) return bfq_q_kernel2<MT, 1, BILIN, NK, QS>;  // SPLITM
+    }
   }
   return nullptr;
 }

@@ -176,6 +176,7 @@ struct HostPlan {
   Program sym;                    // Q(f,f) program (folded when `folded`)
   Program full;                   // Q(f2,f3) program (all channels, weight 1)
   double alg_flops_per_cell = 0.0, alg_bytes_per_cell = 0.0;
+  double useful_macs_per_cell = 0.0;  // folded program, no tile / row padding
 };
 
 // Thread-local error detail.

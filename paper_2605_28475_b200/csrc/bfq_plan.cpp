@@ -98,6 +98,32 @@ static bool choose_config(int nk, int qs, int k2s, int nf, int smem_limit, int m
       return true;
     }
   }
+  // One cell per tile, the unit's 8 output columns split over its two warps
+  // (SPLITM, bfq_qkernel2.cuh): half the staged cells of the 2-cell tile,
+  // which at n_k = 17 leaves room for a second R ring or more units.
+  // Measured at N=L=16 (16,384 cells): 2 cells x 4 units, 1 ring 42.4k cells/s;
+  // 1 cell x 4 units, 2 rings 44.1k; 1 cell x 5 units (10 warps), 2 rings 44.9k;
+  // 6 units with 1 ring 36.8k (one l1 group per CTA: packing 0.47).
+  static const int popts1[][4] = {{1, 5, 1, 2}, {1, 4, 1, 2}, {1, 6, 1, 1}, {1, 4, 1, 1}};
+  if (kernel == 2 && (force_cells == 1 || (!force_cells && nk == 17))) {
+    for (auto o0 : popts1) {
+      int o[4] = {o0[0], o0[1], o0[2], force_teams ? force_teams : o0[3]};
+      if (force_units && o[1] != force_units) continue;
+      if (o[3] > MAX_TEAMS) continue;
+      const long smem = smem_bytes(nk, qs, k2s, nf, o[0], o[1], o[2], c.hdr, o[3]);
+      if (smem > smem_limit) continue;
+      c.cells = 1;
+      c.m1t = 8;
+      c.upc = o[1];
+      c.nw = 2 * o[1];
+      c.nstage = o[2];
+      c.nteams = o[3];
+      c.smem = (int)smem;
+      c.cg = 1;
+      c.pairsplit = 1;
+      return true;
+    }
+  }
   if (kernel == 2) {
     for (auto o0 : popts) {
       int o[4] = {o0[0], o0[1], force_stages ? force_stages : o0[2], force_teams ? force_teams : o0[3]};
@@ -175,14 +201,17 @@ static void build_items(const HostPlan& hp, Program& pg) {
     std::vector<std::pair<double, int>> cols;
     for (int m1 = 0; m1 < gr.d1; ++m1) cols.push_back({m1_steps(gr, m1), m1});
     std::stable_sort(cols.begin(), cols.end(), [](auto& x, auto& y) { return x.first > y.first; });
-    std::vector<double> load(units, 0.0);
-    std::vector<int> fill(units, 0);
+    // SPLITM (one cell per tile): each unit is two halves of m1t/2 slots, one
+    // per warp, run in parallel -- deal into the lightest half instead.
+    const int halves = c.cells == 1 ? 2 : 1, hs = c.m1t / halves;
+    std::vector<double> load((size_t)units * halves, 0.0);
+    std::vector<int> fill((size_t)units * halves, 0);
     std::vector<int16_t> slots((size_t)units * c.m1t, (int16_t)-1);
     for (auto& col : cols) {
       int best = -1;
-      for (int u = 0; u < units; ++u)
-        if (fill[u] < c.m1t && (best < 0 || load[u] < load[best])) best = u;
-      slots[(size_t)best * c.m1t + fill[best]++] = (int16_t)col.second;
+      for (int u = 0; u < units * halves; ++u)
+        if (fill[u] < hs && (best < 0 || load[u] < load[best])) best = u;
+      slots[(size_t)(best / halves) * c.m1t + (best % halves) * hs + fill[best]++] = (int16_t)col.second;
       load[best] += col.first;
     }
     pg.unit_m1.insert(pg.unit_m1.end(), slots.begin(), slots.end());
@@ -191,12 +220,15 @@ static void build_items(const HostPlan& hp, Program& pg) {
     double work = 0.0;
     for (int e = 0; e < gr.n_chan; ++e) {
       const ChanEntry& ce = pg.chans[gr.chan_off + e];
+      double half[2] = {0.0, 0.0};
       for (int ml = 0; ml < c.m1t; ++ml) {
         const int m1 = pg.unit_m1[(size_t)(gr.unit_off + u) * c.m1t + ml];
         if (m1 < 0) continue;
         const int rows = hp.sstart[ce.slice_base + m1 + 1] - hp.sstart[ce.slice_base + m1];
-        work += (double)c.cells * c.mt * c.mt * 256.0 * ((rows + 3) / 4);
+        half[c.cells == 1 ? ml / (c.m1t / 2) : 0] += (double)c.cells * c.mt * c.mt * 256.0 * ((rows + 3) / 4);
       }
+      // SPLITM: the two warps walk their halves in parallel
+      work += c.cells == 1 ? 2.0 * std::max(half[0], half[1]) : half[0];
       work += stage2;
     }
     return work;
@@ -219,36 +251,102 @@ static void build_items(const HostPlan& hp, Program& pg) {
       total += w;
     }
   std::stable_sort(units_all.begin(), units_all.end(), [](const U& x, const U& y) { return x.work > y.work; });
+  if (const char* e = std::getenv("BFQ_PLAN_STATS"))
+    if (std::atoi(e) >= 2)
+      for (const U& un : units_all) std::fprintf(stderr, "unit l1=%d u=%d work=%.4g\n", un.l1, un.u, un.work);
   struct Cta {
     std::vector<std::vector<int>> team_units;  // per team: old unit ids
     std::vector<int> team_l1;
     double work = 0.0;
   };
-  std::vector<Cta> ctas;
-  std::vector<char> taken(units_all.size(), 0);
-  size_t left = units_all.size();
-  while (left) {
-    Cta cta;
-    int used = 0;
-    for (size_t k = 0; k < units_all.size() && used < c.upc; ++k) {
-      if (taken[k]) continue;
-      const U& un = units_all[k];
-      int t = -1;
-      for (size_t j = 0; j < cta.team_l1.size(); ++j)
-        if (cta.team_l1[j] == un.l1) t = (int)j;
-      if (t < 0) {
-        if ((int)cta.team_l1.size() == c.nteams) continue;
-        cta.team_l1.push_back(un.l1);
-        cta.team_units.emplace_back();
-        t = (int)cta.team_l1.size() - 1;
+  // (a) work order: the next units in descending work whose group fits.
+  auto pack_by_work = [&]() {
+    std::vector<Cta> out;
+    std::vector<char> taken(units_all.size(), 0);
+    size_t left = units_all.size();
+    while (left) {
+      Cta cta;
+      int used = 0;
+      for (size_t k = 0; k < units_all.size() && used < c.upc; ++k) {
+        if (taken[k]) continue;
+        const U& un = units_all[k];
+        int t = -1;
+        for (size_t j = 0; j < cta.team_l1.size(); ++j)
+          if (cta.team_l1[j] == un.l1) t = (int)j;
+        if (t < 0) {
+          if ((int)cta.team_l1.size() == c.nteams) continue;
+          cta.team_l1.push_back(un.l1);
+          cta.team_units.emplace_back();
+          t = (int)cta.team_l1.size() - 1;
+        }
+        cta.team_units[t].push_back(un.u);
+        cta.work = std::max(cta.work, un.work);
+        taken[k] = 1;
+        --left;
+        ++used;
       }
-      cta.team_units[t].push_back(un.u);
-      cta.work = std::max(cta.work, un.work);
-      taken[k] = 1;
-      --left;
-      ++used;
+      out.push_back(std::move(cta));
     }
-    ctas.push_back(std::move(cta));
+    return out;
+  };
+  // (b) group fill: the group holding the heaviest remaining unit opens a CTA,
+  // then each further team slot goes to the group whose units fill the free
+  // slots with the most work.  Wins when few teams fit (n_k = 17: two R rings)
+  // and groups hold few units each, where (a) leaves slots empty.
+  auto pack_by_group = [&]() {
+    std::vector<std::vector<U>> per(pg.groups.size());
+    for (const U& un : units_all) per[un.l1].push_back(un);  // already in descending work
+    std::vector<size_t> next(pg.groups.size(), 0);
+    size_t left = units_all.size();
+    std::vector<Cta> out;
+    while (left) {
+      int g = -1;
+      for (size_t l = 0; l < per.size(); ++l)
+        if (next[l] < per[l].size() && (g < 0 || per[l][next[l]].work > per[g][next[g]].work)) g = (int)l;
+      Cta cta;
+      int used = 0;
+      auto take = [&](int l, int n) {
+        cta.team_l1.push_back(l);
+        cta.team_units.emplace_back();
+        for (int i = 0; i < n; ++i) {
+          const U& un = per[l][next[l]++];
+          cta.team_units.back().push_back(un.u);
+          cta.work = std::max(cta.work, un.work);
+        }
+        used += n;
+        left -= n;
+      };
+      take(g, std::min<int>(c.upc, (int)(per[g].size() - next[g])));
+      while (used < c.upc && (int)cta.team_l1.size() < c.nteams) {
+        int best = -1;
+        double best_fill = 0.0;
+        for (size_t l = 0; l < per.size(); ++l) {
+          if (next[l] >= per[l].size() || std::find(cta.team_l1.begin(), cta.team_l1.end(), (int)l) != cta.team_l1.end())
+            continue;
+          double fill = 0.0;
+          for (size_t i = next[l]; i < per[l].size() && (int)(i - next[l]) < c.upc - used; ++i)
+            fill += std::min(per[l][i].work, cta.work);
+          if (fill > best_fill) {
+            best_fill = fill;
+            best = (int)l;
+          }
+        }
+        if (best < 0) break;
+        take(best, std::min<int>(c.upc - used, (int)(per[best].size() - next[best])));
+      }
+      out.push_back(std::move(cta));
+    }
+    return out;
+  };
+  auto cost = [&](const std::vector<Cta>& v) {
+    double s = 0.0;
+    for (const Cta& x : v) s += x.work;
+    return s;
+  };
+  std::vector<Cta> ctas = pack_by_work();
+  if (!std::getenv("BFQ_PACK_WORK")) {
+    std::vector<Cta> alt = pack_by_group();
+    if (cost(alt) < cost(ctas)) ctas.swap(alt);
   }
   // renumber units inside each group in order of appearance
   std::vector<int16_t> new_m1 = pg.unit_m1;
@@ -626,6 +724,20 @@ int build_host_plan(const bfq_desc& d, int smem_limit, HostPlan& hp) {
       }
     }
     hp.sym.exec_macs_per_cell = total;
+  }
+  // useful MACs of the evaluated channels (no padding): what the kernel must do
+  {
+    std::vector<int64_t> chan_rows(d.n_t, 0);
+    for (int64_t z = 0; z < d.n_g; ++z) ++chan_rows[d.tau[z]];
+    double useful = 0.0;
+    for (int t = 0; t < d.n_t; ++t) {
+      const int l1 = hp.triplets[3 * t], l2 = hp.triplets[3 * t + 1], l3 = hp.triplets[3 * t + 2];
+      if (hp.folded && l2 > l3) continue;
+      const bool diag = hp.folded && l2 == l3 && hp.sym.cfg.pairsplit && !std::getenv("BFQ_NO_DIAG");
+      const double kk = diag ? nk * (nk + 1) / 2.0 : (double)nk * nk;
+      useful += (double)chan_rows[t] * kk + (2.0 * l1 + 1.0) * nk * kk;
+    }
+    hp.useful_macs_per_cell = useful;
   }
   hp.alg_flops_per_cell = 2.0 * ((double)d.n_g * nk * nk + (double)d.n_s * nk * nk * nk);
   hp.alg_bytes_per_cell = 16.0 * nk * nq;

@@ -19,10 +19,15 @@
 // independent DMMA chains per warp (ncu at 8 warps: 37% "wait" stalls on the
 // single chain); the second group of an odd tail has g = 0 (fetch_row_bf).
 template <int MT, int CELLS, bool BILIN, int NKT, int QST>
-__global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const KParams p) {
+__global__ void __launch_bounds__(NKT == 17 ? (CELLS == 1 ? 384 : 256) : 512, 1) bfq_q_kernel2(const KParams p) {
   constexpr int M1T = 8 / CELLS;
-  constexpr int HC = CELLS / 2;  // cells per warp in stage 1
-  static_assert(CELLS >= 2, "pair split needs at least two cells per tile");
+  // Stage-1 split of a unit over its two warps: by cells (warp h takes cells
+  // h*HC..h*HC+HC-1, every slice), or -- one cell per tile (SPLITM, n_k = 17:
+  // half the staged cells, room for more units) -- by slices (warp h takes
+  // slices h*MS..h*MS+MS-1 of the single cell).
+  constexpr bool SPLITM = CELLS == 1;
+  constexpr int HC = SPLITM ? 1 : CELLS / 2;  // cells per warp in stage 1
+  constexpr int MS = SPLITM ? M1T / 2 : M1T;  // slices (output columns m1) per warp in stage 1
   constexpr bool FIXED = NKT > 0;
   constexpr int NF = BILIN ? 2 : 1;
   // 8k+1 sizes (n_k = 9, 17): the last radial index is handled by DFMA +
@@ -132,9 +137,10 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
   const bool nowait = (p.debug & 4) != 0;  // do not wait for the R ring (stale R: timing only)
   const bool rowhit = (p.debug & 16) != 0;  // fetch table rows 0..15 only (always L1 hits: timing only)
   const bool nostore = (p.debug & 64) != 0;  // skip the per-slice Phi stores (timing only)
+  const bool nog = (p.debug & 128) != 0;     // skip the g scaling of the A operand (timing only)
 #else
   constexpr bool clk_on = false;  // build with -DBFQ_PHASE_CLOCKS for per-phase cycle counts
-  constexpr bool skip1 = false, skip2 = false, nowait = false, rowhit = false, nostore = false;
+  constexpr bool skip1 = false, skip2 = false, nowait = false, rowhit = false, nostore = false, nog = false;
 #endif
   long long ck_s1 = 0, ck_b1 = 0, ck_w = 0, ck_s2 = 0, ck_b2 = 0, ck0 = clock64(), ckt = ck0;
   auto tick = [&](long long& acc) {
@@ -146,9 +152,11 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
   };
   const Group grp = p.groups[t_l1];
   const int unit = t_ubase + tunit;
-  int m1s[M1T];
+  const int mlb = SPLITM ? h * MS : 0;  // this warp's first slice of the unit
+  const int cb = SPLITM ? 0 : h * HC;    // this warp's first cell of the tile
+  int m1s[MS];
 #pragma unroll
-  for (int ml = 0; ml < M1T; ++ml) m1s[ml] = p.unit_m1[(grp.unit_off + unit) * M1T + ml];
+  for (int ml = 0; ml < MS; ++ml) m1s[ml] = p.unit_m1[(grp.unit_off + unit) * M1T + mlb + ml];
   uint64_t* tfull = full + team * 2;
   int* tarr = arrivals + team * 2;
   const uint32_t ring_u32 = smem_u32(rs + team * NST * rblk);
@@ -159,7 +167,7 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
   const uint32_t fspan = (uint32_t)HC * cell_bytes;
   const uint32_t phu_hi = phu_u32 + (uint32_t)(8 * K2S) * 8u;  // end of this unit's Phi buffer
   {
-    const uint32_t f0 = smem_u32(fs) + (uint32_t)(h * HC) * cell_bytes;  // this warp's first cell
+    const uint32_t f0 = smem_u32(fs) + (uint32_t)cb * cell_bytes;  // this warp's first cell
     const uint32_t f3off = BILIN ? (uint32_t)(CELLS * cell_elems) * 8u : 0u;
 #pragma unroll
     for (int t = 0; t < MT; ++t) {
@@ -185,7 +193,7 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
   auto slice_bounds = [&](int ci, int* zs, int* ze) {
     const ChanEntry ce = p.chans[grp.chan_off + ci];
 #pragma unroll
-    for (int ml = 0; ml < M1T; ++ml) {
+    for (int ml = 0; ml < MS; ++ml) {
       const int m1 = m1s[ml];
       const bool ok = m1 >= 0;
       zs[ml] = ok ? __ldg(p.sstart + ce.slice_base + m1) : 0;
@@ -205,7 +213,7 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
   auto store_phi = [&](int ml, double (&acc)[HC][MT][MT][2], bool dg) {
 #pragma unroll
     for (int cc = 0; cc < HC; ++cc) {
-      const uint32_t ph = phu_u32 + (uint32_t)((ml * CELLS + h * HC + cc) * K2S) * 8u;
+      const uint32_t ph = phu_u32 + (uint32_t)(((mlb + ml) * CELLS + cb + cc) * K2S) * 8u;
 #pragma unroll
       for (int a = 0; a < MTM; ++a)
 #pragma unroll
@@ -226,7 +234,7 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
     }
   };
 
-  int zs_n[M1T], ze_n[M1T], zs_nn[M1T], ze_nn[M1T];
+  int zs_n[MS], ze_n[MS], zs_nn[MS], ze_nn[MS];
   slice_bounds(0, zs_n, ze_n);
   if (nch > 1) slice_bounds(1, zs_nn, ze_nn);
   // slices are padded to whole k-steps with g = 0 rows (bfq_plan.cpp), and a
@@ -238,19 +246,23 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
   Row nxt_row = fetch_rb(zs_n[0] + kq, ze_n[0]);
   // DUAL: the second row group of the next iteration, also one iteration ahead
   // (rows of a 600k-row table miss L1; ncu showed long-scoreboard stalls on it)
+#ifdef BFQ_EXPERIMENT
+  constexpr bool DUALK = NKT == 17 && !SPLITM;
+#else
   constexpr bool DUALK = NKT == 17;
+#endif
   Row nxt_b = DUALK ? fetch_rb(zs_n[0] + 4 + kq, ze_n[0]) : nxt_row;
 
   for (int i = 0; i < nch; ++i) {
-    int zs[M1T], ze[M1T];
+    int zs[MS], ze[MS];
 #pragma unroll
-    for (int ml = 0; ml < M1T; ++ml) {
+    for (int ml = 0; ml < MS; ++ml) {
       zs[ml] = zs_n[ml];
       ze[ml] = ze_n[ml];
     }
     if (i + 1 < nch) {
 #pragma unroll
-      for (int ml = 0; ml < M1T; ++ml) {
+      for (int ml = 0; ml < MS; ++ml) {
         zs_n[ml] = zs_nn[ml];
         ze_n[ml] = ze_nn[ml];
       }
@@ -259,9 +271,9 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
     const bool dg = (ctau[team * p.max_chan + i] & 1) != 0;
     auto stage1 = [&](auto dgtag) {
       constexpr bool DGC = decltype(dgtag)::value;
-      // ---- stage 1: Phi of this warp's HC cells for the unit's M1T columns
+      // ---- stage 1: Phi of this warp's HC cells for its MS columns
 #pragma unroll
-      for (int ml = 0; ml < M1T; ++ml) {
+      for (int ml = 0; ml < MS; ++ml) {
         double acc[HC][MT][MT][2];
         double xr[HC][MTM], xc[HC][MTM], xd[HC];  // X1: row / column / corner of index n_k-1
 #pragma unroll
@@ -274,7 +286,11 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
           for (int t = 0; t < MTM; ++t) xr[cc][t] = xc[cc][t] = 0.0;
           xd[cc] = 0.0;
         }
+#ifdef BFQ_EXPERIMENT
+        constexpr bool DUAL = NKT == 17 && !SPLITM;  // A/B: single row group with more warps
+#else
         constexpr bool DUAL = NKT == 17;
+#endif
         double acc2[DUAL ? HC : 1][MT][MT][2];
         if constexpr (DUAL) {
 #pragma unroll
@@ -291,7 +307,8 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
             double av[MT], bv[MT];
 #pragma unroll
             for (int t = 0; t < MTM; ++t) {
-              av[t] = rw.g * lds_ro(BFQ_CHK(fa[t] + qa + cc * cell_bytes, fa_lo, fa_lo + fspan, CHK_F2));
+              const double fv = lds_ro(BFQ_CHK(fa[t] + qa + cc * cell_bytes, fa_lo, fa_lo + fspan, CHK_F2));
+              av[t] = nog ? fv : rw.g * fv;
               bv[t] = lds_ro(BFQ_CHK(fb[t] + qb + cc * cell_bytes, fb_lo, fb_lo + fspan, CHK_F3));
             }
 #pragma unroll
@@ -312,8 +329,8 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
             }
           }
         };
-        const int zn = ml + 1 < M1T ? zs[ml + 1 < M1T ? ml + 1 : ml] : zs_n[0];
-        const int en = ml + 1 < M1T ? ze[ml + 1 < M1T ? ml + 1 : ml] : (i + 1 < nch ? ze_n[0] : 0);
+        const int zn = ml + 1 < MS ? zs[ml + 1 < MS ? ml + 1 : ml] : zs_n[0];
+        const int en = ml + 1 < MS ? ze[ml + 1 < MS ? ml + 1 : ml] : (i + 1 < nch ? ze_n[0] : 0);
         if constexpr (DUAL) {
           for (int z0 = zs[ml]; z0 < (skip1 ? zs[ml] : ze[ml]); z0 += 8) {
             const Row rwa = nxt_row;
@@ -342,10 +359,10 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
           }
         }
         if (zs[ml] >= ze[ml]) {
-          if (ml + 1 < M1T) nxt_row = fetch_rb(zs[ml + 1 < M1T ? ml + 1 : ml] + kq, ze[ml + 1 < M1T ? ml + 1 : ml]);
+          if (ml + 1 < MS) nxt_row = fetch_rb(zs[ml + 1 < MS ? ml + 1 : ml] + kq, ze[ml + 1 < MS ? ml + 1 : ml]);
           else nxt_row = fetch_rb(zs_n[0] + kq, i + 1 < nch ? ze_n[0] : 0);
           if constexpr (DUALK) {
-            if (ml + 1 < M1T) nxt_b = fetch_rb(zs[ml + 1 < M1T ? ml + 1 : ml] + 4 + kq, ze[ml + 1 < M1T ? ml + 1 : ml]);
+            if (ml + 1 < MS) nxt_b = fetch_rb(zs[ml + 1 < MS ? ml + 1 : ml] + 4 + kq, ze[ml + 1 < MS ? ml + 1 : ml]);
             else nxt_b = fetch_rb(zs_n[0] + 4 + kq, i + 1 < nch ? ze_n[0] : 0);
           }
         }
@@ -364,7 +381,7 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
             }
             xd[cc] += __shfl_xor_sync(0xffffffffu, xd[cc], 1);
             xd[cc] += __shfl_xor_sync(0xffffffffu, xd[cc], 2);
-            const uint32_t ph = phu_u32 + (uint32_t)((ml * CELLS + h * HC + cc) * K2S) * 8u;
+            const uint32_t ph = phu_u32 + (uint32_t)(((mlb + ml) * CELLS + cb + cc) * K2S) * 8u;
             // store-order K of row / column L = n_k - 1 = 8 (MT - 1): tile row or
             // column MT - 1 holds one index (r0 = 0 or kq = e = 0)
             constexpr int L = NKT - 1, TL = MT - 1;
@@ -463,10 +480,10 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
       // the same).  Unused K padding keeps its zeros, so a correct schedule
       // is unaffected: 1e300 x 0 = 0.
 #pragma unroll 1
-      for (int ml = 0; ml < (i + 1 < nch ? M1T : 0); ++ml)  // not after the last channel: the
+      for (int ml = 0; ml < (i + 1 < nch ? MS : 0); ++ml)  // not after the last channel: the
 #pragma unroll 1                                           // epilogue reuses the buffer
         for (int cc = 0; cc < HC; ++cc) {
-          const uint32_t ph = phu_u32 + (uint32_t)((ml * CELLS + h * HC + cc) * K2S) * 8u;
+          const uint32_t ph = phu_u32 + (uint32_t)(((mlb + ml) * CELLS + cb + cc) * K2S) * 8u;
           for (int e = lane; e < NK * NK; e += 32) sts_v(ph + (uint32_t)e * 8u, 1e300);
         }
       __syncwarp();
@@ -520,9 +537,13 @@ __global__ void __launch_bounds__(NKT == 17 ? 256 : 512, 1) bfq_q_kernel2(const 
   if (h == 1) return;
   const int ml = r0 / CELLS, c = r0 - ml * CELLS;
   int m1 = -1;
+  if constexpr (SPLITM) {
+    m1 = p.unit_m1[(grp.unit_off + unit) * M1T + ml];  // all M1T slices (warp 0 staged only its own)
+  } else {
 #pragma unroll
-  for (int t = 0; t < M1T; ++t)
-    if (t == ml) m1 = m1s[t];
+    for (int t = 0; t < M1T; ++t)
+      if (t == ml) m1 = m1s[t];
+  }
   const long long cell = tile * CELLS + c;
   if (m1 >= 0 && cell < p.n_cells) {
     const int l1 = grp.l1, q1 = l1 * l1 + m1;
