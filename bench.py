@@ -53,6 +53,10 @@ RBUILD = {
     "rbuild12": (12, 12, 1.0),
     "rbuild16": (16, 16, 1.0),
 }
+# the general projection basis.project(f, cfg, order) of
+# sampled distributions.  One step = one projection of every cell's samples.
+PROJ = {"proj12": (12, 12, 64, 4096), "proj8": (8, 8, 32, 16384)}
+PROJ_METRIC = "projected cells/s (fp64 basis.project of sampled f, quadrature order as configured)"
 METRIC = "Q(f,f) cell-evals/s (fp64, hard spheres L=N=12) and FP64/HBM roofline frac"
 RBUILD_METRIC = "R-tensor assembly channel integrals/s (fp64, hard spheres, pad 16/16)"
 FP64_PEAK_TFLOPS = 37.1  # DMMA.8x8x4 sustained, measured on this pool (profiles/fp64_peak.txt)
@@ -342,6 +346,42 @@ def run_reference(args, rank, world):
             "e2e": {"value": v, "unit": "channels/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         }), flush=True)
         return
+    if args.config in PROJ:  # the reference's basis.project einsums on sampled f, all host cores
+        import multiprocessing as mp
+
+        import numpy as np
+
+        from paper_2605_28475_b200 import project as gproject
+        from paper_2605_28475_b200.operator import SpectralConfig
+
+        k, l, order, _ = PROJ[args.config]
+        cfg = SpectralConfig(k, l, 1.0)
+        pts = gproject.project_points(cfg, order)
+        cores = os.cpu_count() or 1
+        rng = np.random.default_rng(args.seed)
+        u = rng.uniform(-0.3, 0.3, size=(cores, 3))
+        t = rng.uniform(0.8, 1.2, size=cores)
+        hs = np.stack([(2 * np.pi * t[i]) ** -1.5 * np.exp(-np.sum((pts - u[i]) ** 2, axis=1) / (2 * t[i]))
+                       for i in range(cores)])
+        rates, walls = [], []
+        with mp.get_context("spawn").Pool(cores) as pool:
+            for _ in range(args.steps):
+                t0 = time.perf_counter()
+                res = pool.map(_proj_worker, [(k, l, order, hs[i:i + 1]) for i in range(cores)])
+                walls.append(time.perf_counter() - t0)
+                rates.append(cores / max(r[1] for r in res))
+        v = statistics.median(rates)
+        print(json.dumps({
+            "impl": "reference", "metric": PROJ_METRIC, "value": v, "unit": "cells/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(walls),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic drifting Maxwellians sampled on the host",
+            "config": {"workload": f"basis.project of sampled f, N={k} L={l}, radial order {order}"},
+            "cpu_baseline": {"value": v, "unit": "cells/s", "cores": cores, "kind": "port",
+                             "sample": "one cell per core per step (oracle/project_oracle.py)", "cpu": cpu_model()},
+            "e2e": {"value": v, "unit": "cells/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }), flush=True)
+        return
     opfile, n_global, _, desc, _ = CONFIGS[args.config]
     from paper_2605_28475_b200.operator import load_cache
 
@@ -471,6 +511,152 @@ def run_rbuild(args, rank, world, local_rank):
                                 "sample": f"{cpu['channels']} random channels, one per core (oracle port of "
                                           "kinematic channel_half, 1 thread per process)"}
     print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def _proj_worker(args):
+    """Oracle restatement of basis.project on sampled f, one process (CPU baseline)."""
+    k, l, order, samples = args
+    from oracle.project_oracle import ProjectionOracle
+    from paper_2605_28475_b200 import project as gproject
+
+    try:
+        from threadpoolctl import threadpool_limits
+    except ImportError:  # pragma: no cover
+        threadpool_limits = None
+    ctx = threadpool_limits(limits=1) if threadpool_limits else None
+    if ctx:
+        ctx.__enter__()
+    orc = ProjectionOracle(k, l, gproject.projection_grid(l, order))
+    t0 = time.perf_counter()
+    out = [orc.project(s) for s in samples]
+    dt = time.perf_counter() - t0
+    if ctx:
+        ctx.__exit__(None, None, None)
+    return out, dt
+
+
+def run_project(args, rank, world, local_rank):
+    """General projection on the GPU (bfq_project_samples).  Replicas on N GPUs
+    (each projects its own batch); samples are drifting Maxwellians evaluated
+    on the device at the reference's quadrature points (generation outside
+    the timed region), checked against the closed-form projection."""
+    import numpy as np
+    import torch
+
+    from paper_2605_28475_b200 import inputs
+    from paper_2605_28475_b200 import project as gproject
+    from paper_2605_28475_b200.operator import SpectralConfig
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    k, l, order, n = PROJ[args.config]
+    if args.cells:
+        n = args.cells
+    cfg = SpectralConfig(k, l, 1.0)
+    pj = gproject.Projector(cfg, order, local_rank)
+    pts = torch.from_numpy(gproject.project_points(cfg, order)).to(dev)
+    rng = np.random.default_rng(args.seed + rank)
+    u = rng.uniform(-0.3, 0.3, size=(n, 3))
+    t = rng.uniform(0.8, 1.2, size=n)
+    samples = torch.empty((n, pj.n_points), dtype=torch.float64, device=dev)
+    ut, tt = torch.from_numpy(u).to(dev), torch.from_numpy(t).to(dev)
+    for i in range(0, n, 64):
+        d2 = ((pts[None, :, :] - ut[i:i + 64, None, :]) ** 2).sum(-1)
+        samples[i:i + 64] = (2 * np.pi * tt[i:i + 64, None]) ** -1.5 * torch.exp(-d2 / (2 * tt[i:i + 64, None]))
+    out = torch.empty((n, cfg.n_k, cfg.n_q), dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(max(args.warmup, 0)):
+        pj.project(samples, out)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    with ClockSampler(local_rank) as clk:
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        for i in range(args.steps):
+            starts[i].record(stream)
+            pj.project(samples, out)
+            ends[i].record(stream)
+            clk.sample()
+        clk.sample()
+        torch.cuda.synchronize(dev)
+    step_ms = [a.elapsed_time(b) for a, b in zip(starts, ends)]
+    total_ms = starts[0].elapsed_time(ends[-1])
+    tm = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if dist is not None:
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+    total_ms = float(tm[0])
+    # parity: closed-form projection of the same drifting Maxwellians
+    idx = stratified_indices(n, 64)
+    got = out[torch.from_numpy(idx).to(dev)].cpu().numpy()
+    ref = inputs.project_maxwellians(cfg.n_k, cfg.l_max, u[idx], t[idx])
+    errs = [float(np.max(np.abs(got[j] - ref[j])) / np.max(np.abs(ref[j]))) for j in range(len(idx))]
+    # end to end: samples from pinned host memory, projection, coefficients back
+    e2e = None
+    if args.e2e_steps != 0:
+        nh = min(n, 512)
+        hin = samples[:nh].cpu().pin_memory()
+        hout = torch.empty((nh, cfg.n_k, cfg.n_q), dtype=torch.float64).pin_memory()
+        dbuf = torch.empty_like(samples[:nh])
+        dout = torch.empty_like(out[:nh])
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        ne = 3
+        for _ in range(ne):
+            dbuf.copy_(hin, non_blocking=True)
+            pj.project(dbuf, dout)
+            hout.copy_(dout, non_blocking=True)
+        torch.cuda.synchronize(dev)
+        el = time.perf_counter() - t0
+        e2e = {"value": nh * ne * world / el, "unit": "cells/s", "h2d_bytes_per_step": hin.numel() * 8,
+               "d2h_bytes_per_step": hout.numel() * 8, "steps": ne, "cells_per_step": nh,
+               "path": "pinned host samples -> H2D -> bfq_project_samples -> D2H (PCIe-bound: "
+                       f"{pj.n_points * 8 / 1e6:.1f} MB of samples per cell)"}
+    if rank == 0:
+        kern_s = statistics.mean(step_ms) / 1e3
+        gbs = pj.bytes_per_cell * n / kern_s / 1e9
+        tfs = pj.flops_per_cell * n / kern_s / 1e12
+        hbm = measured_peaks().get("hbm_gbs", 6537.3)
+        line = {
+            "metric": PROJ_METRIC, "value": n * world * args.steps / (total_ms / 1e3), "unit": "cells/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: drifting Maxwellians (u ~ U(-0.3,0.3)^3, T ~ U(0.8,1.2)) sampled on the device",
+            "config": {"workload": f"basis.project of sampled f, N={k} L={l}, radial order {order} "
+                                   f"({pj.n_v}x{pj.n_t}x{pj.n_p} points per cell)", "cells_per_gpu": n,
+                       "l2": f"inputs larger than L2 ({n * pj.n_points * 8 / 1e9:.1f} GB per GPU)"},
+            "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
+                         "traffic": None, "kernel": "k_project_samples (DMMA azimuthal GEMM + polar/radial sums)",
+                         "bytes_per_cell": pj.bytes_per_cell, "flops_per_cell": pj.flops_per_cell,
+                         "fp64_tflops": tfs, "fp64_frac": tfs / FP64_PEAK_TFLOPS,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
+            "e2e": e2e, "gpu_launches": args.steps, "clocks": clk.summary(),
+            "parity": {"cells": int(len(idx)), "max_rel_err": max(errs), "bar": 1e-12,
+                       "pass": bool(max(errs) <= 1e-12),
+                       "against": "closed-form projection of the same Maxwellians (bfq_project_maxwellians path, "
+                                  "itself pinned to the reference's project)"},
+        }
+        if world == 1 and not args.no_cpu:
+            import multiprocessing as mp
+
+            cores = os.cpu_count() or 1
+            m = min(n, 2 * cores)
+            hs = samples[:m].cpu().numpy()
+            chunks = [(k, l, order, hs[i::cores]) for i in range(cores) if len(hs[i::cores])]
+            with mp.get_context("spawn").Pool(len(chunks)) as pool:
+                res = pool.map(_proj_worker, chunks)
+            busy = max(r[1] for r in res)
+            line["cpu_baseline"] = {"value": m / busy, "unit": "cells/s", "cores": len(chunks), "kind": "port",
+                                    "sample": f"{m} cells' samples, 2 per process (oracle/project_oracle.py: "
+                                              "basis.project's einsums on the sampled grid)", "cpu": cpu_model()}
+        print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
 
@@ -751,7 +937,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="hs12", choices=sorted(CONFIGS) + sorted(RBUILD))
+    ap.add_argument("--config", default="hs12", choices=sorted(CONFIGS) + sorted(RBUILD) + sorted(PROJ))
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
                     help="strong: one fixed global batch sharded over the GPUs (BASELINE config 3); "
                          "weak: the batch per GPU")
@@ -776,6 +962,8 @@ def main():
         run_reference(args, rank, world)
     elif args.config in RBUILD:
         run_rbuild(args, rank, world, local_rank)
+    elif args.config in PROJ:
+        run_project(args, rank, world, local_rank)
     else:
         run_ours(args, rank, world, local_rank)
 

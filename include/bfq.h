@@ -21,6 +21,8 @@
  *   bfq_project_maxwellians <- basis.project(M_{u,T}, cfg, order) batched over
  *                            drifting Maxwellians (basis.py:262-299), closed
  *                            angular form (input generator of configs 2-5)
+ *   bfq_projector_* / bfq_project_samples <- basis.project(f, cfg, order) for
+ *                            any f sampled on the reference's quadrature grid
  *
  * Conventions: plain pointers and sizes, no torch types.  Every function returns
  * 0 on success and a negative BFQ_E* code otherwise; bfq_strerror() maps a code
@@ -143,6 +145,27 @@ int bfq_moments(const bfq_plan* plan, const double* c, double* out, int64_t n_ce
 int bfq_project_maxwellians(int32_t k_max, int32_t l_max, const double* rule_x, const double* rule_w,
                             int32_t n_rule, const double* u, const double* temp, const double* noise,
                             double* out, int64_t n, void* stream);
+
+/* General batched projection basis.project(f, cfg, order) (basis.py:262-299)
+ * of distributions SAMPLED on the reference's product grid: n_v radial
+ * (generalised Gauss-Laguerre) x n_t polar (Gauss-Legendre) x n_p azimuthal
+ * (periodic trapezoid) nodes, point order (v, t, p) with p fastest
+ * (basis.py:284-290).  The projector owns device copies of the HOST tables
+ * that carry the rule weights:
+ *   phi_tab    [2 l_max + 1][n_p]  w_p x {1 (row 0), sin(m phi) (row 2m-1), cos(m phi) (row 2m)}
+ *   theta_tab  [(l_max+1)(l_max+2)/2][n_t]  w_t x (-1)^m sqrt2 (m > 0) x N_lm P_l^m(cos t), row l(l+1)/2 + m
+ *   radial_tab [l_max + 1][k_max + 1][n_v]  phi_kl(v) x the radial weight
+ * bfq_project_samples maps samples [n][n_v][n_t][n_p] (DEVICE) to
+ * out [n][n_k][n_q] (DEVICE), stream-ordered, one CTA per cell. */
+typedef struct bfq_projector bfq_projector;
+int bfq_projector_create(int32_t k_max, int32_t l_max, int32_t n_v, int32_t n_t, int32_t n_p,
+                         const double* phi_tab, const double* theta_tab, const double* radial_tab, int device,
+                         bfq_projector** out);
+int bfq_project_samples(const bfq_projector* proj, const double* samples, double* out, int64_t n, void* stream);
+int bfq_projector_destroy(bfq_projector* proj);
+/* Algorithmic work per cell: flops of the azimuthal, polar and radial sums;
+ * bytes = the samples read + the coefficients written. */
+int bfq_projector_work(const bfq_projector* proj, double* flops_per_cell, double* bytes_per_cell);
 
 /* Diagnostic: validate `desc` and build the host-side plan (folding check,
  * tiling, CTA schedule) WITHOUT touching a GPU; fills `info` as

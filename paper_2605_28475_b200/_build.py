@@ -33,7 +33,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-Xptxas", "-v"]
 SOURCES = [
-    "bfq_cuda.cu", "bfq_plan.cpp", "bfr_build.cu", "bfq_project.cu",
+    "bfq_cuda.cu", "bfq_plan.cpp", "bfr_build.cu", "bfq_project.cu", "bfq_project_samples.cu",
     "bfq_inst_n5.cu", "bfq_inst_n9.cu", "bfq_inst_n11.cu", "bfq_inst_n13.cu", "bfq_inst_n17.cu",
     "bfq_inst_generic.cu",
 ]

@@ -45,6 +45,10 @@ EXPORTED_SYMBOLS = (
     "bfq_moments",
     "bfq_host_plan_info",
     "bfq_project_maxwellians",
+    "bfq_projector_create",
+    "bfq_project_samples",
+    "bfq_projector_destroy",
+    "bfq_projector_work",
     "bfq_strerror",
     "bfq_last_error",
     "bfq_build_id",
@@ -172,6 +176,11 @@ def _declare(lib):
     lib.bfq_build_id.restype = ctypes.c_char_p
     lib.bfq_project_maxwellians.argtypes = [ctypes.c_int32, ctypes.c_int32, _f64p, _f64p, ctypes.c_int32, vp, vp, vp,
                                             vp, ctypes.c_int64, vp]
+    lib.bfq_projector_create.argtypes = [ctypes.c_int32] * 5 + [_f64p, _f64p, _f64p, ctypes.c_int,
+                                                                 ctypes.POINTER(ctypes.c_void_p)]
+    lib.bfq_project_samples.argtypes = [vp, vp, vp, ctypes.c_int64, vp]
+    lib.bfq_projector_destroy.argtypes = [vp]
+    lib.bfq_projector_work.argtypes = [vp, _f64p, _f64p]
     lib.bfr_assemble.argtypes = [ctypes.POINTER(BfrDesc), ctypes.c_int, vp, vp, ctypes.POINTER(BfrStats)]
     for name in EXPORTED_SYMBOLS + EXPORTED_SYMBOLS_BFR:
         if name not in ("bfq_strerror", "bfq_last_error", "bfq_build_id"):

@@ -246,11 +246,7 @@ __global__ void __launch_bounds__(NKT == 17 ? (CELLS == 1 ? 384 : 256) : 512, 1)
   Row nxt_row = fetch_rb(zs_n[0] + kq, ze_n[0]);
   // DUAL: the second row group of the next iteration, also one iteration ahead
   // (rows of a 600k-row table miss L1; ncu showed long-scoreboard stalls on it)
-#ifdef BFQ_EXPERIMENT
-  constexpr bool DUALK = NKT == 17 && !SPLITM;
-#else
   constexpr bool DUALK = NKT == 17;
-#endif
   Row nxt_b = DUALK ? fetch_rb(zs_n[0] + 4 + kq, ze_n[0]) : nxt_row;
 
   for (int i = 0; i < nch; ++i) {
@@ -286,11 +282,7 @@ __global__ void __launch_bounds__(NKT == 17 ? (CELLS == 1 ? 384 : 256) : 512, 1)
           for (int t = 0; t < MTM; ++t) xr[cc][t] = xc[cc][t] = 0.0;
           xd[cc] = 0.0;
         }
-#ifdef BFQ_EXPERIMENT
-        constexpr bool DUAL = NKT == 17 && !SPLITM;  // A/B: single row group with more warps
-#else
-        constexpr bool DUAL = NKT == 17;
-#endif
+        constexpr bool DUAL = NKT == 17;  // also with SPLITM: without it 7.5% slower (r02_ab_xsh_dual.txt)
         double acc2[DUAL ? HC : 1][MT][MT][2];
         if constexpr (DUAL) {
 #pragma unroll
@@ -317,9 +309,10 @@ __global__ void __launch_bounds__(NKT == 17 ? (CELLS == 1 ? 384 : 256) : 512, 1)
               for (int b = 0; b < MTM; ++b)
                 if (b >= a || !DGC) dmma884(ac[cc][a][b][0], ac[cc][a][b][1], av[a], bv[b]);
             if constexpr (X1) {
-              const double ea =
-                  rw.g * lds_ro(BFQ_CHK(fx_a + qa + cc * cell_bytes, fa_lo, fa_lo + fspan, CHK_F2));  // g f2[n_k-1, q2]
-              const double eb = lds_ro(BFQ_CHK(fx_b + qb + cc * cell_bytes, fb_lo, fb_lo + fspan, CHK_F3));  // f3[n_k-1, q3]
+              // g f2[n_k-1, q2], f3[n_k-1, q3] of this lane's row kq, cell cc (broadcast
+              // loads; one gather + shuffles measured 3.5% slower, profiles/r02_ab_xsh_dual.txt)
+              const double ea = rw.g * lds_ro(BFQ_CHK(fx_a + qa + cc * cell_bytes, fa_lo, fa_lo + fspan, CHK_F2));
+              const double eb = lds_ro(BFQ_CHK(fx_b + qb + cc * cell_bytes, fb_lo, fb_lo + fspan, CHK_F3));
 #pragma unroll
               for (int t = 0; t < MTM; ++t) {
                 if (!DGC) xr[cc][t] = fma(ea, bv[t], xr[cc][t]);

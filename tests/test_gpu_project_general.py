@@ -1,0 +1,84 @@
+"""General batched projection on the GPU (bfq_project_samples, csrc/
+bfq_project_samples.cu) against the live reference's basis.project(f, cfg,
+order) outputs (tests/golden/project_general.npz, make_project_golden.py) and
+against the closed-form projection of drifting Maxwellians; the single-cell
+drop-in project(f, cfg, order); determinism and argument validation."""
+
+import os
+import sys
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+sys.path.insert(0, GOLDEN)
+from project_funcs import CASES, FUNCS  # noqa: E402
+
+from paper_2605_28475_b200 import inputs  # noqa: E402
+from paper_2605_28475_b200 import project as gproject  # noqa: E402
+from paper_2605_28475_b200.operator import CoefficientField, SpectralConfig  # noqa: E402
+
+GOLD = np.load(os.path.join(GOLDEN, "project_general.npz"))
+
+
+def rel(a, b):
+    return float(np.max(np.abs(a - b)) / np.max(np.abs(b)))
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_batch_matches_reference_project(case):
+    k, l, order = case
+    cfg = SpectralConfig(k, l, 1.0)
+    pts = gproject.project_points(cfg, order)
+    names = sorted(FUNCS)
+    samples = np.stack([FUNCS[n](pts) for n in names] * 3)  # 3 copies: ragged-free batch of 9
+    pj = gproject.Projector(cfg, order)
+    got = pj.project(torch.from_numpy(samples).cuda()).cpu().numpy()
+    for i, n in enumerate(names * 3):
+        assert rel(got[i], GOLD[f"{n}_k{k}_l{l}_o{order}"]) <= 1e-13, (n, i)
+    # bitwise deterministic and position independent
+    again = pj.project(torch.from_numpy(samples[::-1].copy()).cuda()).cpu().numpy()[::-1]
+    assert np.array_equal(got, again)
+
+
+def test_maxwellians_match_closed_form():
+    cfg = SpectralConfig(12, 12, 1.0)
+    order = 64
+    pts = torch.from_numpy(gproject.project_points(cfg, order)).cuda()
+    rng = np.random.default_rng(3)
+    n = 37
+    u = rng.uniform(-0.3, 0.3, size=(n, 3))
+    t = rng.uniform(0.8, 1.2, size=n)
+    ut, tt = torch.from_numpy(u).cuda(), torch.from_numpy(t).cuda()
+    d2 = ((pts[None, :, :] - ut[:, None, :]) ** 2).sum(-1)
+    samples = (2 * np.pi * tt[:, None]) ** -1.5 * torch.exp(-d2 / (2 * tt[:, None]))
+    got = gproject.Projector(cfg, order).project(samples.contiguous()).cpu().numpy()
+    ref = inputs.project_maxwellians(cfg.n_k, cfg.l_max, u, t)
+    for i in range(n):
+        assert rel(got[i], ref[i]) <= 1e-12, i
+
+
+def test_single_cell_dropin():
+    cfg = SpectralConfig(8, 8, 1.0)
+    c = gproject.project(FUNCS["quartic"], cfg, 32)
+    assert isinstance(c, CoefficientField)
+    assert rel(c.values, GOLD["quartic_k8_l8_o32"]) <= 1e-13
+
+
+def test_validation():
+    cfg = SpectralConfig(4, 4, 1.0)
+    pj = gproject.Projector(cfg, 16)
+    with pytest.raises(ValueError):
+        pj.project(torch.zeros((2, pj.n_points + 1), dtype=torch.float64, device="cuda"))
+    with pytest.raises(ValueError):
+        pj.project(torch.zeros((2, pj.n_points), dtype=torch.float32, device="cuda"))
+    with pytest.raises(ValueError):
+        pj.project(torch.zeros((2, pj.n_points), dtype=torch.float64))
+    assert pj.project(torch.zeros((0, pj.n_points), dtype=torch.float64, device="cuda")).shape == (0, 5, 25)

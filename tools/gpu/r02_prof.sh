@@ -8,7 +8,7 @@ for spec in $PROFS; do
   op=${spec%%:*}; n=${spec##*:}
   tag=${TAG:-}$op
   timeout 300 python tools/prof_q.py --op $op --cells $n > $OUT/prof_$tag.log 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:bfq_q_kernel -s 2 -c 1 \
+  timeout 900 ncu -f --set full --clock-control none --import-source on -k regex:bfq_q_kernel -s 2 -c 1 \
      -o /tmp/ncurep/prof_$tag python tools/prof_q.py --op $op --cells $n > $OUT/ncu_$tag.log 2>&1
   if [ -f /tmp/ncurep/prof_$tag.ncu-rep ]; then
     python tools/ncu_summary.py /tmp/ncurep/prof_$tag.ncu-rep > $OUT/ncu_sum_$tag.txt 2>&1

@@ -16,6 +16,7 @@ ap.add_argument("--op", default="hs_n8")
 ap.add_argument("--cells", type=int, default=8192)
 ap.add_argument("--iters", type=int, default=4)
 ap.add_argument("--bilinear", action="store_true")
+ap.add_argument("--check", type=int, default=0, help="compare this many cells with the CPU oracle")
 a = ap.parse_args()
 path = os.path.join(ROOT, "operators", a.op + ".bfct")
 if os.path.exists(path):
@@ -57,3 +58,18 @@ if os.environ.get("BFQ_DEBUG", "0") != "0" and int(os.environ["BFQ_DEBUG"]) & 8:
     tot = buf[len(names) - 1]
     print("phase cycles per warp (avg over %d warps):" % n, {k: round(buf[j] / n) for j, k in enumerate(names)})
     print("shares:", {k: round(100.0 * buf[j] / max(tot, 1), 1) for j, k in enumerate(names[:-1])})
+
+if a.check:
+    import numpy as np
+
+    from oracle import q_oracle
+
+    oop = q_oracle.OracleOperator.from_operator(op)
+    ws = q_oracle.angular_workspace(oop)
+    qh = q.cpu().numpy()
+    idx = np.unique(np.linspace(0, a.cells - 1, a.check).round().astype(int))
+    c3 = f3.cpu().numpy() if f3 is not None else cells
+    errs = [q_oracle.rel_err(qh[i], q_oracle.q_angular_first(oop, cells[i], c3[i] if a.bilinear else None,
+                                                             workspace=ws)) for i in idx]
+    print(f"check: {len(idx)} cells, max rel err {max(errs):.3e}", "OK" if max(errs) <= 1e-12 else "FAIL")
+

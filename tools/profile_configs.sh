@@ -11,7 +11,7 @@ done
 for spec in $PROFS; do
   op=${spec%%:*}; n=${spec##*:}
   timeout 300 python tools/prof_q.py --op $op --cells $n > $OUT/prof_$op.log 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:bfq_q_kernel -s 2 -c 1 \
+  timeout 900 ncu -f --set full --clock-control none --import-source on -k regex:bfq_q_kernel -s 2 -c 1 \
      -o /tmp/ncurep/prof_$op python tools/prof_q.py --op $op --cells $n > $OUT/ncu_$op.log 2>&1
   if [ -f /tmp/ncurep/prof_$op.ncu-rep ]; then
     python tools/ncu_summary.py /tmp/ncurep/prof_$op.ncu-rep > $OUT/ncu_sum_$op.txt 2>&1
