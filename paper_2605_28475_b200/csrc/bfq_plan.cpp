@@ -616,6 +616,47 @@ int build_host_plan(const bfq_desc& d, int smem_limit, HostPlan& hp) {
   }
   hp.folded = fold;
 
+  // Half-row slices of the self-symmetric channels (l2 == l3) for the folded
+  // program.  Their rows come in mirror pairs (q2, q3) / (q3, q2) with equal g
+  // (verified by the fold check), and R[k,a,b] = R[k,b,a], so
+  //   sum_ab R[ab] Phi[ab] = sum_ab R[ab] Phi''[ab],
+  //   Phi'' = sum_{q2 < q3} 2g f[a,q2] f[b,q3] + sum_{q2 = q3} g f[a,q] f[b,q]
+  // (Phi = Phi' + Phi'^T with Phi' the half-row sum): half the stage-1 rows, at
+  // the price of the full K = n_k^2 in stage 2 instead of the packed triangle
+  // (the diag path below).  Measured (profiles/r02_half_diag.txt): N=L=8 +0.4%,
+  // N=L=12 +1.2%, N=L=16 +3.1%.  BFQ_HALF_DIAG=0 restores the packed path.
+  std::vector<int32_t> half_base(d.n_t, -1);
+  {
+    bool half = fold;
+    if (const char* e = std::getenv("BFQ_HALF_DIAG")) half = fold && std::atoi(e) != 0;
+    if (half) {
+      const int padm = nk == 17 ? 8 : 4;
+      hp.rows.resize(hp.rows.size() - 2 * padm);  // drop the tail, re-added below
+      for (int t = 0; t < d.n_t; ++t) {
+        const int l1 = hp.triplets[3 * t], l2 = hp.triplets[3 * t + 1], l3 = hp.triplets[3 * t + 2];
+        if (l2 != l3) continue;
+        half_base[t] = (int32_t)hp.sstart.size() - 1;  // its first slice starts at the current end
+        for (int m1 = 0; m1 < 2 * l1 + 1; ++m1) {
+          const int32_t a = hp.sstart[hp.chan_sbase[t] + m1], b = hp.sstart[hp.chan_sbase[t] + m1 + 1];
+          const int64_t start = (int64_t)hp.rows.size();
+          for (int32_t z = a; z < b; ++z) {
+            const Row r = hp.rows[z];
+            if (r.g == 0.0 && r.q2 == 0 && r.q3 == 0) continue;  // slice padding
+            if (r.q2 < r.q3) hp.rows.push_back(Row{r.q2, r.q3, 2.0 * r.g});
+            else if (r.q2 == r.q3) hp.rows.push_back(r);
+          }
+          if (!std::getenv("BFQ_NO_ROW_REORDER")) {
+            const int64_t bounds[2] = {start, (int64_t)hp.rows.size()};
+            reorder_rows_for_banks(hp, bounds, 1);
+          }
+          while ((hp.rows.size() - start) % padm) hp.rows.push_back(Row{0, 0, 0.0});
+          hp.sstart.push_back((int32_t)hp.rows.size());
+        }
+      }
+      for (int i = 0; i < 2 * padm; ++i) hp.rows.push_back(Row{0, 0, 0.0});
+    }
+  }
+
   // channel programs, grouped by l1 (output columns)
   auto make_program = [&](Program& pg, bool bilinear, bool use_fold) -> bool {
     pg.bilinear = bilinear;
@@ -628,12 +669,13 @@ int build_host_plan(const bfq_desc& d, int smem_limit, HostPlan& hp) {
       for (int t = 0; t < d.n_t; ++t) {
         if (hp.triplets[3 * t] != l1) continue;
         const int l2 = hp.triplets[3 * t + 1], l3 = hp.triplets[3 * t + 2];
-        int w2 = 0;
+        int w2 = 0, base = hp.chan_sbase[t];
         if (use_fold) {
           if (l2 > l3) continue;
           w2 = l2 < l3 ? 1 : 0;
+          if (half_base[t] >= 0) base = half_base[t];
         }
-        pg.chans.push_back(ChanEntry{t, hp.chan_sbase[t], w2, 0});
+        pg.chans.push_back(ChanEntry{t, base, w2, 0});
       }
       pg.groups[l1].n_chan = (int)pg.chans.size() - pg.groups[l1].chan_off;
     }
@@ -661,7 +703,7 @@ int build_host_plan(const bfq_desc& d, int smem_limit, HostPlan& hp) {
   if (hp.folded && hp.sym.cfg.pairsplit && !std::getenv("BFQ_NO_DIAG")) {
     for (ChanEntry& ce : hp.sym.chans) {
       const int t = ce.tau < d.n_t ? ce.tau : -1;
-      if (t < 0 || hp.triplets[3 * t + 1] != hp.triplets[3 * t + 2]) continue;
+      if (t < 0 || hp.triplets[3 * t + 1] != hp.triplets[3 * t + 2] || half_base[t] >= 0) continue;
       const size_t nb = hp.rblocks.size() / blk;
       hp.rblocks.resize((nb + 1) * blk, 0.0);
       for (int k1 = 0; k1 < nk; ++k1) {
@@ -729,11 +771,21 @@ int build_host_plan(const bfq_desc& d, int smem_limit, HostPlan& hp) {
   {
     std::vector<int64_t> chan_rows(d.n_t, 0);
     for (int64_t z = 0; z < d.n_g; ++z) ++chan_rows[d.tau[z]];
+    for (int t = 0; t < d.n_t; ++t)
+      if (half_base[t] >= 0) {  // half-row slices: count their rows without padding
+        int64_t n = 0;
+        const int l1 = hp.triplets[3 * t];
+        for (int m1 = 0; m1 < 2 * l1 + 1; ++m1)
+          for (int32_t z = hp.sstart[half_base[t] + m1]; z < hp.sstart[half_base[t] + m1 + 1]; ++z)
+            n += hp.rows[z].g != 0.0;
+        chan_rows[t] = n;
+      }
     double useful = 0.0;
     for (int t = 0; t < d.n_t; ++t) {
       const int l1 = hp.triplets[3 * t], l2 = hp.triplets[3 * t + 1], l3 = hp.triplets[3 * t + 2];
       if (hp.folded && l2 > l3) continue;
-      const bool diag = hp.folded && l2 == l3 && hp.sym.cfg.pairsplit && !std::getenv("BFQ_NO_DIAG");
+      const bool diag = hp.folded && l2 == l3 && hp.sym.cfg.pairsplit && !std::getenv("BFQ_NO_DIAG") &&
+                        half_base[t] < 0;
       const double kk = diag ? nk * (nk + 1) / 2.0 : (double)nk * nk;
       useful += (double)chan_rows[t] * kk + (2.0 * l1 + 1.0) * nk * kk;
     }

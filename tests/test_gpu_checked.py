@@ -37,7 +37,8 @@ def _run(env_extra, ops, cells):
     ({"BFQ_GENERIC": "1"}, "hs_n4,hs_n8,mm_n10", 9),  # run-time-size instantiations
     ({"BFQ_STAGES": "2"}, "hs_n8,hs_n12", 9),         # two-stage R ring
     ({"BFQ_CELLS": "1"}, "hs_n16", 5),                # one cell per tile, slices split over the warps
-], ids=["default", "fallback", "generic", "stages2", "splitm"])
+    ({"BFQ_HALF_DIAG": "0"}, "hs_n4,hs_n8,hs_n12", 9),  # packed-triangle self-symmetric channels
+], ids=["default", "fallback", "generic", "stages2", "splitm", "packed_diag"])
 def test_checked_kernels(env_extra, ops, cells):
     res, lines = _run(env_extra, ops, cells)
     assert res.returncode == 0, res.stdout[-4000:] + res.stderr[-4000:]
