@@ -92,8 +92,9 @@ __global__ void __launch_bounds__(NKT == 17 ? (CELLS == 1 ? 384 : 256) : 512, 1)
         ctau[t * p.max_chan + i] = 2 * ce.tau + ce.diag;
       }
     }
-  for (int i = threadIdx.x; i < NU * 8 * K2S; i += blockDim.x) phis[i] = 0.0;
   {
+    // stage the tile's cells with cp.async (all loads in flight at once; the
+    // Phi zeroing below overlaps them); cells past the batch read as zeros
     const int rows_total = NF * CELLS * NK;
     const int nwarps = blockDim.x >> 5;
     for (int row = warp; row < rows_total; row += nwarps) {
@@ -101,12 +102,20 @@ __global__ void __launch_bounds__(NKT == 17 ? (CELLS == 1 ? 384 : 256) : 512, 1)
       const int rem = row - arr * CELLS * NK;
       const int c = rem / NK, k = rem - c * NK;
       const long long cell = tile * CELLS + c;
-      const bool ok = cell < p.n_cells;
-      const double* src = (arr == 0 ? p.f2 : p.f3) + (ok ? cell : 0) * (long long)NK * p.nq + (long long)k * p.nq;
       double* dst = fs + (arr * CELLS + c) * cell_elems + k * QS;
-      for (int q = lane; q < p.nq; q += 32) dst[q] = ok ? __ldg(src + q) : 0.0;
+      if (cell < p.n_cells) {
+        const double* src = (arr == 0 ? p.f2 : p.f3) + cell * (long long)NK * p.nq + (long long)k * p.nq;
+        const uint32_t d0 = smem_u32(dst);
+        for (int q = lane; q < p.nq; q += 32)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d0 + (uint32_t)q * 8u), "l"(src + q)
+                       : "memory");
+      } else {
+        for (int q = lane; q < p.nq; q += 32) dst[q] = 0.0;
+      }
     }
   }
+  for (int i = threadIdx.x; i < NU * 8 * K2S; i += blockDim.x) phis[i] = 0.0;
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
   __syncthreads();
 
   const int u = warp >> 1, h = warp & 1;
