@@ -114,7 +114,17 @@ __global__ void __launch_bounds__(NKT == 17 ? (CELLS == 1 ? 384 : 256) : 512, 1)
       }
     }
   }
-  for (int i = threadIdx.x; i < NU * 8 * K2S; i += blockDim.x) phis[i] = 0.0;
+  {
+    // Phi rows: every entry a stage-2 k-step can read before the first store
+    // overwrites it must be finite -- zero the tail [n_k(n_k+1)/2, K2S) of each
+    // row (a packed self-symmetric channel stores only the triangle; the full
+    // n_k^2 rows are always written before they are read)
+    const int z0 = NK * (NK + 1) / 2, zn = K2S - z0;
+    for (int i = threadIdx.x; i < NU * 8 * zn; i += blockDim.x) {
+      const int r = i / zn;
+      phis[r * K2S + z0 + (i - r * zn)] = 0.0;
+    }
+  }
   asm volatile("cp.async.wait_all;\n" ::: "memory");
   __syncthreads();
 
