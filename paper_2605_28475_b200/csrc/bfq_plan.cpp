@@ -175,7 +175,11 @@ static bool choose_config(int nk, int qs, int k2s, int nf, int smem_limit, int m
 // tile's cells) of all l1 groups are laid out group by group (descending l1,
 // whose per-unit work is nearly uniform) and packed nw at a time into CTAs;
 // a CTA spans at most two groups (two teams, two R rings).  Heavy CTAs first.
-static void build_items(const HostPlan& hp, Program& pg) {
+// One packing of the program for a given number of units per l1 group; returns
+// the schedule cost (sum over CTAs of their slowest unit) and the group of the
+// heaviest unit.
+static double pack_program(const HostPlan& hp, Program& pg, const std::vector<int>& want, bool report,
+                           int* heavy_l1) {
   // (groups are modified: unit_off / n_units)
   const KernelConfig& c = pg.cfg;
   const double stage2 = (double)c.mt * 256.0 * (hp.k2p / 4);
@@ -194,7 +198,7 @@ static void build_items(const HostPlan& hp, Program& pg) {
   // warps of a CTA ~20% imbalanced).
   pg.unit_m1.clear();
   for (Group& gr : pg.groups) {
-    const int units = gr.n_chan ? (gr.d1 + c.m1t - 1) / c.m1t : 0;
+    const int units = gr.n_chan ? want[gr.l1] : 0;
     gr.unit_off = (int)(pg.unit_m1.size() / c.m1t);
     gr.n_units = units;
     if (!units) continue;
@@ -251,7 +255,8 @@ static void build_items(const HostPlan& hp, Program& pg) {
       total += w;
     }
   std::stable_sort(units_all.begin(), units_all.end(), [](const U& x, const U& y) { return x.work > y.work; });
-  if (const char* e = std::getenv("BFQ_PLAN_STATS"))
+  if (heavy_l1) *heavy_l1 = units_all.empty() ? -1 : units_all[0].l1;
+  if (const char* e = report ? std::getenv("BFQ_PLAN_STATS") : nullptr)
     if (std::atoi(e) >= 2)
       for (const U& un : units_all) std::fprintf(stderr, "unit l1=%d u=%d work=%.4g\n", un.l1, un.u, un.work);
   struct Cta {
@@ -371,7 +376,7 @@ static void build_items(const HostPlan& hp, Program& pg) {
   }
   pg.unit_m1.swap(new_m1);
   pg.exec_macs_per_cell = total / c.cells;
-  if (std::getenv("BFQ_PLAN_STATS")) {  // packing efficiency: unit work / (slots x slowest unit)
+  if (report && std::getenv("BFQ_PLAN_STATS")) {  // packing efficiency: unit work / (slots x slowest unit)
     double cap = 0.0;
     for (const Cta& cta : ctas) cap += cta.work * c.upc;
     // lockstep model: a team (one R ring) advances channel by channel at the
@@ -404,6 +409,46 @@ static void build_items(const HostPlan& hp, Program& pg) {
     std::fprintf(stderr, "plan: %zu CTAs per tile, %zu units, packing efficiency %.3f, with team lockstep %.3f\n",
                  ctas.size(), units_all.size(), total / cap, total / cap2);
   }
+  return cost(ctas);
+}
+
+// Build the CTA schedule: start from ceil(d1 / m1t) units per l1 group (every
+// slot used), then split the group holding the heaviest unit into one more
+// unit while that lowers the modelled schedule cost (sum over CTAs of their
+// slowest unit).  Opt-in (BFQ_UNIT_BALANCE=1): at n_k = 17 it raises the model's
+// packing efficiency 0.83 -> 0.87 but measured 7% SLOWER (46.5k -> 43.2k
+// cells/s, profiles/r02_unit_balance.txt) -- the extra units' stage-2 work and
+// the extra CTA per tile cost more than the model credits.
+static void build_items(const HostPlan& hp, Program& pg) {
+  const KernelConfig& c = pg.cfg;
+  std::vector<int> want(pg.groups.size(), 0);
+  for (const Group& gr : pg.groups) want[gr.l1] = gr.n_chan ? (gr.d1 + c.m1t - 1) / c.m1t : 0;
+  int heavy = -1;
+  double best_cost;
+  {
+    Program first = pg;
+    best_cost = pack_program(hp, first, want, false, &heavy);
+  }
+  if (std::getenv("BFQ_UNIT_BALANCE")) {
+    // greedy splits with look-ahead: keep splitting the heaviest unit's group
+    // (several groups are often nearly as heavy), remember the cheapest schedule
+    std::vector<int> cur = want;
+    int misses = 0;
+    for (int it = 0; it < 96 && heavy >= 0 && misses < 12; ++it) {
+      if (cur[heavy] >= pg.groups[heavy].d1) break;  // one column per unit already
+      ++cur[heavy];
+      Program trial = pg;
+      const double cst = pack_program(hp, trial, cur, false, &heavy);
+      if (cst < best_cost * (1.0 - 1e-9)) {
+        best_cost = cst;
+        want = cur;
+        misses = 0;
+      } else {
+        ++misses;
+      }
+    }
+  }
+  pack_program(hp, pg, want, true, nullptr);
 }
 
 // Shared-memory wavefronts of one stage-1 gather instruction for a group of
