@@ -311,7 +311,8 @@ __global__ void __launch_bounds__(NKT == 17 ? (CELLS == 1 ? 384 : 256) : 512, 1)
 #pragma unroll
               for (int b = 0; b < MT; ++b) acc2[cc][a][b][0] = acc2[cc][a][b][1] = 0.0;
         }
-        auto group = [&](const Row& rw, double (&ac)[HC][MT][MT][2]) {
+        auto group = [&](const Row& rw, double (&ac)[HC][MT][MT][2], double (&xr_)[HC][MTM], double (&xc_)[HC][MTM],
+                         double (&xd_)[HC]) {
           const uint32_t qa = (uint32_t)rw.q2 * 8u, qb = (uint32_t)rw.q3 * 8u;
 #pragma unroll
           for (int cc = 0; cc < HC; ++cc) {
@@ -334,10 +335,10 @@ __global__ void __launch_bounds__(NKT == 17 ? (CELLS == 1 ? 384 : 256) : 512, 1)
               const double eb = lds_ro(BFQ_CHK(fx_b + qb + cc * cell_bytes, fb_lo, fb_lo + fspan, CHK_F3));
 #pragma unroll
               for (int t = 0; t < MTM; ++t) {
-                if (!DGC) xr[cc][t] = fma(ea, bv[t], xr[cc][t]);
-                xc[cc][t] = fma(av[t], eb, xc[cc][t]);
+                if (!DGC) xr_[cc][t] = fma(ea, bv[t], xr_[cc][t]);
+                xc_[cc][t] = fma(av[t], eb, xc_[cc][t]);
               }
-              xd[cc] = fma(ea, eb, xd[cc]);
+              xd_[cc] = fma(ea, eb, xd_[cc]);
             }
           }
         };
@@ -350,8 +351,8 @@ __global__ void __launch_bounds__(NKT == 17 ? (CELLS == 1 ? 384 : 256) : 512, 1)
             const bool same = z0 + 8 < ze[ml];
             nxt_row = fetch_rb((same ? z0 + 8 : zn) + kq, same ? ze[ml] : en);
             nxt_b = fetch_rb((same ? z0 + 12 : zn + 4) + kq, same ? ze[ml] : en);
-            group(rwa, acc);
-            group(rwb, acc2);
+            group(rwa, acc, xr, xc, xd);
+            group(rwb, acc2, xr, xc, xd);  // shared X1 sums (separate ones: 3% slower, r02_ab_xsh_dual.txt)
           }
 #pragma unroll
           for (int cc = 0; cc < HC; ++cc)
@@ -367,7 +368,7 @@ __global__ void __launch_bounds__(NKT == 17 ? (CELLS == 1 ? 384 : 256) : 512, 1)
             const Row rw = nxt_row;
             const bool same = z0 + 4 < ze[ml];
             nxt_row = fetch_rb((same ? z0 + 4 : zn) + kq, same ? ze[ml] : en);
-            group(rw, acc);
+            group(rw, acc, xr, xc, xd);
           }
         }
         if (zs[ml] >= ze[ml]) {
