@@ -50,9 +50,8 @@ namespace {
 constexpr int TC = 32;        // polar rows per chunk (4 DMMA M-tiles)
 constexpr int TCP = TC + 1;   // row stride of the polar-table chunk: odd, so the threads of
                               // the polar sum (one (l, |m|) row each) hit distinct banks
-constexpr int PS_THREADS = 256;
+constexpr int PS_THREADS = 384;  // 8 GEMM warps + 4 epilogue warps
 constexpr int MAXT = 7;       // N tiles of the azimuthal GEMM: 2 l_max + 1 <= 56 (l_max <= 27)
-constexpr int RAD_MAX = 24;   // coefficient entries per thread: n_k n_q <= 24 x 256 (bfq_projector_create)
 
 struct PsParams {
   const double* f;
@@ -74,147 +73,219 @@ __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-template <int NT>  // N tiles of the azimuthal GEMM (ceil((2 l_max + 1) / 8)): no predicated-off DMMAs
-__global__ void __launch_bounds__(PS_THREADS, 1) k_project_samples(const PsParams p) {
+__device__ __forceinline__ void bar_sync(unsigned id, unsigned n) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(unsigned id, unsigned n) {
+  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(n) : "memory");
+}
+
+// Warp roles: warps 0..7 stream the samples (cp.async ring) and run the
+// azimuthal GEMM, writing G (and the v's radial table) into one of two G
+// buffers; warps 8..11 run the polar and radial sums out of the other buffer.
+// Named barriers: BAR_GEMM among the GEMM warps (ring), FULL[b] GEMM -> epilogue
+// (buffer b written), EMPTY[b] epilogue -> GEMM (buffer b consumed), BAR_EPI
+// among the epilogue warps.
+// Azimuthal GEMM of one warp: M tile rows (arow), every k-step, the N tiles
+// j = NH, NH + 2, ... (compile-time: no predicated-off DMMAs); `store` runs after
+// the accumulation with the warp's C fragments.
+template <int NT, int NH, class Store>
+__device__ __forceinline__ void azim_gemm(uint32_t arow, uint32_t bw, int ks, int ntile, Store&& store) {
+  constexpr int NJ = (NT - NH + 1) / 2;  // may be 0 (NT = 1): the store still runs (barrier)
+  double c[NJ > 0 ? NJ : 1][2];
+#pragma unroll
+  for (int jj = 0; jj < NJ; ++jj) c[jj][0] = c[jj][1] = 0.0;
+#pragma unroll 4
+  for (int k = 0; k < ks; ++k) {
+    const double a = lds_ro(arow + (uint32_t)(4 * k) * 8u);
+    const uint32_t bk = bw + (uint32_t)(k * ntile * 32) * 8u;
+#pragma unroll
+    for (int jj = 0; jj < NJ; ++jj) dmma884(c[jj][0], c[jj][1], a, lds_ro(bk + (uint32_t)((NH + 2 * jj) * 32) * 8u));
+  }
+  store(c, NH, NJ);
+}
+
+constexpr int GEMM_WARPS = 8, EPI_WARPS = 4;
+constexpr unsigned BAR_GEMM = 1, BAR_FULL0 = 2, BAR_EMPTY0 = 4, BAR_EPI = 6;
+constexpr unsigned NT_ALL = PS_THREADS, NT_GEMM = GEMM_WARPS * 32, NT_EPI = EPI_WARPS * 32;
+
+constexpr int NKMAX_REG = 17;  // register accumulators in the epilogue: n_k <= 17, n_q <= 2 x 128
+
+template <int NT, bool REGACC>  // N tiles of the azimuthal GEMM (ceil((2 l_max + 1) / 8)); coefficient
+__global__ void __launch_bounds__(PS_THREADS, 1) k_project_samples(const PsParams p) {  // columns in registers
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const long long cell = blockIdx.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, r0 = lane >> 2, kq = lane & 3;
   const int nrv = (p.L + 1) * p.nk;               // radial table of one v, staged with its slab
   const int slab = TC * p.sp + (nrv + 1) / 2 * 2;  // doubles per ring slot: samples | radial table
-  double* buf = reinterpret_cast<double*>(smem_raw);  // [nbuf][TC][sp]
+  const int gsz = TC * p.gs + (nrv + 1) / 2 * 2;  // doubles per G buffer: G | radial table
+  double* buf = reinterpret_cast<double*>(smem_raw);  // [nbuf][slab]
   double* wf = buf + (size_t)p.nbuf * slab;        // [ks][ntile][32]
   double* pt = wf + (size_t)p.ks * p.ntile * 32;   // [npl][TCP] polar chunk
-  double* g = pt + (size_t)p.npl * TCP;            // [2][TC][gs] azimuthal sums of the chunk (two K halves)
-  double* acc = g + (size_t)2 * TC * p.gs;         // [nk][nq]   coefficients of the cell
-  double* aq = acc + (size_t)p.nk * p.nq;          // [nq]       polar sums of the chunk
+  double* g = pt + (size_t)p.npl * TCP;            // [2][gsz]    G buffers
+  double* acc = g + (size_t)2 * gsz;               // [nk][nq]   coefficients of the cell
+  double* aq = acc + (size_t)p.nk * p.nq;          // [nq]       polar sums of one (chunk, v)
+  int* lq = reinterpret_cast<int*>(aq + p.nq);     // [nq]       l(q)
   for (int i = tid; i < p.ks * p.ntile * 32; i += PS_THREADS) wf[i] = p.wfrag[i];
   for (int i = tid; i < p.nbuf * slab; i += PS_THREADS) buf[i] = 0.0;  // zero padding rows/columns
   for (int i = tid; i < p.nk * p.nq; i += PS_THREADS) acc[i] = 0.0;
-  __syncthreads();
-
-  const double* fc = p.f + cell * (long long)p.nv * p.nt * p.np;
-  const int nsteps = p.nchunk * p.nv;  // (chunk outer, v inner)
-  auto issue = [&](int s) {
-    if (s < nsteps) {
-      const int c = s / p.nv, v = s - c * p.nv;
-      const int t0 = c * TC, rows = min(TC, p.nt - t0);
-      const double* src = fc + ((long long)v * p.nt + t0) * p.np;
-      const uint32_t dst = smem_u32(buf + (size_t)(s % p.nbuf) * slab);
-      const double* rsrc = p.rtab + (size_t)v * nrv;
-      for (int i = tid; i < nrv; i += PS_THREADS) cp_async8(dst + (uint32_t)(TC * p.sp + i) * 8u, rsrc + i);
-      int r = tid / p.np, col = tid - r * p.np;  // walk (row, column) without a division per element
-      const int dr = PS_THREADS / p.np, dc = PS_THREADS - dr * p.np;
-      for (int i = tid; i < rows * p.np; i += PS_THREADS) {
-        cp_async8(dst + (uint32_t)(r * p.sp + col) * 8u, src + i);
-        r += dr;
-        col += dc;
-        if (col >= p.np) {
-          col -= p.np;
-          ++r;
-        }
-      }
-    }
-    cp_commit();  // possibly empty group: keeps the wait count uniform
-  };
-  for (int s = 0; s < p.nbuf - 1; ++s) issue(s);
-
-  const int mt = warp & 3;  // M tile (8 polar rows) of this warp
-  // this thread's entries (k, q) of the coefficient block, with l(q), for the radial sums
-  int rad_i[RAD_MAX], rad_q[RAD_MAX], rad_lk[RAD_MAX];
-#pragma unroll
-  for (int j = 0; j < RAD_MAX; ++j) {
-    const int i = tid + j * PS_THREADS;
-    rad_i[j] = i < p.nk * p.nq ? i : -1;
-    const int k = i / p.nq, q = i - k * p.nq;
+  for (int q = tid; q < p.nq; q += PS_THREADS) {
     int l = (int)sqrtf((float)q);
     while (l * l > q) --l;
     while ((l + 1) * (l + 1) <= q) ++l;
-    rad_q[j] = q;
-    rad_lk[j] = l * p.nk + k;
+    lq[q] = l;
   }
-  for (int s = 0; s < nsteps; ++s) {
-    const int c = s / p.nv, v = s - c * p.nv;
-    if (v == 0) {  // new chunk: its polar table
-      __syncthreads();
-      for (int i = tid; i < p.npl * TC; i += PS_THREADS) {
-        const int row = i / TC;
-        pt[row * TCP + (i - row * TC)] = p.ptab[(size_t)c * p.npl * TC + i];
-      }
-    }
-    issue(s + p.nbuf - 1);
-    if (p.nbuf == 3) cp_wait<2>();
-    else cp_wait<1>();
-    __syncthreads();
-    // ---- azimuthal GEMM: G[t][col] = sum_p f[t][p] W[p][col] (DMMA.8x8x4).
-    // Warp (mt, kh): M tile mt (8 polar rows) x every N tile, half kh of the
-    // k-steps -- each A fragment (the samples) feeds all N tiles, and the two
-    // K halves land in separate G buffers that the polar sum adds.
-    const double* bs = buf + (size_t)(s % p.nbuf) * slab;
-    {
-      const int kh = warp >> 2, kmid = (p.ks + 1) / 2;
-      const int k0 = kh ? kmid : 0, k1 = kh ? p.ks : kmid;
-      const uint32_t arow = smem_u32(bs + (size_t)(8 * mt + r0) * p.sp + kq);
-      const uint32_t bw = smem_u32(wf + lane);
-      double cacc[NT][2];
-#pragma unroll
-      for (int j = 0; j < NT; ++j) cacc[j][0] = cacc[j][1] = 0.0;
-      // plain (non-volatile) shared loads: the slab and W are stable between the
-      // barriers, so the compiler may hoist the next k-steps' loads over the DMMAs
-#pragma unroll 4
-      for (int k = k0; k < k1; ++k) {
-        const double a = lds_ro(arow + (uint32_t)(4 * k) * 8u);
-        const uint32_t bk = bw + (uint32_t)(k * p.ntile * 32) * 8u;
-#pragma unroll
-        for (int j = 0; j < NT; ++j) dmma884(cacc[j][0], cacc[j][1], a, lds_ro(bk + (uint32_t)(j * 32) * 8u));
-      }
-      double* gr = g + (size_t)kh * TC * p.gs + (size_t)(8 * mt + r0) * p.gs + 2 * kq;
-#pragma unroll
-      for (int j = 0; j < NT; ++j) {
-        gr[8 * j] = cacc[j][0];
-        gr[8 * j + 1] = cacc[j][1];
-      }
-    }
-    __syncthreads();
-    // ---- polar sum of the chunk: aq[q] = sum_t P[l,|m|][t] G[t][col(m)]
-    for (int q = tid; q < p.nq; q += PS_THREADS) {
-      int l = (int)sqrtf((float)q);
-      while (l * l > q) --l;
-      while ((l + 1) * (l + 1) <= q) ++l;
-      const int m = q - l * l - l, am = m < 0 ? -m : m;
-      const int col = m == 0 ? 0 : (m < 0 ? 2 * am - 1 : 2 * am);
-      const double* prow = pt + (size_t)(l * (l + 1) / 2 + am) * TCP;
-      double a = 0.0;
-#pragma unroll 8
-      for (int t = 0; t < TC; ++t) a = fma(prow[t], g[(size_t)t * p.gs + col] + g[(size_t)(TC + t) * p.gs + col], a);
-      aq[q] = a;
-    }
-    __syncthreads();
-    // ---- radial sum of this (chunk, v): acc[k][q] += Rv[v][l][k] aq[q]
-    const double* rv = bs + (size_t)TC * p.sp;  // staged with the slab (no global latency here)
-#pragma unroll
-    for (int j = 0; j < RAD_MAX; ++j)
-      if (rad_i[j] >= 0) acc[rad_i[j]] = fma(rv[rad_lk[j]], aq[rad_q[j]], acc[rad_i[j]]);
-    // the next iteration's __syncthreads (after its wait) orders these reads of
-    // aq / g before they are rewritten; the ring slot s % nbuf is refilled only
-    // by issue(s + nbuf), which follows that barrier
-  }
-  cp_wait<0>();
   __syncthreads();
-  double* oc = p.out + cell * (long long)p.nk * p.nq;
-  for (int i = tid; i < p.nk * p.nq; i += PS_THREADS) oc[i] = acc[i];
+  const int nsteps = p.nchunk * p.nv;  // (chunk outer, v inner)
+
+  if (warp < GEMM_WARPS) {
+    // ------------------------------------------------ producer: samples -> G
+    const double* fc = p.f + cell * (long long)p.nv * p.nt * p.np;
+    auto issue = [&](int s) {
+      if (s < nsteps) {
+        const int c = s / p.nv, v = s - c * p.nv;
+        const int t0 = c * TC, rows = min(TC, p.nt - t0);
+        const double* src = fc + ((long long)v * p.nt + t0) * p.np;
+        const uint32_t dst = smem_u32(buf + (size_t)(s % p.nbuf) * slab);
+        const double* rsrc = p.rtab + (size_t)v * nrv;
+        for (int i = tid; i < nrv; i += NT_GEMM) cp_async8(dst + (uint32_t)(TC * p.sp + i) * 8u, rsrc + i);
+        int r = tid / p.np, col = tid - r * p.np;  // walk (row, column) without a division per element
+        const int dr = NT_GEMM / p.np, dc = NT_GEMM - dr * p.np;
+        for (int i = tid; i < rows * p.np; i += NT_GEMM) {
+          cp_async8(dst + (uint32_t)(r * p.sp + col) * 8u, src + i);
+          r += dr;
+          col += dc;
+          if (col >= p.np) {
+            col -= p.np;
+            ++r;
+          }
+        }
+      }
+      cp_commit();  // possibly empty group: keeps the wait count uniform
+    };
+    for (int s = 0; s < p.nbuf - 1; ++s) issue(s);
+    const int mt = warp & 3, nh = warp >> 2;
+    const uint32_t bw = smem_u32(wf + lane);
+    for (int s = 0; s < nsteps; ++s) {
+      issue(s + p.nbuf - 1);
+      if (p.nbuf == 3) cp_wait<2>();
+      else cp_wait<1>();
+      bar_sync(BAR_GEMM, NT_GEMM);  // slab s landed for every producer thread
+      const double* bs = buf + (size_t)(s % p.nbuf) * slab;
+      // azimuthal GEMM: G[t][col] = sum_p f[t][p] W[p][col] (DMMA.8x8x4); warp
+      // (mt, nh): M tile mt (8 polar rows) x the N tiles nh, nh + 2, .., every k-step
+      const uint32_t arow = smem_u32(bs + (size_t)(8 * mt + r0) * p.sp + kq);
+      const int b = s & 1;
+      double* gb = g + (size_t)b * gsz;
+      auto store = [&](auto& c, int h, int nj) {
+        if (s >= 2) bar_sync(BAR_EMPTY0 + b, NT_ALL);  // the epilogue has consumed buffer b
+        double* gr = gb + (size_t)(8 * mt + r0) * p.gs + 2 * kq;
+#pragma unroll
+        for (int jj = 0; jj < (int)(sizeof(c) / sizeof(c[0])); ++jj)
+          if (jj < nj) {
+            gr[8 * (h + 2 * jj)] = c[jj][0];
+            gr[8 * (h + 2 * jj) + 1] = c[jj][1];
+          }
+      };
+      if (nh == 0) azim_gemm<NT, 0>(arow, bw, p.ks, p.ntile, store);
+      else azim_gemm<NT, 1>(arow, bw, p.ks, p.ntile, store);
+      for (int i = tid; i < nrv; i += NT_GEMM) gb[TC * p.gs + i] = bs[(size_t)TC * p.sp + i];
+      __threadfence_block();
+      bar_arrive(BAR_FULL0 + b, NT_ALL);
+      // the ring slot s % nbuf is refilled by issue(s + nbuf) in the next
+      // iteration, after every producer passed this step's BAR_GEMM and its reads
+      bar_sync(BAR_GEMM, NT_GEMM);
+    }
+    cp_wait<0>();
+  } else {
+    // ------------------------------------------------ consumer: G -> coefficients
+    // each epilogue thread owns whole coefficient columns q (every k): the polar
+    // sum a = sum_t P[l,|m|][t] G[t][col(m)] (four partial chains), then the
+    // radial sum c[k][q] += Rv[v][l][k] a, accumulated in registers (REGACC) or
+    // in shared memory
+    const int et = tid - NT_GEMM;
+    double racc[REGACC ? 2 : 1][REGACC ? NKMAX_REG : 1];
+#pragma unroll
+    for (int u = 0; u < (REGACC ? 2 : 1); ++u)
+#pragma unroll
+      for (int k = 0; k < (REGACC ? NKMAX_REG : 1); ++k) racc[u][k] = 0.0;
+    for (int s = 0; s < nsteps; ++s) {
+      const int c = s / p.nv, b = s & 1;
+      if (s % p.nv == 0) {  // new chunk: its polar table
+        bar_sync(BAR_EPI, NT_EPI);
+        for (int i = et; i < p.npl * TC; i += NT_EPI) {
+          const int row = i / TC;
+          pt[row * TCP + (i - row * TC)] = p.ptab[(size_t)c * p.npl * TC + i];
+        }
+      }
+      bar_sync(BAR_FULL0 + b, NT_ALL);  // buffer b written (also orders the pt stores above)
+      const double* gb = g + (size_t)b * gsz;
+      const double* rv = gb + (size_t)TC * p.gs;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int q = et + u * NT_EPI;
+        if (!REGACC && u > 0) break;
+        for (int qq = q; qq < p.nq; qq += (REGACC ? p.nq : 2 * NT_EPI)) {  // REGACC: one pass
+          const int l = lq[qq], m = qq - l * l - l, am = m < 0 ? -m : m;
+          const int col = m == 0 ? 0 : (m < 0 ? 2 * am - 1 : 2 * am);
+          const double* prow = pt + (size_t)(l * (l + 1) / 2 + am) * TCP;
+          const double* g0 = gb + col;
+          double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+          for (int t = 0; t < TC; t += 4) {
+            a0 = fma(prow[t], g0[(size_t)t * p.gs], a0);
+            a1 = fma(prow[t + 1], g0[(size_t)(t + 1) * p.gs], a1);
+            a2 = fma(prow[t + 2], g0[(size_t)(t + 2) * p.gs], a2);
+            a3 = fma(prow[t + 3], g0[(size_t)(t + 3) * p.gs], a3);
+          }
+          const double a = (a0 + a1) + (a2 + a3);
+          const double* rvl = rv + l * p.nk;
+          if constexpr (REGACC) {
+#pragma unroll
+            for (int k = 0; k < NKMAX_REG; ++k)
+              if (k < p.nk) racc[u][k] = fma(rvl[k], a, racc[u][k]);
+          } else {
+            for (int k = 0; k < p.nk; ++k) acc[(size_t)k * p.nq + qq] = fma(rvl[k], a, acc[(size_t)k * p.nq + qq]);
+          }
+          if (!REGACC) continue;
+        }
+      }
+      __threadfence_block();
+      bar_arrive(BAR_EMPTY0 + b, NT_ALL);  // buffer b may be rewritten
+    }
+    double* oc = p.out + cell * (long long)p.nk * p.nq;
+    if constexpr (REGACC) {
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int q = et + u * NT_EPI;
+        if (q < p.nq)
+#pragma unroll
+          for (int k = 0; k < NKMAX_REG; ++k)
+            if (k < p.nk) oc[(size_t)k * p.nq + q] = racc[u][k];
+      }
+    } else {
+      bar_sync(BAR_EPI, NT_EPI);  // every column complete
+      for (int i = et; i < p.nk * p.nq; i += NT_EPI) oc[i] = acc[i];
+    }
+  }
 }
 
 typedef void (*PsKernel)(const PsParams);
-PsKernel ps_kernel(int ntile) {
+template <bool R>
+PsKernel ps_kernel_r(int ntile) {
   switch (ntile) {
-    case 1: return k_project_samples<1>;
-    case 2: return k_project_samples<2>;
-    case 3: return k_project_samples<3>;
-    case 4: return k_project_samples<4>;
-    case 5: return k_project_samples<5>;
-    case 6: return k_project_samples<6>;
-    default: return k_project_samples<7>;
+    case 1: return k_project_samples<1, R>;
+    case 2: return k_project_samples<2, R>;
+    case 3: return k_project_samples<3, R>;
+    case 4: return k_project_samples<4, R>;
+    case 5: return k_project_samples<5, R>;
+    case 6: return k_project_samples<6, R>;
+    default: return k_project_samples<7, R>;
   }
+}
+bool ps_regacc(int nk, int nq) { return nk <= NKMAX_REG && nq <= 2 * (EPI_WARPS * 32); }
+PsKernel ps_kernel(int ntile, int nk, int nq) {
+  return ps_regacc(nk, nq) ? ps_kernel_r<true>(ntile) : ps_kernel_r<false>(ntile);
 }
 
 int fail(int code, const std::string& msg) {
@@ -245,8 +316,6 @@ int bfq_projector_create(int32_t k_max, int32_t l_max, int32_t n_v, int32_t n_t,
   *out = nullptr;
   if (k_max < 0 || l_max < 0 || n_v < 1 || n_t < 1 || n_p < 1) return fail(BFQ_EINVAL, "bad sizes");
   if (2 * l_max + 1 > 8 * MAXT) return fail(BFQ_EINVAL, "l_max above the projection kernel's limit (27)");
-  if ((k_max + 1) * (l_max + 1) * (l_max + 1) > RAD_MAX * PS_THREADS)
-    return fail(BFQ_EINVAL, "n_k n_q above the projection kernel's limit (6144)");
   if (n_t < l_max + 1 || n_p < 2 * l_max + 1)
     return fail(BFQ_EINVAL, "angular grid too small for l_max (basis.py:284-285)");
   DevGuard guard(device);
@@ -268,8 +337,10 @@ int bfq_projector_create(int32_t k_max, int32_t l_max, int32_t n_v, int32_t n_t,
   int optin = 0;
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   auto smem_for = [&](int nbuf) {
-    return (size_t)8 * ((size_t)nbuf * (TC * pj->sp + ((l_max + 1) * pj->nk + 1) / 2 * 2) + (size_t)pj->ks * pj->ntile * 32 + (size_t)npl * TC +
-                        (size_t)2 * TC * gs + (size_t)pj->nk * pj->nq + pj->nq + (size_t)npl);
+    const size_t rvp = ((size_t)(l_max + 1) * pj->nk + 1) / 2 * 2;  // radial table of one v, padded
+    return (size_t)8 * ((size_t)nbuf * (TC * pj->sp + rvp) + (size_t)pj->ks * pj->ntile * 32 + (size_t)npl * TCP +
+                        2 * ((size_t)TC * gs + rvp) + (size_t)pj->nk * pj->nq + pj->nq) +
+           (size_t)4 * pj->nq;  // l(q) table
   };
   pj->nbuf = smem_for(3) <= (size_t)optin ? 3 : 2;
   pj->smem = smem_for(pj->nbuf);
@@ -310,7 +381,7 @@ int bfq_projector_create(int32_t k_max, int32_t l_max, int32_t n_v, int32_t n_t,
     delete pj;
     return fail(BFQ_ENOMEM, "device allocation of the projection tables failed");
   }
-  if (cudaFuncSetAttribute(ps_kernel(pj->ntile), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pj->smem) !=
+  if (cudaFuncSetAttribute(ps_kernel(pj->ntile, pj->nk, pj->nq), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pj->smem) !=
       cudaSuccess) {
     bfq_projector_destroy(pj);
     return fail(BFQ_ECUDA, "cannot set the projection kernel's shared memory");
@@ -356,7 +427,7 @@ int bfq_project_samples(const bfq_projector* pj, const double* samples, double* 
   p.ptab = pj->ptab;
   p.rtab = pj->rtab;
   p.gs = conflict_free_stride_dev(pj->ntile * 8);
-  ps_kernel(pj->ntile)<<<(unsigned)n, PS_THREADS, pj->smem, (cudaStream_t)stream>>>(p);
+  ps_kernel(pj->ntile, pj->nk, pj->nq)<<<(unsigned)n, PS_THREADS, pj->smem, (cudaStream_t)stream>>>(p);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(BFQ_ECUDA, std::string("projection launch: ") + cudaGetErrorString(e));
   return BFQ_OK;
