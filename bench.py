@@ -901,7 +901,8 @@ def run_ours(args, rank, world, local_rank):
                                    "of the folded channels without padding (what the kernel must do)",
                      "hbm_frac": bytes_cell * n_cells / kern_s / 1e9 / measured_peaks().get("hbm_gbs", 6548.2)},
         "e2e": e2e,
-        "gpu_launches": args.steps * (11 if rk4 else 1),
+        # RK4: 4 Q launches + 7 elementwise stage kernels (BFQ_RK4_FUSED=1: the 4 Q launches alone)
+        "gpu_launches": args.steps * ((4 if os.environ.get("BFQ_RK4_FUSED", "0") not in ("", "0") else 11) if rk4 else 1),
         "clocks": clk.summary(),
         "parity": parity,
         "conservation": {"invariant_slots_exact": bool(ok.item() == 1.0), **diag},

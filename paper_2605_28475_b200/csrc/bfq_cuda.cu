@@ -202,11 +202,24 @@ void free_program(DevProgram& dp) {
   dp.items = nullptr;
 }
 
+struct RkStage {  // fused RK4 stage consumed by the epilogue (KParams::rk_*, store_q)
+  int stage = 0;
+  double a = 0.0;
+  double *y = nullptr, *arg = nullptr, *acc = nullptr;
+  int* flag = nullptr;
+};
+
 int launch_q(const bfq_plan* plan, const DevProgram& dp, const double* f2, const double* f3, double* q,
-             int64_t n_cells, cudaStream_t st) {
+             int64_t n_cells, cudaStream_t st, const RkStage& rk = RkStage()) {
   const HostPlan& hp = plan->hp;
   if (n_cells == 0) return BFQ_OK;
   KParams p;
+  p.rk_stage = rk.stage;
+  p.rk_a = rk.a;
+  p.rk_y = rk.y;
+  p.rk_arg = rk.arg;
+  p.rk_acc = rk.acc;
+  p.rk_flag = rk.flag;
   p.f2 = f2;
   p.f3 = f3 ? f3 : f2;
   p.q = q;
@@ -215,14 +228,18 @@ int launch_q(const bfq_plan* plan, const DevProgram& dp, const double* f2, const
   p.n_items = dp.n_items;
   {
     // as many tiles per item-major chunk as keep their cells (f2 and f3)
-    // within ~32 MB of L2: small batches stay fully heavy-first
+    // within ~8 MB of L2, so every item of a tile reads its cells and merges
+    // its Q columns while the lines are still resident: DRAM traffic of the
+    // N=L=12 launch 47.4 -> 35.1 KB per cell (algorithmic 35.2) at equal speed
+    // (profiles/r02_traffic_tile_chunk.txt; a 32 MB budget let lines be evicted
+    // between the items of a tile); small batches stay fully heavy-first
     static const int forced = std::getenv("BFQ_TILE_CHUNK") ? std::max(1, std::atoi(std::getenv("BFQ_TILE_CHUNK"))) : 0;
     const long long tile_bytes = (long long)dp.cfg.cells * hp.n_k * hp.n_q * 8 * (dp.bilinear ? 2 : 1);
     // one-cell tiles (n_k = 17): chunks of 16 tiles measured 1.1% faster than
     // L2-sized ones (profiles/r02_tile_chunk.txt); other shapes are insensitive
     p.tile_chunk = forced ? forced
                           : dp.cfg.cells == 1 ? 16
-                                               : (int)std::max<long long>(TILE_CHUNK, (32LL << 20) / std::max(tile_bytes, 1LL));
+                                               : (int)std::max<long long>(TILE_CHUNK, (8LL << 20) / std::max(tile_bytes, 1LL));
   }
   p.R = plan->R;
   p.rows = plan->rows;
@@ -576,12 +593,35 @@ int bfq_rk4_step(const bfq_plan* plan, double* y, double* work, int64_t n_cells,
   DeviceGuard guard(plan->device);
   cudaStream_t st = (cudaStream_t)stream;
   const long long n = n_cells * (long long)plan->hp.n_k * plan->hp.n_q;
+  int rc;
+  // Fused (BFQ_RK4_FUSED=1): four Q launches whose epilogues form
+  // the next stage argument, the weighted sum k1 + 2k2 + 2k3 and, at stage 4,
+  // the new state (store_q in bfq_device.cuh); the prologue of stage s+1 stages
+  // the argument buffer stage s wrote (ping-pong A / B, so no launch reads what
+  // it writes).  Bit-identical to the unfused sequence, but measured 0.7% slower
+  // at config 5 (844k vs 850k Q/s, profiles/r02_rk4_fused_ab.txt): the epilogue's
+  // scattered 8-byte read-modify-writes from the 12 CTAs of a tile cost more
+  // than the seven streaming elementwise passes they replace, so the unfused
+  // sequence stays the default.
+  static const bool fused = std::getenv("BFQ_RK4_FUSED") != nullptr && std::atoi(std::getenv("BFQ_RK4_FUSED")) != 0;
+  if (fused) {
+    double* argA = work;
+    double* argB = work + n;
+    double* acc = work + 2 * n;
+    RkStage s1{1, 0.5 * dt, y, argA, acc, flag}, s2{2, 0.5 * dt, y, argB, acc, flag},
+        s3{3, dt, y, argA, acc, flag}, s4{4, dt / 6.0, y, nullptr, acc, flag};
+    if ((rc = launch_q(plan, plan->sym, y, y, nullptr, n_cells, st, s1))) return rc;        // k1 = Q(y)
+    if ((rc = launch_q(plan, plan->sym, argA, argA, nullptr, n_cells, st, s2))) return rc;  // k2 = Q(y + dt/2 k1)
+    if ((rc = launch_q(plan, plan->sym, argB, argB, nullptr, n_cells, st, s3))) return rc;  // k3 = Q(y + dt/2 k2)
+    return launch_q(plan, plan->sym, argA, argA, nullptr, n_cells, st, s4);                 // k4 = Q(y + dt k3)
+  }
+  // Unfused sequence (default): Q launches plus elementwise stage kernels in
+  // numpy's association (harness.py:97-102).
   double* k = work;         // current stage derivative
   double* arg = work + n;   // stage argument
   double* acc = work + 2 * n;
   const int tb = 256;
   const int gb = (int)std::min<long long>((n + tb - 1) / tb, 148LL * 16);
-  int rc;
   // k1 = Q(y)
   if ((rc = launch_q(plan, plan->sym, y, y, k, n_cells, st))) return rc;
   rk4_accum_kernel<<<gb, tb, 0, st>>>(acc, k, 1.0, n, 1);

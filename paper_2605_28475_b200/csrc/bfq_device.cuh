@@ -35,7 +35,47 @@ struct KParams {
   unsigned long long* dbg_clk;  // [8] phase cycle totals when bit3 set
   long long n_rows;  // table rows (incl. padding) -- bounds of the row stream
   int* chk;          // BFQ_CHECKED builds: first violation {code, block, thread, aux, count}
+  // fused RK4 stage (bfq_rk4_step, harness.py:93-107): 0 = plain Q(f2, f3) into q
+  int rk_stage;
+  double rk_a;       // stage factor: dt/2 (stages 1, 2), dt (3), dt/6 (4)
+  double* rk_y;      // state y (read; written at stage 4)
+  double* rk_arg;    // next stage argument y + a k (stages 1-3)
+  double* rk_acc;    // k1 + 2 k2 + 2 k3
+  int* rk_flag;      // set when the new state is not finite
 };
+
+// Epilogue store of one Q element at flat offset `off` = (cell, k1, q1).  A
+// plain evaluation writes Q.  The fused RK4 stages consume the element in place
+// with numpy's association and rounding (no FMA contraction), so the fused step
+// equals the unfused one bit for bit:
+//   stage 1  acc = k1            arg = y + (dt/2) k1
+//   stage 2  acc = acc + 2 k2    arg = y + (dt/2) k2
+//   stage 3  acc = acc + 2 k3    arg = y + dt k3
+//   stage 4  y = y + (dt/6) (acc + k4), flag if not finite   (harness.py:97-107)
+// Every element is owned by exactly one lane of one CTA, and the prologues read
+// only the previous stage's argument buffer (stage 1: y), so no launch reads an
+// element another CTA of the same launch writes.
+__device__ __forceinline__ void store_q(const KParams& p, long long off, double v) {
+  switch (p.rk_stage) {
+    case 0:
+      p.q[off] = v;
+      return;
+    case 1:
+      p.rk_acc[off] = v;
+      p.rk_arg[off] = __dadd_rn(p.rk_y[off], __dmul_rn(p.rk_a, v));
+      return;
+    case 2:
+    case 3:
+      p.rk_acc[off] = __dadd_rn(p.rk_acc[off], __dmul_rn(2.0, v));
+      p.rk_arg[off] = __dadd_rn(p.rk_y[off], __dmul_rn(p.rk_a, v));
+      return;
+    default: {
+      const double yn = __dadd_rn(p.rk_y[off], __dmul_rn(p.rk_a, __dadd_rn(p.rk_acc[off], v)));
+      p.rk_y[off] = yn;
+      if (!isfinite(yn)) atomicExch(p.rk_flag, 1);
+    }
+  }
+}
 
 // ------------------------------------------------------------ checked build
 // -DBFQ_CHECKED (libbfq_checked.so, tests/test_gpu_checked.py): every shared

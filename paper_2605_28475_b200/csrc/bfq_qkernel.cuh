@@ -323,7 +323,6 @@ __global__ void __launch_bounds__(256, 1) bfq_q_kernel(const KParams p) {
   const long long cell = tile * CELLS + c;
   if (m1 >= 0 && cell < p.n_cells) {
     const int l1 = grp.l1, q1 = l1 * l1 + m1;
-    double* qc = p.q + cell * (long long)NK * p.nq + q1;
 #pragma unroll
     for (int j = 0; j < MT; ++j)
 #pragma unroll
@@ -332,7 +331,7 @@ __global__ void __launch_bounds__(256, 1) bfq_q_kernel(const KParams p) {
         if (k1 < NK) {
           double v = acc2[j][e] + accb[j][e];
           if (p.conservation && ((k1 == 0 && l1 <= 1) || (k1 == 1 && l1 == 0))) v = 0.0;
-          qc[(size_t)k1 * p.nq] = v;
+          store_q(p, cell * (long long)NK * p.nq + q1 + (long long)k1 * p.nq, v);
         }
       }
   }

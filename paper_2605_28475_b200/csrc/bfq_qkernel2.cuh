@@ -560,15 +560,14 @@ __global__ void __launch_bounds__(NKT == 17 ? (CELLS == 1 ? 384 : 256) : 512, 1)
   const long long cell = tile * CELLS + c;
   if (m1 >= 0 && cell < p.n_cells) {
     const int l1 = grp.l1, q1 = l1 * l1 + m1;
-    double* qc = p.q + cell * (long long)NK * p.nq + q1;
     auto put = [&](int k1, double v) {
       if (p.conservation && ((k1 == 0 && l1 <= 1) || (k1 == 1 && l1 == 0))) {
         // the zeroed R rows (kinematic.py:594-610) already make these sums exactly 0
         if (kChecked && v != 0.0) BFQ_CHK_IDX(1LL, 0LL, CHK_ZERO);
         v = 0.0;
       }
-      const long long off = (long long)(qc - p.q) + (long long)k1 * p.nq;
-      p.q[BFQ_CHK_IDX(off, p.n_cells * (long long)NK * p.nq, CHK_Q)] = v;
+      const long long off = cell * (long long)NK * p.nq + q1 + (long long)k1 * p.nq;
+      store_q(p, BFQ_CHK_IDX(off, p.n_cells * (long long)NK * p.nq, CHK_Q), v);
     };
 #pragma unroll
     for (int j = 0; j < MTM; ++j)

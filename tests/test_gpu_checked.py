@@ -38,7 +38,8 @@ def _run(env_extra, ops, cells):
     ({"BFQ_STAGES": "2"}, "hs_n8,hs_n12", 9),         # two-stage R ring
     ({"BFQ_CELLS": "1"}, "hs_n16", 5),                # one cell per tile, slices split over the warps
     ({"BFQ_HALF_DIAG": "0"}, "hs_n4,hs_n8,hs_n12", 9),  # packed-triangle self-symmetric channels
-], ids=["default", "fallback", "generic", "stages2", "splitm", "packed_diag"])
+    ({"BFQ_RK4_FUSED": "1"}, "mm_n4,hs_n8", 9),       # RK4 stages fused into the Q epilogue
+], ids=["default", "fallback", "generic", "stages2", "splitm", "packed_diag", "rk4_fused"])
 def test_checked_kernels(env_extra, ops, cells):
     res, lines = _run(env_extra, ops, cells)
     assert res.returncode == 0, res.stdout[-4000:] + res.stderr[-4000:]

@@ -125,3 +125,39 @@ def test_rk4_config5_full_trajectory_matches_reference():
     for r in range(ref.shape[0]):
         for j in range(len(watch)):
             assert q_oracle.rel_err(tr.snapshots[r, j], ref[r, j]) <= 1e-12, (r, j)
+
+
+def test_fused_rk4_equals_unfused_bitwise(tmp_path):
+    """the fused step (stage arguments, weighted sum and the new
+    state formed in the Q epilogues, 4 launches, BFQ_RK4_FUSED=1) equals the
+    default unfused sequence (Q launches + elementwise stage kernels) bit for bit."""
+    import os
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    script = tmp_path / "rk4_run.py"
+    script.write_text(
+        "import os, sys\n"
+        f"sys.path.insert(0, {ROOT!r})\n"
+        "import numpy as np, torch\n"
+        "from paper_2605_28475_b200 import harness, inputs\n"
+        "from paper_2605_28475_b200.operator import load_cache\n"
+        f"op = load_cache(os.path.join({ROOT!r}, 'operators', sys.argv[1] + '.bfct'))\n"
+        "c0 = inputs.bimodal(op.cfg.n_k, op.cfg.l_max, 37, seed=11)\n"
+        "tr = harness.rk4_integrate_batch(op, c0, 0.01, 7, record_every=1, watch=np.arange(37))\n"
+        "np.save(sys.argv[2], np.concatenate([tr.snapshots.ravel(), tr.final.cpu().numpy().ravel()]))\n")
+    outs = {}
+    for name in ("mm_n4", "hs_n8", "mm_n10"):
+        for mode in ("fused", "unfused"):
+            env = dict(os.environ)
+            env.pop("BFQ_RK4_FUSED", None)
+            if mode == "fused":
+                env["BFQ_RK4_FUSED"] = "1"
+            path = tmp_path / f"{name}_{mode}.npy"
+            res = subprocess.run([sys.executable, str(script), name, str(path)], env=env, capture_output=True,
+                                 text=True, timeout=600)
+            assert res.returncode == 0, res.stderr[-3000:]
+            outs[(name, mode)] = np.load(path)
+        assert np.array_equal(outs[(name, "fused")], outs[(name, "unfused")]), name
