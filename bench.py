@@ -122,35 +122,70 @@ def stratified_indices(n, k):
 
 
 # ------------------------------------------------------------------ CPU legs
-def _cpu_worker(args):
-    """Oracle Q of a block of cells in one process, one BLAS thread: the
-    reference's q_angular_first operations (oracle/q_oracle.py)."""
-    path, cells = args
-    import numpy as np
+REF_PKG = os.path.join(ROOT, "baseline", "_ref")  # the unmodified reference (pip --target), when shipped
 
-    from oracle import q_oracle
-    from paper_2605_28475_b200.operator import load_cache
+
+def live_reference():
+    """The reference's own package from baseline/_ref, or None."""
+    if not os.path.isdir(os.path.join(REF_PKG, "boltzfact")):
+        return None
+    if REF_PKG not in sys.path:
+        sys.path.insert(0, REF_PKG)
+    try:
+        from boltzfact import basis, cache, contraction  # noqa: F401
+    except Exception:  # pragma: no cover - broken install
+        return None
+    return contraction
+
+
+def _cpu_worker(args):
+    """CPU Q of a block of cells in one process, one BLAS thread: the LIVE
+    reference's evaluate(op, c) (angular_first, contraction.py:327-340) when
+    baseline/_ref is shipped, else the oracle port of its operations
+    (oracle/q_oracle.py).  Returns (Q, busy seconds, kind)."""
+    path, cells = args[0], args[1]
+    use_live = args[2] if len(args) > 2 else True
+    import numpy as np
 
     try:
         from threadpoolctl import threadpool_limits
     except ImportError:  # pragma: no cover
         threadpool_limits = None
+    contraction = live_reference() if use_live else None
+    out = np.empty_like(cells)
+    if contraction is not None:
+        from boltzfact import basis, cache
+
+        op = cache.load_cache(path)
+        contraction.evaluate(op, basis.CoefficientField(cells[0].copy(), op.cfg))  # builds the cached workspace
+        ctx = threadpool_limits(limits=1) if threadpool_limits else None
+        if ctx:
+            ctx.__enter__()
+        t0 = time.perf_counter()
+        for i, c in enumerate(cells):
+            out[i] = contraction.evaluate(op, basis.CoefficientField(np.array(c), op.cfg)).values
+        dt = time.perf_counter() - t0
+        if ctx:
+            ctx.__exit__(None, None, None)
+        return out, dt, "reference"
+    from oracle import q_oracle
+    from paper_2605_28475_b200.operator import load_cache
+
     op = q_oracle.OracleOperator.from_operator(load_cache(path))
     ws = q_oracle.angular_workspace(op)  # cached per operator, as the reference does
     ctx = threadpool_limits(limits=1) if threadpool_limits else None
     if ctx:
         ctx.__enter__()
-    out = np.empty_like(cells)
     t0 = time.perf_counter()
     for i, c in enumerate(cells):
         out[i] = q_oracle.q_angular_first(op, c, workspace=ws)
     dt = time.perf_counter() - t0
     if ctx:
         ctx.__exit__(None, None, None)
-    return out, dt
+    return out, dt, "port"
 
 
-def oracle_pool(path, cells, cores=None):
+def oracle_pool(path, cells, cores=None, live=True):
     """Oracle Q of ``cells`` on ``cores`` host processes (one thread each),
     contiguous blocks, the pattern of cli.py:406-410.  Returns (q, info):
     cells/s over the slowest worker's busy time, plus the 1-core rate."""
@@ -159,9 +194,9 @@ def oracle_pool(path, cells, cores=None):
     import numpy as np
 
     cores = max(1, min(cores or os.cpu_count() or 1, cells.shape[0]))
-    _, t1 = _cpu_worker((path, cells[:2]))  # 1-core rate (operator load + workspace excluded)
+    _, t1, _ = _cpu_worker((path, cells[:2], live))  # 1-core rate (operator load + workspace excluded)
     bounds = np.linspace(0, cells.shape[0], cores + 1).round().astype(int)
-    chunks = [(path, cells[bounds[i]:bounds[i + 1]]) for i in range(cores) if bounds[i + 1] > bounds[i]]
+    chunks = [(path, cells[bounds[i]:bounds[i + 1]], live) for i in range(cores) if bounds[i + 1] > bounds[i]]
     t0 = time.perf_counter()
     with mp.get_context("spawn").Pool(len(chunks)) as pool:
         res = pool.map(_cpu_worker, chunks)
@@ -169,7 +204,7 @@ def oracle_pool(path, cells, cores=None):
     q = np.concatenate([r[0] for r in res])
     busy = max(r[1] for r in res)
     return q, {"value": cells.shape[0] / busy, "cells": int(cells.shape[0]), "cores": len(chunks),
-               "busy_s": busy, "wall_s": wall, "single_core_cells_per_s": 2.0 / t1}
+               "busy_s": busy, "wall_s": wall, "single_core_cells_per_s": 2.0 / t1, "kind": res[0][2]}
 
 
 def free_port():
@@ -394,7 +429,7 @@ def run_reference(args, rank, world):
     cores = os.cpu_count() or 1
     # calibrate one cell, then size each step's sample to ~cpu_budget s per core
     probe = make_cells(args.config, op.cfg.n_k, op.cfg.l_max, 2, seed=args.seed, start=0)
-    _, t2 = _cpu_worker((path, probe))
+    _, t2, _ = _cpu_worker((path, probe))
     per_core = max(1, int(args.cpu_budget / max(t2 / 2, 1e-6)))
     n_sample = min(n_global, per_core * cores)
     # the leading cells of the batch (per-cell CPU cost does not depend on the values;
@@ -419,7 +454,10 @@ def run_reference(args, rank, world):
         "data": "synthetic (seeded, BASELINE.json distributions)",
         "config": {"workload": desc, "global_cells": n_global, "operator": opfile, "seed": args.seed,
                    "step": "one bounded sample of the workload on all host cores (multiprocessing pool)"},
-        "cpu_baseline": {"value": v, "unit": "cells/s", "cores": last["cores"], "kind": "port", "sample": sample,
+        "cpu_baseline": {"value": v, "unit": "cells/s", "cores": last["cores"], "kind": last["kind"],
+                         "sample": sample + ("; the live reference package (baseline/_ref): contraction.evaluate"
+                                             if last["kind"] == "reference" else
+                                             "; oracle/q_oracle.py (the reference's operations, bit-identical)"),
                          "cpu": cpu_model(), "single_core_cells_per_s": last["single_core_cells_per_s"]},
         "e2e": {"value": v, "unit": "cells/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -849,7 +887,9 @@ def run_ours(args, rank, world, local_rank):
                   "pass": bool(len(idx) and errs.max() <= 1e-12),
                   "selection": "every cell" if len(idx) == n_cells else
                   "stratified: evenly spread over the shard incl. first/last cell and the last tile",
-                  "metric": "max|Q_gpu - Q_oracle| / max|Q_oracle| per cell (test_contraction.py:63-65)",
+                  "metric": "max|Q_gpu - Q_ref| / max|Q_ref| per cell (test_contraction.py:63-65)",
+                  "against": ("the live reference's evaluate(op, c) (baseline/_ref)" if cpu["kind"] == "reference"
+                              else "the CPU oracle (oracle/q_oracle.py)"),
                   "invariant_slots_exact": bool(ok.item() == 1.0)}
     elif rk4:
         parity = {"skipped": "RK4 trajectory parity is tests/test_gpu_rk4.py (reference golden, every 100th step)",
@@ -913,11 +953,13 @@ def run_ours(args, rank, world, local_rank):
                        "full_run_estimate_s": 1000 * ms_per_step / 1e3}
     if world == 1 and cpu is not None:
         line["cpu_baseline"] = {
-            "value": cpu["value"], "unit": "cells/s", "cores": cpu["cores"], "kind": "port",
+            "value": cpu["value"], "unit": "cells/s", "cores": cpu["cores"], "kind": cpu["kind"],
             "sample": f"the {cpu['cells']} parity cells of the timed batch, contiguous blocks over {cpu['cores']} "
-                      f"processes (1 thread each), ~{cpu['busy_s']:.1f} s per process (oracle/q_oracle.py: the "
-                      "reference's q_angular_first operations, bit-identical to it and the same speed per cell, "
-                      "profiles/r01_cpu_ref_vs_port.txt)",
+                      f"processes (1 thread each), ~{cpu['busy_s']:.1f} s per process ("
+                      + ("the live reference package from baseline/_ref: boltzfact.contraction.evaluate"
+                         if cpu["kind"] == "reference" else
+                         "oracle/q_oracle.py: the reference's q_angular_first operations, bit-identical to it and "
+                         "the same speed per cell, profiles/r01_cpu_ref_vs_port.txt") + ")",
             "cpu": cpu_model(), "single_core_cells_per_s": cpu["single_core_cells_per_s"]}
     print(json.dumps(line), flush=True)
     if dist is not None:
