@@ -105,7 +105,8 @@ static bool choose_config(int nk, int qs, int k2s, int nf, int smem_limit, int m
   // 1 cell x 4 units, 2 rings 44.1k; 1 cell x 5 units (10 warps), 2 rings 44.9k;
   // 6 units with 1 ring 36.8k (one l1 group per CTA: packing 0.47).
   static const int popts1[][4] = {{1, 5, 1, 2}, {1, 4, 1, 2}, {1, 6, 1, 1}, {1, 4, 1, 1}};
-  if (kernel == 2 && (force_cells == 1 || (!force_cells && nk == 17))) {
+  // (SPLITM is instantiated for the compile-time n_k = 17 kernel only)
+  if (kernel == 2 && nk == 17 && !std::getenv("BFQ_GENERIC") && (force_cells == 1 || !force_cells)) {
     for (auto o0 : popts1) {
       int o[4] = {o0[0], o0[1], o0[2], force_teams ? force_teams : o0[3]};
       if (force_units && o[1] != force_units) continue;

@@ -19,7 +19,7 @@
 // independent DMMA chains per warp (ncu at 8 warps: 37% "wait" stalls on the
 // single chain); the second group of an odd tail has g = 0 (fetch_row_bf).
 template <int MT, int CELLS, bool BILIN, int NKT, int QST>
-__global__ void __launch_bounds__(NKT == 17 ? (CELLS == 1 ? 384 : 256) : 512, 1) bfq_q_kernel2(const KParams p) {
+__global__ void __launch_bounds__(MT == 3 ? (CELLS == 1 ? 384 : 256) : 512, 1) bfq_q_kernel2(const KParams p) {
   constexpr int M1T = 8 / CELLS;
   // Stage-1 split of a unit over its two warps: by cells (warp h takes cells
   // h*HC..h*HC+HC-1, every slice), or -- one cell per tile (SPLITM, n_k = 17:

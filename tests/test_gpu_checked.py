@@ -39,7 +39,8 @@ def _run(env_extra, ops, cells):
     ({"BFQ_CELLS": "1"}, "hs_n16", 5),                # one cell per tile, slices split over the warps
     ({"BFQ_HALF_DIAG": "0"}, "hs_n4,hs_n8,hs_n12", 9),  # packed-triangle self-symmetric channels
     ({"BFQ_RK4_FUSED": "1"}, "mm_n4,hs_n8", 9),       # RK4 stages fused into the Q epilogue
-], ids=["default", "fallback", "generic", "stages2", "splitm", "packed_diag", "rk4_fused"])
+    ({"BFQ_GENERIC": "1"}, "hs_n16", 3),              # run-time-size kernel with three tiles per axis
+], ids=["default", "fallback", "generic", "stages2", "splitm", "packed_diag", "rk4_fused", "generic_mt3"])
 def test_checked_kernels(env_extra, ops, cells):
     res, lines = _run(env_extra, ops, cells)
     assert res.returncode == 0, res.stdout[-4000:] + res.stderr[-4000:]
