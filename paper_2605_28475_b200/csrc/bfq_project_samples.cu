@@ -13,14 +13,15 @@
 // B200 mapping.  The azimuthal sum is the only one with grid-sized work:
 // G[t][col] = sum_p f[t][p] W[p][col] is a GEMM per (cell, v) slab with M = t,
 // N = 2 l_max + 1, K = p, run on DMMA.8x8x4 (FP64 tensor pipe).  One CTA per
-// cell walks its samples in t-chunks of 32 rows: the polar-table chunk stays in
-// shared memory while the (v) slabs of that chunk stream through a ring of
-// cp.async buffers (8-byte granules: rows of n_p doubles are not 16-byte
-// aligned), so the HBM stream -- the roofline of this kernel at quadrature
-// order ~64 -- overlaps the DMMAs.  The polar and radial sums (O(n_q n_t) and
-// O(n_q n_k) per slab) run on DFMA out of shared memory, and the radial sum is
-// applied per chunk (the whole map is linear), so no per-v intermediate is kept.
-// The coefficient accumulator lives in shared memory: deterministic.
+// cell walks its samples in t-chunks of 32 rows (chunk outer, v inner): the
+// polar-table chunk stays in shared memory while the (v) slabs stream through
+// a ring of cp.async buffers (8-byte granules: rows of n_p doubles are not
+// 16-byte aligned), so the HBM stream overlaps the DMMAs.  The CTA is warp-
+// specialized: 8 GEMM warps produce G (and copy the v's radial table) into one
+// of two G buffers while 4 epilogue warps consume the other -- the polar sum
+// (O(n_q n_t) per slab) and the radial sum (O(n_q n_k)), applied per chunk
+// (the whole map is linear), each epilogue thread owning whole coefficient
+// columns q in registers.  Deterministic and position independent.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -124,8 +125,7 @@ __global__ void __launch_bounds__(PS_THREADS, 1) k_project_samples(const PsParam
   double* pt = wf + (size_t)p.ks * p.ntile * 32;   // [npl][TCP] polar chunk
   double* g = pt + (size_t)p.npl * TCP;            // [2][gsz]    G buffers
   double* acc = g + (size_t)2 * gsz;               // [nk][nq]   coefficients of the cell
-  double* aq = acc + (size_t)p.nk * p.nq;          // [nq]       polar sums of one (chunk, v)
-  int* lq = reinterpret_cast<int*>(aq + p.nq);     // [nq]       l(q)
+  int* lq = reinterpret_cast<int*>(acc + (size_t)p.nk * p.nq);  // [nq] l(q)
   for (int i = tid; i < p.ks * p.ntile * 32; i += PS_THREADS) wf[i] = p.wfrag[i];
   for (int i = tid; i < p.nbuf * slab; i += PS_THREADS) buf[i] = 0.0;  // zero padding rows/columns
   for (int i = tid; i < p.nk * p.nq; i += PS_THREADS) acc[i] = 0.0;
@@ -339,7 +339,7 @@ int bfq_projector_create(int32_t k_max, int32_t l_max, int32_t n_v, int32_t n_t,
   auto smem_for = [&](int nbuf) {
     const size_t rvp = ((size_t)(l_max + 1) * pj->nk + 1) / 2 * 2;  // radial table of one v, padded
     return (size_t)8 * ((size_t)nbuf * (TC * pj->sp + rvp) + (size_t)pj->ks * pj->ntile * 32 + (size_t)npl * TCP +
-                        2 * ((size_t)TC * gs + rvp) + (size_t)pj->nk * pj->nq + pj->nq) +
+                        2 * ((size_t)TC * gs + rvp) + (size_t)pj->nk * pj->nq) +
            (size_t)4 * pj->nq;  // l(q) table
   };
   pj->nbuf = smem_for(3) <= (size_t)optin ? 3 : 2;
