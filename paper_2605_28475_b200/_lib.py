@@ -217,6 +217,13 @@ def lib():
     global _lib
     if _lib is None:
         with _lock:
+            if _lib is None and os.environ.get("BFQ_AB_LIB"):
+                # A/B tooling only (tools/gpu/ablib.sh): load a library built from
+                # another revision, without the source-hash check
+                handle = ctypes.CDLL(os.environ["BFQ_AB_LIB"])
+                _declare(handle)
+                _lib = handle
+                return _lib
             if _lib is None:
                 _ensure_current(LIB_PATH)
                 if not os.path.exists(LIB_PATH):
