@@ -1001,6 +1001,18 @@ def main():
     world = env_int("WORLD_SIZE", 1)
     rank = env_int("RANK", 0)
     local_rank = env_int("LOCAL_RANK", 0)
+    if args.backend == "gloo" and not args.dry_run:
+        # functional multi-rank run on fewer GPUs than ranks (gloo only; NCCL
+        # needs one GPU per rank): ranks share devices round-robin.  Not a
+        # scaling measurement -- the ranks then contend for the same SMs.
+        try:
+            import torch
+
+            n_dev = torch.cuda.device_count()
+            if n_dev and local_rank >= n_dev:
+                local_rank %= n_dev
+        except Exception:  # pragma: no cover
+            pass
     if args.impl == "reference":
         run_reference(args, rank, world)
     elif args.config in RBUILD:

@@ -61,3 +61,26 @@ def test_moments_kernel_matches_oracle():
     for i in range(host.shape[0]):
         mass, mom, energy = q_oracle.moments(host[i])
         assert got[i, 0] == mass and np.array_equal(got[i, 1:4], mom) and got[i, 4] == energy, i
+
+
+def test_bench_two_ranks_functional():
+    """The multi-rank bench path end to end on the GPU: ``bench.py --gpus 2``
+    launches two ranks (gloo, sharing the device when only one exists), shards
+    one fixed batch, checks rank 0's outputs against the oracle and reduces
+    the per-rank times -- a functional check, not a scaling number."""
+    import json
+    import subprocess
+
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--backend", "gloo",
+                          "--config", "hs8", "--cells", "1000", "--steps", "2", "--warmup", "1", "--e2e-steps", "1",
+                          "--parity-cells", "16"], capture_output=True, text=True, timeout=900, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["global_cells"] == 1000 and d["config"]["cells_per_rank"] == 500
+    assert len(d["rank_ms"]) == 2 and d["ms_per_step"] > 0
+    assert d["parity"]["pass"] and d["conservation"]["invariant_slots_exact"]
+    assert d["conservation"]["cells"] == 1000.0
