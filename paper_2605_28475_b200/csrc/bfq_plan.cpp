@@ -505,6 +505,39 @@ static void reorder_rows_for_banks(HostPlan& hp, const int64_t* slice_starts, in
         hp.rows[out++] = tmp[best];
       }
     }
+    // Local search on top of the greedy grouping: swap rows between k-step
+    // groups of the slice while that lowers the total gather wavefronts.
+    if (n <= 96 && !std::getenv("BFQ_NO_ROW_SWAP")) {
+      const int ng = (n + 3) / 4;
+      auto gcost = [&](int g) {
+        int a2[4], a3[4], m = 0;
+        for (int j = 0; j < 4 && 4 * g + j < n; ++j, ++m) {
+          a2[m] = hp.rows[a + 4 * g + j].q2;
+          a3[m] = hp.rows[a + 4 * g + j].q3;
+        }
+        return group_wavefronts(a2, m, hp.qs) + group_wavefronts(a3, m, hp.qs);
+      };
+      std::vector<int> cost(ng);
+      for (int g = 0; g < ng; ++g) cost[g] = gcost(g);
+      for (int pass = 0; pass < 4; ++pass) {
+        bool improved = false;
+        for (int i = 0; i < n; ++i)
+          for (int j = i + 1; j < n; ++j) {
+            const int gi = i / 4, gj = j / 4;
+            if (gi == gj) continue;
+            std::swap(hp.rows[a + i], hp.rows[a + j]);
+            const int ci = gcost(gi), cj = gcost(gj);
+            if (ci + cj < cost[gi] + cost[gj]) {
+              cost[gi] = ci;
+              cost[gj] = cj;
+              improved = true;
+            } else {
+              std::swap(hp.rows[a + i], hp.rows[a + j]);
+            }
+          }
+        if (!improved) break;
+      }
+    }
   }
 }
 
