@@ -398,22 +398,32 @@ __global__ void __launch_bounds__(MT == 3 ? (CELLS == 1 ? 384 : 256) : 512, 1) b
             // store-order K of row / column L = n_k - 1 = 8 (MT - 1): tile row or
             // column MT - 1 holds one index (r0 = 0 or kq = e = 0)
             constexpr int L = NKT - 1, TL = MT - 1;
-            if (kq == 0) {
+            // after the butterfly every kq lane of row r0 holds the sums: at n_k = 9
+            // (shared-memory-bound) lanes kq = 0 store the row value and lanes kq = 1
+            // the column value in ONE store per t (2 wavefronts for 16 values;
+            // +1.4% there, -0.2% at n_k = 17: profiles/r02_x1_store_ab.txt)
+            constexpr bool XCOMB = NKT == 9;
+            if (XCOMB ? kq <= 1 : kq == 0) {
 #pragma unroll
               for (int t = 0; t < MTM; ++t) {
                 if (!DGC) {
                   // Phi[L][8t + r0]: tile (TL, t), half r0 & 1, kq' = r0 >> 1
                   const int kr = ((r0 & 1) ? phi_base(NKT, TL, t, 1) : phi_base(NKT, TL, t, 0)) + (r0 >> 1);
-                  sts_v(BFQ_CHK(ph + (uint32_t)kr * 8u, ph, ph + (uint32_t)K2S * 8u, CHK_PHI_ST), xr[cc][t]);
                   // Phi[8t + r0][L]: tile (t, TL), half 0, kq' = 0 (one valid kq)
                   const int kc = phi_base(NKT, t, TL, 0) + r0 * kq_count(NKT, TL, 0);
-                  sts_v(BFQ_CHK(ph + (uint32_t)kc * 8u, ph, ph + (uint32_t)K2S * 8u, CHK_PHI_ST), xc[cc][t]);
-                } else {
+                  if constexpr (XCOMB) {
+                    sts_v(BFQ_CHK(ph + (uint32_t)(kq == 0 ? kr : kc) * 8u, ph, ph + (uint32_t)K2S * 8u, CHK_PHI_ST),
+                          kq == 0 ? xr[cc][t] : xc[cc][t]);
+                  } else {
+                    sts_v(BFQ_CHK(ph + (uint32_t)kr * 8u, ph, ph + (uint32_t)K2S * 8u, CHK_PHI_ST), xr[cc][t]);
+                    sts_v(BFQ_CHK(ph + (uint32_t)kc * 8u, ph, ph + (uint32_t)K2S * 8u, CHK_PHI_ST), xc[cc][t]);
+                  }
+                } else if (kq == 0) {
                   const int kc = phid_base(NKT, t, TL, 0) + r0 * kq_count(NKT, TL, 0);
                   sts_v(BFQ_CHK(ph + (uint32_t)kc * 8u, ph, ph + (uint32_t)K2S * 8u, CHK_PHI_ST), xc[cc][t]);
                 }
               }
-              if (r0 == 0) {
+              if (r0 == 0 && kq == 0) {
                 const int pl = DGC ? phid_k(NKT, L, L) : phi_k(NKT, L, L);
                 sts_v(BFQ_CHK(ph + (uint32_t)pl * 8u, ph, ph + (uint32_t)K2S * 8u, CHK_PHI_ST), xd[cc]);
               }
