@@ -300,21 +300,15 @@ def q_gpu(op, c, c2=None, stats=None):
     Signature and result type follow the reference strategies
     (contraction.py:293-317): returns ``type(c)(values, cfg)``.
     """
-    import torch
-
     cfg = op.cfg
     if c.values.shape != (cfg.n_k, cfg.n_q):
         raise ValueError("coefficient field does not match the operator")
     if c2 is not None and c2.values.shape != (cfg.n_k, cfg.n_q):
         raise ValueError("coefficient field does not match the operator")
-    plan = plan_for(op)
     t0 = time.perf_counter()
-    dev = torch.device("cuda", plan.device)
-    f = torch.from_numpy(np.ascontiguousarray(c.values, dtype=np.float64)).to(dev).unsqueeze(0)
-    f3 = None
-    if c2 is not None:
-        f3 = torch.from_numpy(np.ascontiguousarray(c2.values, dtype=np.float64)).to(dev).unsqueeze(0)
-    q = evaluate_batch(plan, f, f3)[0].cpu().numpy()
+    # one C-ABI call (bfq_eval_host: staged H2D, Q launch, D2H, sync) -- no torch
+    # tensors on the per-cell path (profiles/r02_dropin_latency.json)
+    q = evaluate_host(op, c.values[None], None if c2 is None else c2.values[None])[0]
     _record(stats, op, time.perf_counter() - t0)
     return type(c)(q, c.cfg)
 
