@@ -622,7 +622,6 @@ def run_project(args, rank, world, local_rank):
             starts[i].record(stream)
             pj.project(samples, out)
             ends[i].record(stream)
-            clk.sample()
         clk.sample()
         torch.cuda.synchronize(dev)
     step_ms = [a.elapsed_time(b) for a, b in zip(starts, ends)]
@@ -800,7 +799,8 @@ def run_ours(args, rank, world, local_rank):
             starts[i].record(stream)
             one_step()
             ends[i].record(stream)
-            clk.sample()  # queued work is still running
+        # (the sampler thread polls NVML every 2 ms while the queued steps run; a
+        # synchronous NVML query between enqueues could starve the launch queue)
         clk.sample()
         barrier()
         wall = time.perf_counter() - t0
