@@ -25,6 +25,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstdint>
 #include <string>
@@ -44,6 +45,11 @@ struct bfq_projector {
   double* wfrag = nullptr;  // [ks][ntile][32] B fragments of W (zero padded)
   double* ptab = nullptr;   // [nchunk][(L+1)(L+2)/2][TC] polar table, t-chunked, zero padded
   double* rtab = nullptr;   // [nv][L+1][nk] radial table
+  // v2 kernel (k_project_v2): used when the shape fits its register tiles
+  bool v2 = false;
+  int kfull = 0, ks2 = 0, slot2 = 0, nbuf2 = 0, kb2 = 0;
+  size_t smem2 = 0;
+  double* wreg = nullptr;   // [ntile][ks2][32] A fragments of W^T, K permuted
 };
 
 namespace {
@@ -270,6 +276,336 @@ __global__ void __launch_bounds__(PS_THREADS, 1) k_project_samples(const PsParam
   }
 }
 
+// ---------------------------------------------------------------- v2 kernel
+// The same three sums with the operand traffic cut to what the FP64 tensor
+// pipe needs (the v1 kernel above is shared-memory-wavefront bound, ncu ~60%):
+//
+// * azimuthal GEMM transposed, G^T[col][t] = sum_p W^T[col][p] f[t][p]: the A
+//   operand W^T is the same for every slab, so each GEMM warp keeps the
+//   fragments of ONE column tile and ONE part of the K axis in REGISTERS and
+//   loads only the B fragments f[t][p] of the chunk's four polar tiles -- one
+//   shared load per DMMA (v1: 1.5) and four independent accumulator chains per
+//   warp.  The KP partial products of a column tile are added in a fixed order
+//   (deterministic) by the part-0 warp, which stores G;
+// * the slab (TC polar rows x n_p samples, contiguous in HBM) lands with one
+//   cp.async.bulk + mbarrier per ring slot, unpadded (v1: 8-byte cp.async per
+//   element into padded rows).  Conflict-free gathers without padding come
+//   from the K order: inside every 16-sample block, k-step j of lane kq reads
+//   sample 16 B + j + 4 kq, so a half-warp (rows r0 = 0..3, kq = 0..3) hits
+//   r0 n_p + 4 kq (mod 16): distinct for odd n_p (n_p = 2 n_t + 1 always);
+//   the W fragments are permuted the same way on the host.  The last partial
+//   block keeps the natural order; its samples past n_p meet W = 0;
+// * epilogue: a lane PAIR per (l, |m|) row instead of a thread per coefficient
+//   column: each lane of the pair takes every other polar row of the chunk and
+//   reads the (sin, cos) pair G[t][col(-m)], G[t][col(+m)] with one 16-byte
+//   load (G is stored |m|-major), so P[l,|m|][t] is loaded once for both
+//   signs of m; the halves meet by one shuffle, and the lanes split the radial
+//   sums (k < h / k >= h) of both columns in registers.  Its DFMAs share the
+//   FP64 pipe with the DMMA stream, so it runs on 8 warps with 4 G buffers of
+//   slack behind the GEMM.
+constexpr int V2_EPI_WARPS = 8;
+constexpr int V2_GA = 2 * TC + 4;  // doubles per |m| block of a G buffer ([t][sin, cos]); = 4 (mod 16):
+                                   // the epilogue's 16-byte loads of a quarter-warp hit distinct banks
+constexpr int V2_TCP = TC + 2;     // row stride of the polar chunk: = 2 (mod 16), the lane pairs
+                                   // (row r, half h) of a half-warp read r V2_TCP + h: distinct banks
+constexpr int V2_NKMAX = 17;       // n_k <= 17: radial accumulators (half of them per lane) in registers
+constexpr int V2_KH = (V2_NKMAX + 1) / 2;
+constexpr int V2_MAXBUF = 6;
+constexpr int V2_NGB = 4;  // G buffers: the epilogue may lag the GEMM by three slabs
+constexpr unsigned V2_BAR_FULL0 = 2, V2_BAR_EMPTY0 = 2 + V2_NGB, V2_BAR_EPI = 2 + 2 * V2_NGB,
+                   V2_BAR_RED0 = 3 + 2 * V2_NGB;  // + column tile: the K-part reduction
+
+struct Ps2Params {
+  const double* f;
+  double* out;
+  long long n;
+  int nk, L, nq, nv, nt, np, ncol, ks, kfull, nchunk, npl, nbuf, slot;
+  const double* wreg;  // [ntile][ks][32] A fragments of W^T, K permuted as above
+  const double* ptab;  // [nchunk][npl][TC]
+  const double* rtab;  // [nv][L+1][nk]
+};
+
+// GEMM warps = column tiles x K parts (a multiple of 4: one per scheduler).
+// The K axis is split in whole 16-sample blocks (4 k-steps each, immediate
+// shared-memory offsets); the natural-order tail steps (n_p mod 16 samples)
+// go to the last part, which does not reduce.
+template <int NTILE>
+struct V2Shape {
+  static constexpr int KP = NTILE == 4 ? 2 : 4;
+  static constexpr int GW = NTILE * KP;
+  static constexpr int THREADS = (GW + V2_EPI_WARPS) * 32;
+};
+constexpr int V2_TAIL = 4;  // tail k-steps: ceil(15 / 4)
+
+__device__ __forceinline__ double2 lds128_v(uint32_t addr) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(addr) : "memory");
+  return v;
+}
+
+template <int NTILE, int KB>  // KB: most 16-sample blocks of any K part (the others may have one fewer)
+__global__ void __launch_bounds__(V2Shape<NTILE>::THREADS, 1) k_project_v2(const Ps2Params p) {
+  constexpr int KP = V2Shape<NTILE>::KP, GW = V2Shape<NTILE>::GW;
+  constexpr int NTH = V2Shape<NTILE>::THREADS, NT_G = GW * 32, NT_E = V2_EPI_WARPS * 32;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);  // [V2_MAXBUF] slab landed
+  uint64_t* empty = full + V2_MAXBUF;                         // [V2_MAXBUF] slab released by every GEMM warp
+  double* ring = reinterpret_cast<double*>(smem_raw + 128);  // [nbuf][slot]
+  const int gsz = (p.L + 1) * V2_GA;
+  double* gbuf = ring + (size_t)p.nbuf * p.slot;            // [NGB][L+1][GA]
+  double* red = gbuf + (size_t)V2_NGB * gsz;                // [2][NTILE][KP-1][8][32] K-part partials
+  double* pt = red + (size_t)2 * NTILE * (KP - 1) * 8 * 32; // [npl][V2_TCP]
+  const long long cell = blockIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, r0 = lane >> 2, kq = lane & 3;
+  // the ring starts zeroed: samples past a row (K padding) and the rows of a
+  // partial polar chunk are read as finite values that meet W = 0 / P = 0
+  for (int i = tid; i < p.nbuf * p.slot / 2; i += NTH) reinterpret_cast<double2*>(ring)[i] = make_double2(0.0, 0.0);
+  if (tid == 0) {
+    for (int b = 0; b < p.nbuf; ++b) {
+      mbar_init(&full[b], 1);
+      mbar_init(&empty[b], GW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // zeros before the bulk copies
+  __syncthreads();
+  const int nsteps = p.nchunk * p.nv;  // (chunk outer, v inner)
+  const long long cell_off = cell * (long long)p.nv * p.nt * p.np;
+  // slab s: element range [e0, e0 + cnt) of f; smem index of element e is
+  // (e - e0) + m, m = 1 when f + e0 is not 16-byte aligned
+  auto geom = [&](int s, long long& e0, int& cnt, int& m) {
+    const int c = s / p.nv, v = s - c * p.nv, t0 = c * TC;
+    e0 = cell_off + ((long long)v * p.nt + t0) * p.np;
+    cnt = min(TC, p.nt - t0) * p.np;
+    m = (int)((reinterpret_cast<uintptr_t>(p.f + e0) >> 3) & 1);
+  };
+
+  if (warp < GW) {
+    // ------------------------------------------------ producer: samples -> G
+    const int j = warp % NTILE, part = warp / NTILE;
+    // this warp's blocks [b0, b0 + nb) of the n_p / 16 full blocks; the last
+    // part also takes the tail k-steps [4 nfull, ks)
+    const int nfull = p.kfull / 4, bq = nfull / KP, br = nfull - bq * KP;
+    const int nb = bq + (part >= KP - br ? 1 : 0);  // the extra blocks go to the last parts
+    const int b0 = part * bq + max(0, part - (KP - br));
+    const int ntail = part == KP - 1 ? p.ks - p.kfull : 0;
+    double wr[KB * 4], wt[V2_TAIL];
+    {
+      const double* ws = p.wreg + ((size_t)j * p.ks + 4 * b0) * 32 + lane;
+#pragma unroll
+      for (int k = 0; k < KB * 4; ++k) wr[k] = k < 4 * nb ? __ldg(ws + k * 32) : 0.0;
+      const double* wq = p.wreg + ((size_t)j * p.ks + p.kfull) * 32 + lane;
+#pragma unroll
+      for (int k = 0; k < V2_TAIL; ++k) wt[k] = k < ntail ? __ldg(wq + k * 32) : 0.0;
+    }
+    const bool full_kb = nb == KB;
+    // one thread issues: head / tail elements by hand, the rest in one bulk
+    // copy; a refilled slot waits for every GEMM warp's release of its
+    // previous slab (empty[]); the mbarrier arrive publishes the generic stores
+    auto issue = [&](int s) {
+      if (s >= nsteps) return;
+      long long e0;
+      int cnt, m;
+      geom(s, e0, cnt, m);
+      const int b = s % p.nbuf;
+      if (s >= p.nbuf) mbar_wait(&empty[b], (unsigned)(((s / p.nbuf) - 1) & 1));
+      double* dst = ring + (size_t)b * p.slot;
+      const int nin = (cnt - m) & ~1;
+      if (m) dst[1] = __ldg(p.f + e0);
+      if ((cnt - m) & 1) dst[m + cnt - 1] = __ldg(p.f + e0 + cnt - 1);
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // earlier generic stores to the slot
+      mbar_arrive_expect_tx(&full[b], (unsigned)nin * 8u);
+      if (nin > 0) bulk_g2s(dst + 2 * m, p.f + e0 + m, (unsigned)nin * 8u, &full[b]);
+    };
+    if (tid == 0)
+      for (int s = 0; s < p.nbuf - 1; ++s) issue(s);
+    const int col = 8 * j + r0;
+    const int ga = (col + 1) >> 1, side = (col & 1) ? 0 : 1;  // col 2a-1: sin (m = -a), col 2a: cos (m = +a)
+    for (int s = 0; s < nsteps; ++s) {
+      // slab s + nbuf - 2 into the slot of slab s - 2 (one slab of slack for its release)
+      if (tid == 0 && s >= 1) issue(s + p.nbuf - 2);
+      const int b = s % p.nbuf;
+      mbar_wait(&full[b], (unsigned)((s / p.nbuf) & 1));
+      long long e0;
+      int cnt, m;
+      geom(s, e0, cnt, m);
+      // the B gathers are plain (reorderable) loads; this zero, produced after
+      // the wait, keeps them from being hoisted above it
+      uint32_t after_wait;
+      asm volatile("mov.u32 %0, 0;\n" : "=r"(after_wait)::"memory");
+      const uint32_t base = smem_u32(ring + (size_t)b * p.slot) + (uint32_t)(m + r0 * p.np) * 8u + after_wait;
+      const uint32_t tstep = (uint32_t)(8 * p.np) * 8u;  // one polar tile
+      uint32_t rowb[4];  // block b0, lane offset 4 kq, polar tile i: k-step (block, jj) is +(16 block + jj) doubles
+#pragma unroll
+      for (int i = 0; i < 4; ++i) rowb[i] = base + (uint32_t)(16 * b0 + 4 * kq) * 8u + (uint32_t)i * tstep;
+      double acc[4][2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = 0.0;
+      auto kstep = [&](double w, uint32_t off) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) dmma884(acc[i][0], acc[i][1], w, lds_ro(rowb[i] + off));
+      };
+#pragma unroll
+      for (int blk = 0; blk < KB - 1; ++blk)
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) kstep(wr[4 * blk + jj], (uint32_t)(16 * blk + jj) * 8u);
+      if (full_kb) {
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) kstep(wr[4 * (KB - 1) + jj], (uint32_t)(16 * (KB - 1) + jj) * 8u);
+      }
+      if (ntail > 0) {  // natural order: sample 16 nfull + 4 u + kq
+        const uint32_t tb = (uint32_t)(16 * (nfull - b0) - 3 * kq) * 8u;
+#pragma unroll
+        for (int u = 0; u < V2_TAIL; ++u)
+          if (u < ntail) kstep(wt[u], tb + (uint32_t)(4 * u) * 8u);
+      }
+      const int b2 = s % V2_NGB;
+      // partials of the K parts, double-buffered by slab parity: a part writes
+      // buffer (s & 1) again at slab s + 2, after the pair barrier of s + 1,
+      // which part 0 reaches only after reading it at slab s
+      double* rbuf = red + (size_t)(s & 1) * NTILE * (KP - 1) * 8 * 32;
+      if (part > 0) {
+        const uint32_t rw = smem_u32(rbuf + (size_t)(j * (KP - 1) + part - 1) * 8 * 32 + lane);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          sts_v(rw + (uint32_t)(64 * i) * 8u, acc[i][0]);
+          sts_v(rw + (uint32_t)(64 * i + 32) * 8u, acc[i][1]);
+        }
+        bar_sync(V2_BAR_RED0 + j, KP * 32);
+      } else {
+        bar_sync(V2_BAR_RED0 + j, KP * 32);
+        if constexpr (KP > 1) {
+          // fixed order: ((p0 + p1) + p2) + p3
+#pragma unroll
+          for (int q = 0; q < KP - 1; ++q) {
+            const uint32_t rq = smem_u32(rbuf + (size_t)(j * (KP - 1) + q) * 8 * 32 + lane);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              acc[i][0] += lds_v(rq + (uint32_t)(64 * i) * 8u);
+              acc[i][1] += lds_v(rq + (uint32_t)(64 * i + 32) * 8u);
+            }
+          }
+        }
+        if (s >= V2_NGB) bar_sync(V2_BAR_EMPTY0 + b2, NTH - (GW - NTILE) * 32);  // epilogue consumed b2
+        if (col < p.ncol) {
+          const uint32_t gb = smem_u32(gbuf + (size_t)b2 * gsz + (size_t)ga * V2_GA + side);
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) sts_v(gb + (uint32_t)(2 * (8 * i + 2 * kq + e)) * 8u, acc[i][e]);
+        }
+        __threadfence_block();
+        bar_arrive(V2_BAR_FULL0 + b2, NTH - (GW - NTILE) * 32);
+      }
+      // release ring slot b: after the stores above, which consume every gather
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[b]);
+    }
+  } else {
+    // ------------------------------------------------ consumer: G -> coefficients
+    const int et = tid - NT_G, r = et >> 1, hf = et & 1;  // (l, |m|) row of this lane pair, half
+    int l = (int)((sqrtf(8.0f * (float)r + 1.0f) - 1.0f) * 0.5f);
+    while (l * (l + 1) / 2 > r) --l;
+    while ((l + 1) * (l + 2) / 2 <= r) ++l;
+    const int a = r - l * (l + 1) / 2;
+    const bool live = r < p.npl;
+    const int kh = (p.nk + 1) / 2, kb = hf ? kh : 0, ke = hf ? p.nk : kh;  // this lane's radial indices
+    double racc[2][V2_KH];
+#pragma unroll
+    for (int k = 0; k < V2_KH; ++k) racc[0][k] = racc[1][k] = 0.0;
+    const uint32_t prow = smem_u32(pt + (size_t)r * V2_TCP + hf);  // this lane's polar rows: t = 2 u + hf
+    for (int s = 0; s < nsteps; ++s) {
+      const int c = s / p.nv, v = s - c * p.nv, b2 = s % V2_NGB;
+      if (v == 0) {  // new chunk: its polar table (after every epilogue thread finished the old one)
+        bar_sync(V2_BAR_EPI, NT_E);
+        for (int i = et; i < p.npl * TC; i += NT_E) {
+          const int row = i / TC;
+          pt[row * V2_TCP + (i - row * TC)] = p.ptab[(size_t)c * p.npl * TC + i];
+        }
+      }
+      // radial factors of this slab's v (global / L1; issued before the wait)
+      double rk[V2_KH];
+      const double* rv = p.rtab + ((size_t)v * (p.L + 1) + l) * p.nk + kb;
+#pragma unroll
+      for (int k = 0; k < V2_KH; ++k) rk[k] = (live && kb + k < ke) ? __ldg(rv + k) : 0.0;
+      bar_sync(V2_BAR_FULL0 + b2, NTH - (GW - NTILE) * 32);  // G buffer b2 written (also orders pt)
+      double as = 0.0, ac = 0.0;
+      if (live) {
+        // the pair interleaves its rows (t = 2 u + hf): the two lanes hit adjacent banks
+        const uint32_t g = smem_u32(gbuf + (size_t)b2 * gsz + (size_t)a * V2_GA) + (uint32_t)(2 * hf) * 8u;
+        double sa[4] = {0.0, 0.0, 0.0, 0.0}, ca[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int t = 0; t < TC / 2; t += 4) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const double2 gv = lds128_v(g + (uint32_t)(4 * (t + u)) * 8u);
+            const double pv = lds_v(prow + (uint32_t)(2 * (t + u)) * 8u);
+            sa[u] = fma(pv, gv.x, sa[u]);
+            ca[u] = fma(pv, gv.y, ca[u]);
+          }
+        }
+        as = (sa[0] + sa[1]) + (sa[2] + sa[3]);
+        ac = (ca[0] + ca[1]) + (ca[2] + ca[3]);
+      }
+      __threadfence_block();
+      bar_arrive(V2_BAR_EMPTY0 + b2, NTH - (GW - NTILE) * 32);  // buffer b2 may be rewritten
+      // both halves of the row, added in the same order on both lanes
+      const double os = __shfl_xor_sync(0xffffffffu, as, 1), oc = __shfl_xor_sync(0xffffffffu, ac, 1);
+      const double ts = hf ? os + as : as + os, tcv = hf ? oc + ac : ac + oc;
+#pragma unroll
+      for (int k = 0; k < V2_KH; ++k) {
+        racc[0][k] = fma(rk[k], ts, racc[0][k]);
+        racc[1][k] = fma(rk[k], tcv, racc[1][k]);
+      }
+    }
+    if (live) {
+      double* oc = p.out + cell * (long long)p.nk * p.nq;
+      const int qc = l * l + l + a, qs = l * l + l - a;  // cos side: m = +a (m = 0: column 0); sin side: m = -a
+#pragma unroll
+      for (int k = 0; k < V2_KH; ++k)
+        if (kb + k < ke) {
+          oc[(size_t)(kb + k) * p.nq + qc] = racc[1][k];
+          if (a > 0) oc[(size_t)(kb + k) * p.nq + qs] = racc[0][k];
+        }
+    }
+  }
+}
+
+typedef void (*Ps2Kernel)(const Ps2Params);
+template <int NTILE>
+Ps2Kernel ps2_kernel_kb(int kb) {
+  switch (kb) {
+    case 1: return k_project_v2<NTILE, 1>;
+    case 2: return k_project_v2<NTILE, 2>;
+    case 3: return k_project_v2<NTILE, 3>;
+    case 4: return k_project_v2<NTILE, 4>;
+    default: return nullptr;
+  }
+}
+// KB = ceil(full blocks / K parts); n_p <= 131 gives at most 8 blocks
+Ps2Kernel ps2_kernel(int ntile, int kb) {
+  switch (ntile) {
+    case 1: return ps2_kernel_kb<1>(kb);
+    case 2: return ps2_kernel_kb<2>(kb);
+    case 3: return ps2_kernel_kb<3>(kb);
+    case 4: return ps2_kernel_kb<4>(kb);
+    default: return nullptr;
+  }
+}
+int ps2_kparts(int ntile) { return ntile == 4 ? 2 : 4; }
+int ps2_threads(int ntile) {
+  switch (ntile) {
+    case 1: return V2Shape<1>::THREADS;
+    case 2: return V2Shape<2>::THREADS;
+    case 3: return V2Shape<3>::THREADS;
+    default: return V2Shape<4>::THREADS;
+  }
+}
+int ps2_red_doubles(int ntile) {
+  const int kp = ntile == 4 ? 2 : 4;
+  return 2 * ntile * (kp - 1) * 8 * 32;
+}
+
 typedef void (*PsKernel)(const PsParams);
 template <bool R>
 PsKernel ps_kernel_r(int ntile) {
@@ -386,6 +722,43 @@ int bfq_projector_create(int32_t k_max, int32_t l_max, int32_t n_v, int32_t n_t,
     bfq_projector_destroy(pj);
     return fail(BFQ_ECUDA, "cannot set the projection kernel's shared memory");
   }
+  // v2 (register W tiles, bulk-copied slabs, per-(l,|m|) epilogue): K = n_p in
+  // 16-sample blocks (permuted order) plus a natural-order tail
+  pj->kfull = 4 * (n_p / 16);
+  pj->ks2 = pj->kfull + (n_p % 16 + 3) / 4;
+  pj->slot2 = TC * n_p + 8;  // + the misalignment shift and the K-padding overrun of the last row
+  pj->slot2 += pj->slot2 & 1;
+  const int kp2 = ps2_kparts(pj->ntile), nfull2 = pj->kfull / 4;
+  pj->kb2 = (nfull2 + kp2 - 1) / kp2;
+  const bool v2_fits = pj->ntile <= 4 && npl <= V2_EPI_WARPS * 16 && pj->nk <= V2_NKMAX && pj->kb2 >= 1 &&
+                       pj->kb2 <= 4 && !std::getenv("BFQ_PROJ_V1");
+  if (v2_fits) {
+    auto smem2_for = [&](int nbuf) {
+      return (size_t)128 + (size_t)8 * ((size_t)nbuf * pj->slot2 + (size_t)V2_NGB * (l_max + 1) * V2_GA +
+                                        (size_t)ps2_red_doubles(pj->ntile) + (size_t)npl * V2_TCP);
+    };
+    int nb = V2_MAXBUF;
+    while (nb > 2 && smem2_for(nb) > (size_t)optin) --nb;
+    if (smem2_for(nb) <= (size_t)optin) {
+      std::vector<double> wr((size_t)pj->ntile * pj->ks2 * 32, 0.0);
+      for (int j = 0; j < pj->ntile; ++j)
+        for (int k = 0; k < pj->ks2; ++k)
+          for (int lane = 0; lane < 32; ++lane) {
+            const int kq = lane & 3, col = 8 * j + (lane >> 2);
+            const int pp = k < pj->kfull ? 16 * (k >> 2) + (k & 3) + 4 * kq : 4 * k + kq;
+            if (pp < n_p && col < pj->ncol) wr[((size_t)j * pj->ks2 + k) * 32 + lane] = phi_tab[(size_t)col * n_p + pp];
+          }
+      pj->nbuf2 = nb;
+      pj->smem2 = smem2_for(nb);
+      if (!up(wr, &pj->wreg) ||
+          cudaFuncSetAttribute(ps2_kernel(pj->ntile, pj->kb2), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pj->smem2) !=
+              cudaSuccess) {
+        bfq_projector_destroy(pj);
+        return fail(BFQ_ECUDA, "cannot set up the v2 projection kernel");
+      }
+      pj->v2 = true;
+    }
+  }
   *out = pj;
   return BFQ_OK;
 }
@@ -396,6 +769,7 @@ int bfq_projector_destroy(bfq_projector* pj) {
   cudaFree(pj->wfrag);
   cudaFree(pj->ptab);
   cudaFree(pj->rtab);
+  cudaFree(pj->wreg);
   delete pj;
   return BFQ_OK;
 }
@@ -406,6 +780,32 @@ int bfq_project_samples(const bfq_projector* pj, const double* samples, double* 
   if (n == 0) return BFQ_OK;
   if (n > 0x7fffffffLL) return fail(BFQ_EINVAL, "too many cells for one launch");
   DevGuard guard(pj->device);
+  if (pj->v2) {
+    Ps2Params q;
+    q.f = samples;
+    q.out = out;
+    q.n = n;
+    q.nk = pj->nk;
+    q.L = pj->L;
+    q.nq = pj->nq;
+    q.nv = pj->nv;
+    q.nt = pj->nt;
+    q.np = pj->np;
+    q.ncol = pj->ncol;
+    q.ks = pj->ks2;
+    q.kfull = pj->kfull;
+    q.nchunk = pj->nchunk;
+    q.npl = (pj->L + 1) * (pj->L + 2) / 2;
+    q.nbuf = pj->nbuf2;
+    q.slot = pj->slot2;
+    q.wreg = pj->wreg;
+    q.ptab = pj->ptab;
+    q.rtab = pj->rtab;
+    ps2_kernel(pj->ntile, pj->kb2)<<<(unsigned)n, ps2_threads(pj->ntile), pj->smem2, (cudaStream_t)stream>>>(q);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(BFQ_ECUDA, std::string("projection launch: ") + cudaGetErrorString(e));
+    return BFQ_OK;
+  }
   PsParams p;
   p.f = samples;
   p.out = out;

@@ -82,3 +82,43 @@ def test_validation():
     with pytest.raises(ValueError):
         pj.project(torch.zeros((2, pj.n_points), dtype=torch.float64))
     assert pj.project(torch.zeros((0, pj.n_points), dtype=torch.float64, device="cuda")).shape == (0, 5, 25)
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_v1_kernel_matches_reference_project(case, monkeypatch):
+    """The first-generation kernel (forced with BFQ_PROJ_V1; used for shapes the
+    v2 register tiles do not cover) stays on the reference's outputs, and the
+    two kernels agree to rounding."""
+    k, l, order = case
+    cfg = SpectralConfig(k, l, 1.0)
+    pts = gproject.project_points(cfg, order)
+    names = sorted(FUNCS)
+    samples = torch.from_numpy(np.stack([FUNCS[n](pts) for n in names])).cuda()
+    v2 = gproject.Projector(cfg, order).project(samples).cpu().numpy()
+    monkeypatch.setenv("BFQ_PROJ_V1", "1")
+    v1 = gproject.Projector(cfg, order).project(samples).cpu().numpy()
+    for i, n in enumerate(names):
+        assert rel(v1[i], GOLD[f"{n}_k{k}_l{l}_o{order}"]) <= 1e-13, n
+        assert rel(v2[i], v1[i]) <= 1e-14, n
+
+
+@pytest.mark.parametrize("order,offset", [(13, 1), (13, 0), (80, 1)])
+def test_odd_grids_and_misaligned_samples(order, offset):
+    """n_t n_p odd (order 13 at L=4: 13 x 27 points per slab) makes the slabs
+    alternate between 16-byte aligned and not, with an odd element count and a
+    partial polar chunk; a one-double offset of the whole batch shifts every
+    slab; order 80 (n_p = 161) exceeds the v2 register tiles (v1 path).  All
+    against the CPU restatement of basis.project."""
+    from oracle.project_oracle import ProjectionOracle
+
+    cfg = SpectralConfig(4, 4, 1.0)
+    pts = gproject.project_points(cfg, order)
+    names = sorted(FUNCS)
+    host = np.stack([FUNCS[n](pts) for n in names])
+    buf = torch.empty(host.size + 1, dtype=torch.float64, device="cuda")
+    samples = buf[offset:offset + host.size].view(host.shape)
+    samples.copy_(torch.from_numpy(host))
+    got = gproject.Projector(cfg, order).project(samples).cpu().numpy()
+    orc = ProjectionOracle(cfg.k_max, cfg.l_max, gproject.projection_grid(cfg.l_max, order))
+    for i, n in enumerate(names):
+        assert rel(got[i], orc.project(host[i])) <= 1e-13, (n, order, offset)
