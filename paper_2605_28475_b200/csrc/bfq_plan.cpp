@@ -104,7 +104,11 @@ static bool choose_config(int nk, int qs, int k2s, int nf, int smem_limit, int m
   // Measured at N=L=16 (16,384 cells): 2 cells x 4 units, 1 ring 42.4k cells/s;
   // 1 cell x 4 units, 2 rings 44.1k; 1 cell x 5 units (10 warps), 2 rings 44.9k;
   // 6 units with 1 ring 36.8k (one l1 group per CTA: packing 0.47).
-  static const int popts1[][4] = {{1, 5, 1, 2}, {1, 4, 1, 2}, {1, 6, 1, 1}, {1, 4, 1, 1}};
+  // 6 units (12 warps) with 2 rings fill shared memory to 232,288 of 232,448
+  // bytes at the folded program's 57 channels per group; registers are
+  // allocated per scheduler partition, so 12 warps (3 per partition) have the
+  // same 168-register cap as 10: 46.9k -> 51.1k cells/s (profiles/r02_n16_units.txt).
+  static const int popts1[][4] = {{1, 6, 1, 2}, {1, 5, 1, 2}, {1, 4, 1, 2}, {1, 6, 1, 1}, {1, 4, 1, 1}};
   // (SPLITM is instantiated for the compile-time n_k = 17 kernel only)
   if (kernel == 2 && nk == 17 && !std::getenv("BFQ_GENERIC") && (force_cells == 1 || !force_cells)) {
     for (auto o0 : popts1) {
@@ -263,7 +267,8 @@ static double pack_program(const HostPlan& hp, Program& pg, const std::vector<in
   struct Cta {
     std::vector<std::vector<int>> team_units;  // per team: old unit ids
     std::vector<int> team_l1;
-    double work = 0.0;
+    double work = 0.0;  // slowest unit
+    double lock = 0.0;  // lockstep time of the slowest team (set by the refinement)
   };
   // (a) work order: the next units in descending work whose group fits.
   auto pack_by_work = [&]() {
@@ -354,11 +359,169 @@ static double pack_program(const HostPlan& hp, Program& pg, const std::vector<in
     std::vector<Cta> alt = pack_by_group();
     if (cost(alt) < cost(ctas)) ctas.swap(alt);
   }
+  // (c) refinement: deterministic annealing over unit -> CTA assignments
+  // (moves and swaps, <= c.upc units and <= c.nteams groups per CTA) that
+  // minimises the lockstep schedule cost: a CTA lasts as long as its slowest
+  // team, and a team (one R ring) advances channel by channel at the pace of
+  // its slowest unit in that channel.  Only which CTA runs a unit changes; the
+  // units themselves (columns, summation order) do not, so Q is bitwise the same.
+  // On by default where only two R rings fit (n_k = 17: the greedy packers leave
+  // 10 CTAs per tile at lockstep efficiency 0.79, the refinement 9 at 0.86,
+  // measured 50.8k -> 53.0k cells/s).  With 3-4 teams the model gains 1-4% but
+  // the measured rate does not move (N=L=12 366.9k vs 366.2k, N=L=10 and 8 within
+  // 0.3%: those kernels are FP64-pipe / shared-memory throttled, so an idle unit
+  // slot speeds up its neighbours); BFQ_PACK_REFINE=1 forces it on, =0 off
+  // (profiles/r02_pack_refine_ab.txt).
+  const char* refine_env = std::getenv("BFQ_PACK_REFINE");
+  const bool refine = refine_env ? std::atoi(refine_env) != 0 : c.nteams <= 2;
+  if (refine && units_all.size() > 1) {
+    const int nu = (int)units_all.size();
+    // per-(unit, channel) work, as in unit_work()
+    std::vector<std::vector<double>> wch(nu);
+    for (int k = 0; k < nu; ++k) {
+      const Group& gr = pg.groups[units_all[k].l1];
+      wch[k].resize(gr.n_chan);
+      for (int e = 0; e < gr.n_chan; ++e) {
+        const ChanEntry& ce = pg.chans[gr.chan_off + e];
+        double half[2] = {0.0, 0.0};
+        for (int ml = 0; ml < c.m1t; ++ml) {
+          const int m1 = pg.unit_m1[(size_t)(gr.unit_off + units_all[k].u) * c.m1t + ml];
+          if (m1 < 0) continue;
+          const int rows = hp.sstart[ce.slice_base + m1 + 1] - hp.sstart[ce.slice_base + m1];
+          half[c.cells == 1 ? ml / (c.m1t / 2) : 0] += (double)c.cells * c.mt * c.mt * 256.0 * ((rows + 3) / 4);
+        }
+        wch[k][e] = (c.cells == 1 ? 2.0 * std::max(half[0], half[1]) : half[0]) + stage2;
+      }
+    }
+    std::vector<int> where(nu, -1);  // unit (index into units_all) -> CTA
+    for (size_t ci = 0; ci < ctas.size(); ++ci)
+      for (size_t t = 0; t < ctas[ci].team_l1.size(); ++t)
+        for (int u : ctas[ci].team_units[t])
+          for (int k = 0; k < nu; ++k)
+            if (units_all[k].l1 == ctas[ci].team_l1[t] && units_all[k].u == u) where[k] = (int)ci;
+    const int ncta = (int)ctas.size() + 1;  // one spare CTA so a move can open a new one
+    std::vector<std::vector<int>> mem(ncta);
+    for (int k = 0; k < nu; ++k) mem[where[k]].push_back(k);
+    std::vector<double> scratch;
+    auto cta_cost = [&](const std::vector<int>& m, bool* ok) {
+      // groups present, lockstep time of each
+      int l1s[MAX_TEAMS + 1], ng = 0;
+      *ok = (int)m.size() <= c.upc;
+      for (int k : m) {
+        bool seen = false;
+        for (int j = 0; j < ng; ++j) seen |= l1s[j] == units_all[k].l1;
+        if (!seen) {
+          if (ng == c.nteams) {
+            *ok = false;
+            return 0.0;
+          }
+          l1s[ng++] = units_all[k].l1;
+        }
+      }
+      double worst = 0.0;
+      for (int j = 0; j < ng; ++j) {
+        const int nch = pg.groups[l1s[j]].n_chan;
+        scratch.assign(nch, 0.0);
+        for (int k : m)
+          if (units_all[k].l1 == l1s[j])
+            for (int e = 0; e < nch; ++e) scratch[e] = std::max(scratch[e], wch[k][e]);
+        double tt = 0.0;
+        for (int e = 0; e < nch; ++e) tt += scratch[e];
+        worst = std::max(worst, tt);
+      }
+      return worst;
+    };
+    std::vector<double> cc(ncta, 0.0);
+    double cur = 0.0;
+    for (int i = 0; i < ncta; ++i) {
+      bool ok;
+      cc[i] = cta_cost(mem[i], &ok);
+      cur += cc[i];
+    }
+    double best = cur;
+    const double init_cost = cur;
+    std::vector<int> best_where = where;
+    uint64_t rng = 0x9E3779B97F4A7C15ull;
+    auto rnd = [&]() {
+      rng = rng * 6364136223846793005ull + 1442695040888963407ull;
+      return (uint32_t)(rng >> 33);
+    };
+    const int iters = std::getenv("BFQ_PACK_ITERS") ? std::atoi(std::getenv("BFQ_PACK_ITERS")) : 60000;
+    const double t0 = 0.02 * cur / std::max(1, ncta - 1), t1 = t0 * 1e-3;
+    for (int it = 0; it < iters; ++it) {
+      const double temp = t0 * std::pow(t1 / t0, (double)it / iters);
+      const int a = (int)(rnd() % nu), ca = where[a];
+      // moves: one unit or a whole team (the units of a's group in its CTA) to
+      // another CTA, or exchanged against a unit / team of that CTA
+      const uint32_t kind = rnd() & 3;
+      int b = -1, cb;
+      if (kind & 1) {
+        b = (int)(rnd() % nu);
+        cb = where[b];
+      } else {
+        cb = (int)(rnd() % ncta);
+      }
+      if (cb == ca) continue;
+      const bool team = (kind & 2) != 0;
+      std::vector<int> ma, mb, ga, gb;
+      for (int k : mem[ca])
+        ((team ? units_all[k].l1 == units_all[a].l1 : k == a) ? ga : ma).push_back(k);
+      for (int k : mem[cb])
+        ((b >= 0 && (team ? units_all[k].l1 == units_all[b].l1 : k == b)) ? gb : mb).push_back(k);
+      ma.insert(ma.end(), gb.begin(), gb.end());
+      mb.insert(mb.end(), ga.begin(), ga.end());
+      bool oka, okb;
+      const double na = cta_cost(ma, &oka), nb = cta_cost(mb, &okb);
+      if (!oka || !okb) continue;
+      const double d = na + nb - cc[ca] - cc[cb];
+      if (d <= 0.0 || (double)(rnd() & 0xFFFFFF) / 16777216.0 < std::exp(-d / temp)) {
+        mem[ca].swap(ma);
+        mem[cb].swap(mb);
+        cc[ca] = na;
+        cc[cb] = nb;
+        for (int k : ga) where[k] = cb;
+        for (int k : gb) where[k] = ca;
+        cur += d;
+        if (cur < best * (1.0 - 1e-12)) {
+          best = cur;
+          best_where = where;
+        }
+      }
+    }
+    if (report && std::getenv("BFQ_PLAN_STATS"))
+      std::fprintf(stderr, "plan: refinement lockstep cost %.4g -> %.4g\n", init_cost, best);
+    // rebuild the CTA list from the best assignment (teams in order of first appearance)
+    std::vector<Cta> out(ncta);
+    for (int k = 0; k < nu; ++k) {
+      Cta& cta = out[best_where[k]];
+      int t = -1;
+      for (size_t j = 0; j < cta.team_l1.size(); ++j)
+        if (cta.team_l1[j] == units_all[k].l1) t = (int)j;
+      if (t < 0) {
+        cta.team_l1.push_back(units_all[k].l1);
+        cta.team_units.emplace_back();
+        t = (int)cta.team_l1.size() - 1;
+      }
+      cta.team_units[t].push_back(units_all[k].u);
+      cta.work = std::max(cta.work, units_all[k].work);
+    }
+    for (int i = 0; i < ncta; ++i) {
+      std::vector<int> m;
+      for (int k = 0; k < nu; ++k)
+        if (best_where[k] == i) m.push_back(k);
+      bool ok;
+      out[i].lock = cta_cost(m, &ok);
+    }
+    out.erase(std::remove_if(out.begin(), out.end(), [](const Cta& x) { return x.team_l1.empty(); }), out.end());
+    ctas.swap(out);
+  }
   // renumber units inside each group in order of appearance
   std::vector<int16_t> new_m1 = pg.unit_m1;
   std::vector<int> next_id(pg.groups.size(), 0);
   pg.items.clear();
-  std::stable_sort(ctas.begin(), ctas.end(), [](const Cta& x, const Cta& y) { return x.work > y.work; });
+  std::stable_sort(ctas.begin(), ctas.end(), [](const Cta& x, const Cta& y) {
+    return (x.lock > 0.0 ? x.lock : x.work) > (y.lock > 0.0 ? y.lock : y.work);
+  });
   for (const Cta& cta : ctas) {
     Item it{};
     for (size_t t = 0; t < cta.team_l1.size(); ++t) {
