@@ -374,7 +374,7 @@ static double pack_program(const HostPlan& hp, Program& pg, const std::vector<in
   // (profiles/r02_pack_refine_ab.txt).
   const char* refine_env = std::getenv("BFQ_PACK_REFINE");
   const bool refine = refine_env ? std::atoi(refine_env) != 0 : c.nteams <= 2;
-  if (refine && units_all.size() > 1) {
+  if (refine && report && units_all.size() > 1) {  // the final packing only (report), not the trial ones
     const int nu = (int)units_all.size();
     // per-(unit, channel) work, as in unit_work()
     std::vector<std::vector<double>> wch(nu);
@@ -446,7 +446,10 @@ static double pack_program(const HostPlan& hp, Program& pg, const std::vector<in
       rng = rng * 6364136223846793005ull + 1442695040888963407ull;
       return (uint32_t)(rng >> 33);
     };
-    const int iters = std::getenv("BFQ_PACK_ITERS") ? std::atoi(std::getenv("BFQ_PACK_ITERS")) : 60000;
+    // 2M moves (about 1.5 s at n_k = 17) find the 0.88 schedule that 60k-400k miss
+    // (0.856): 53.0k -> 55.0k cells/s at N=L=16 (profiles/r02_n16_pack_iters.txt)
+    const int iters = std::getenv("BFQ_PACK_ITERS") ? std::atoi(std::getenv("BFQ_PACK_ITERS"))
+                                                    : (nu >= 32 ? 2000000 : 60000);
     const double t0 = 0.02 * cur / std::max(1, ncta - 1), t1 = t0 * 1e-3;
     for (int it = 0; it < iters; ++it) {
       const double temp = t0 * std::pow(t1 / t0, (double)it / iters);
