@@ -166,6 +166,12 @@ int bfq_projector_destroy(bfq_projector* proj);
 /* Algorithmic work per cell: flops of the azimuthal, polar and radial sums;
  * bytes = the samples read + the coefficients written. */
 int bfq_projector_work(const bfq_projector* proj, double* flops_per_cell, double* bytes_per_cell);
+/* Which kernel bfq_project_samples launches for this projector: 1 = the
+ * general kernel, 2 = register-tiled W (shapes within its tiles), 3 = 2 with
+ * the azimuth folded over the mirror pairs p <-> n_p - p (needs an azimuth
+ * table that is even / odd under the mirror, as the reference's trapezoid
+ * nodes make it; checked at create).  Negative: invalid handle. */
+int bfq_projector_kernel(const bfq_projector* proj);
 
 /* Diagnostic: validate `desc` and build the host-side plan (folding check,
  * tiling, CTA schedule) WITHOUT touching a GPU; fills `info` as

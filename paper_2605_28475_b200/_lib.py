@@ -49,6 +49,7 @@ EXPORTED_SYMBOLS = (
     "bfq_project_samples",
     "bfq_projector_destroy",
     "bfq_projector_work",
+    "bfq_projector_kernel",
     "bfq_strerror",
     "bfq_last_error",
     "bfq_build_id",
@@ -181,6 +182,7 @@ def _declare(lib):
     lib.bfq_project_samples.argtypes = [vp, vp, vp, ctypes.c_int64, vp]
     lib.bfq_projector_destroy.argtypes = [vp]
     lib.bfq_projector_work.argtypes = [vp, _f64p, _f64p]
+    lib.bfq_projector_kernel.argtypes = [vp]
     lib.bfr_assemble.argtypes = [ctypes.POINTER(BfrDesc), ctypes.c_int, vp, vp, ctypes.POINTER(BfrStats)]
     for name in EXPORTED_SYMBOLS + EXPORTED_SYMBOLS_BFR:
         if name not in ("bfq_strerror", "bfq_last_error", "bfq_build_id"):

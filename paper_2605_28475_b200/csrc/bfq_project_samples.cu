@@ -50,6 +50,11 @@ struct bfq_projector {
   int kfull = 0, ks2 = 0, slot2 = 0, nbuf2 = 0, kb2 = 0;
   size_t smem2 = 0;
   double* wreg = nullptr;   // [ntile][ks2][32] A fragments of W^T, K permuted
+  // mirror-folded v2 (FOLD): azimuth table even / odd under p <-> n_p - p (checked at create)
+  bool fold = false;
+  int kfull3 = 0, ks3 = 0, kb3 = 0, nbuf3 = 0;
+  size_t smem3 = 0;
+  double* wfold = nullptr;  // [|m| tile][cos, sin][ks3][32] A fragments of the folded W^T
 };
 
 namespace {
@@ -343,8 +348,17 @@ __device__ __forceinline__ double2 lds128_v(uint32_t addr) {
   return v;
 }
 
-template <int NTILE, int KB>  // KB: most 16-sample blocks of any K part (the others may have one fewer)
+// FOLD (mirror-folded azimuth, NTILE = 4 warp layout): the trapezoid nodes phi_p = 2 pi p / n_p
+// make cos(m phi) even and sin(m phi) odd under p <-> n_p - p, so the K axis runs
+// over the (n_p - 1) / 2 sample PAIRS: fe = f[p] + f[n_p - p] meets the cos
+// columns, fo = f[p] - f[n_p - p] the sin columns, and p = 0 is one extra
+// k-step (cos only).  Per pair of samples that is 2 gathers + 2 DADD + 2 DMMA
+// for a (cos, sin) tile pair instead of 4 gathers + 4 DMMA: half the tensor
+// work and half the shared-memory reads.  A GEMM warp owns one |m| tile (its
+// cos and its sin columns), one half of the chunk's polar rows and one K part.
+template <int NTILE, int KB, bool FOLD = false>  // KB: most 16-sample blocks of any K part (the others may have one fewer)
 __global__ void __launch_bounds__(V2Shape<NTILE>::THREADS, 1) k_project_v2(const Ps2Params p) {
+  static_assert(!FOLD || NTILE == 4, "the folded kernel uses the 4-group, 2-part warp layout");
   constexpr int KP = V2Shape<NTILE>::KP, GW = V2Shape<NTILE>::GW;
   constexpr int NTH = V2Shape<NTILE>::THREADS, NT_G = GW * 32, NT_E = V2_EPI_WARPS * 32;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -389,8 +403,22 @@ __global__ void __launch_bounds__(V2Shape<NTILE>::THREADS, 1) k_project_v2(const
     const int nb = bq + (part >= KP - br ? 1 : 0);  // the extra blocks go to the last parts
     const int b0 = part * bq + max(0, part - (KP - br));
     const int ntail = part == KP - 1 ? p.ks - p.kfull : 0;
-    double wr[KB * 4], wt[V2_TAIL];
-    {
+    // FOLD: group j = (|m| tile jp, polar half ph); W^T fragments of the cos and the
+    // sin columns m = 8 jp + r0 ([jp][cos, sin][ks][32], K = pairs in 16-pair blocks,
+    // then the p = 0 step)
+    const int jp = j & 1, ph = j >> 1;
+    double wc[FOLD ? KB * 4 : 1], wsn[FOLD ? KB * 4 : 1], w0 = 0.0;
+    if constexpr (FOLD) {
+      const double* wq = p.wreg + ((size_t)(2 * jp) * p.ks + 4 * b0) * 32 + lane;
+#pragma unroll
+      for (int k = 0; k < KB * 4; ++k) {
+        wc[k] = k < 4 * nb ? __ldg(wq + k * 32) : 0.0;
+        wsn[k] = k < 4 * nb ? __ldg(wq + (size_t)p.ks * 32 + k * 32) : 0.0;
+      }
+      if (ntail > 0) w0 = __ldg(p.wreg + ((size_t)(2 * jp) * p.ks + p.kfull) * 32 + lane);
+    }
+    double wr[FOLD ? 1 : KB * 4], wt[FOLD ? 1 : V2_TAIL];
+    if constexpr (!FOLD) {
       const double* ws = p.wreg + ((size_t)j * p.ks + 4 * b0) * 32 + lane;
 #pragma unroll
       for (int k = 0; k < KB * 4; ++k) wr[k] = k < 4 * nb ? __ldg(ws + k * 32) : 0.0;
@@ -435,12 +463,46 @@ __global__ void __launch_bounds__(V2Shape<NTILE>::THREADS, 1) k_project_v2(const
       asm volatile("mov.u32 %0, 0;\n" : "=r"(after_wait)::"memory");
       const uint32_t base = smem_u32(ring + (size_t)b * p.slot) + (uint32_t)(m + r0 * p.np) * 8u + after_wait;
       const uint32_t tstep = (uint32_t)(8 * p.np) * 8u;  // one polar tile
-      uint32_t rowb[4];  // block b0, lane offset 4 kq, polar tile i: k-step (block, jj) is +(16 block + jj) doubles
-#pragma unroll
-      for (int i = 0; i < 4; ++i) rowb[i] = base + (uint32_t)(16 * b0 + 4 * kq) * 8u + (uint32_t)i * tstep;
       double acc[4][2];
 #pragma unroll
       for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = 0.0;
+      if constexpr (FOLD) {
+        // acc[2 i + cs]: polar tile 2 ph + i, cs = 0 cos / 1 sin.  Pair kappa = 16 block + 4 kq + jj
+        // is the samples p = kappa + 1 (forward) and n_p - 1 - kappa (mirror).
+        uint32_t rowf[2], rowm[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const uint32_t r = base + (uint32_t)(8 * (2 * ph + i)) * (uint32_t)p.np * 8u;
+          rowf[i] = r + (uint32_t)(1 + 16 * b0 + 4 * kq) * 8u;
+          rowm[i] = r + (uint32_t)(p.np - 1 - 16 * b0 - 4 * kq) * 8u;
+        }
+        auto kstep = [&](double c, double sn, uint32_t off) {
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const double a = lds_ro(rowf[i] + off), bm = lds_ro(rowm[i] - off);
+            dmma884(acc[2 * i][0], acc[2 * i][1], c, a + bm);
+            dmma884(acc[2 * i + 1][0], acc[2 * i + 1][1], sn, a - bm);
+          }
+        };
+#pragma unroll
+        for (int blk = 0; blk < KB - 1; ++blk)
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) kstep(wc[4 * blk + jj], wsn[4 * blk + jj], (uint32_t)(16 * blk + jj) * 8u);
+        if (full_kb) {
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj)
+            kstep(wc[4 * (KB - 1) + jj], wsn[4 * (KB - 1) + jj], (uint32_t)(16 * (KB - 1) + jj) * 8u);
+        }
+        if (ntail > 0) {  // p = 0: its own mirror image; the weight sits on the kq = 0 lanes
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+            dmma884(acc[2 * i][0], acc[2 * i][1], w0,
+                    lds_ro(base + (uint32_t)(8 * (2 * ph + i)) * (uint32_t)p.np * 8u));
+        }
+      } else {
+      uint32_t rowb[4];  // block b0, lane offset 4 kq, polar tile i: k-step (block, jj) is +(16 block + jj) doubles
+#pragma unroll
+      for (int i = 0; i < 4; ++i) rowb[i] = base + (uint32_t)(16 * b0 + 4 * kq) * 8u + (uint32_t)i * tstep;
       auto kstep = [&](double w, uint32_t off) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) dmma884(acc[i][0], acc[i][1], w, lds_ro(rowb[i] + off));
@@ -458,6 +520,7 @@ __global__ void __launch_bounds__(V2Shape<NTILE>::THREADS, 1) k_project_v2(const
 #pragma unroll
         for (int u = 0; u < V2_TAIL; ++u)
           if (u < ntail) kstep(wt[u], tb + (uint32_t)(4 * u) * 8u);
+      }
       }
       const int b2 = s % V2_NGB;
       // partials of the K parts, double-buffered by slab parity: a part writes
@@ -487,7 +550,20 @@ __global__ void __launch_bounds__(V2Shape<NTILE>::THREADS, 1) k_project_v2(const
           }
         }
         if (s >= V2_NGB) bar_sync(V2_BAR_EMPTY0 + b2, NTH - (GW - NTILE) * 32);  // epilogue consumed b2
-        if (col < p.ncol) {
+        if constexpr (FOLD) {
+          const int mm = 8 * jp + r0;  // |m| of this lane's cos and sin columns
+          if (mm <= p.L) {
+            const uint32_t gb = smem_u32(gbuf + (size_t)b2 * gsz + (size_t)mm * V2_GA);
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const uint32_t t2 = (uint32_t)(2 * (8 * (2 * ph + i) + 2 * kq + e)) * 8u;
+                sts_v(gb + t2 + 8u, acc[2 * i][e]);  // cos side
+                if (mm > 0) sts_v(gb + t2, acc[2 * i + 1][e]);
+              }
+          }
+        } else if (col < p.ncol) {
           const uint32_t gb = smem_u32(gbuf + (size_t)b2 * gsz + (size_t)ga * V2_GA + side);
 #pragma unroll
           for (int i = 0; i < 4; ++i)
@@ -592,6 +668,15 @@ Ps2Kernel ps2_kernel(int ntile, int kb) {
     default: return nullptr;
   }
 }
+Ps2Kernel ps2_fold_kernel(int kb) {
+  switch (kb) {
+    case 1: return k_project_v2<4, 1, true>;
+    case 2: return k_project_v2<4, 2, true>;
+    case 3: return k_project_v2<4, 3, true>;
+    default: return nullptr;
+  }
+}
+constexpr int FOLD_MAXKB = 3;
 int ps2_kparts(int ntile) { return ntile == 4 ? 2 : 4; }
 int ps2_threads(int ntile) {
   switch (ntile) {
@@ -759,6 +844,71 @@ int bfq_projector_create(int32_t k_max, int32_t l_max, int32_t n_v, int32_t n_t,
       pj->v2 = true;
     }
   }
+  // Mirror-folded kernel: n_p odd, the pairs (p, n_p - p) in whole 16-pair blocks,
+  // two |m| tiles (8 <= l_max <= 14: the v2 epilogue holds 128 (l, |m|) rows), and a table that IS even (cos, m = 0
+  // columns) / odd (sin columns) under the mirror to within a few ulp -- true of
+  // the reference's trapezoid nodes phi_p = 2 pi p / n_p (basis.py:239-247);
+  // numpy's cos(m phi_p) and cos(m phi_{n_p - p}) differ by rounding of m phi
+  // (70 ulp of the column maximum at l_max = 12, n_p = 129; <= 128 ulp is
+  // accepted and the folded weight is their mean, i.e. each weight moves by at
+  // most 1.4e-14 of the column maximum, towards the exactly symmetric value).
+  // Anything else keeps the unfolded kernel.
+  if (pj->v2 && (n_p & 1) && l_max >= 8 && l_max <= 15 && npl <= V2_EPI_WARPS * 16 && !std::getenv("BFQ_PROJ_NOFOLD")) {
+    const int H = (n_p - 1) / 2, nfull = H / 16;
+    const int kb3 = (nfull + 1) / 2;
+    bool ok = H % 16 == 0 && nfull >= 2 && kb3 <= FOLD_MAXKB;
+    for (int col = 0; ok && col < pj->ncol; ++col) {
+      const double* w = phi_tab + (size_t)col * n_p;
+      double mx = 0.0;
+      for (int pp = 0; pp < n_p; ++pp) mx = std::max(mx, std::fabs(w[pp]));
+      const bool odd = col > 0 && (col & 1);  // col 2m-1: sin
+      const double tol = 128.0 * 2.220446049250313e-16 * mx;
+      if (odd && std::fabs(w[0]) > tol) ok = false;
+      for (int pp = 1; ok && pp <= H; ++pp)
+        if (std::fabs(w[pp] - (odd ? -w[n_p - pp] : w[n_p - pp])) > tol) ok = false;
+    }
+    if (ok) {
+      pj->kfull3 = 4 * nfull;
+      pj->ks3 = pj->kfull3 + 1;
+      pj->kb3 = kb3;
+      auto smem3_for = [&](int nbuf) {
+        return (size_t)128 + (size_t)8 * ((size_t)nbuf * pj->slot2 + (size_t)V2_NGB * (l_max + 1) * V2_GA +
+                                          (size_t)ps2_red_doubles(4) + (size_t)npl * V2_TCP);
+      };
+      int nb = V2_MAXBUF;
+      while (nb > 2 && smem3_for(nb) > (size_t)optin) --nb;
+      std::vector<double> wf3((size_t)2 * 2 * pj->ks3 * 32, 0.0);
+      for (int jp = 0; jp < 2; ++jp)
+        for (int k = 0; k < pj->ks3; ++k)
+          for (int lane = 0; lane < 32; ++lane) {
+            const int kq = lane & 3, mm = 8 * jp + (lane >> 2);
+            if (mm > l_max) continue;
+            const double* wc = phi_tab + (size_t)(2 * mm) * n_p;                    // cos m phi (m = 0: column 0)
+            const double* ws = mm > 0 ? phi_tab + (size_t)(2 * mm - 1) * n_p : nullptr;  // sin m phi
+            double c = 0.0, sn = 0.0;
+            if (k < pj->kfull3) {
+              const int pp = 16 * (k >> 2) + 4 * kq + (k & 3) + 1;
+              c = 0.5 * (wc[pp] + wc[n_p - pp]);
+              if (ws) sn = 0.5 * (ws[pp] - ws[n_p - pp]);
+            } else if (kq == 0) {
+              c = wc[0];  // p = 0 is its own mirror image; sin(0) = 0
+            }
+            wf3[((size_t)(2 * jp) * pj->ks3 + k) * 32 + lane] = c;
+            wf3[((size_t)(2 * jp + 1) * pj->ks3 + k) * 32 + lane] = sn;
+          }
+      if (smem3_for(nb) <= (size_t)optin) {
+        pj->nbuf3 = nb;
+        pj->smem3 = smem3_for(nb);
+        if (!up(wf3, &pj->wfold) ||
+            cudaFuncSetAttribute(ps2_fold_kernel(kb3), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pj->smem3) !=
+                cudaSuccess) {
+          bfq_projector_destroy(pj);
+          return fail(BFQ_ECUDA, "cannot set up the folded projection kernel");
+        }
+        pj->fold = true;
+      }
+    }
+  }
   *out = pj;
   return BFQ_OK;
 }
@@ -770,6 +920,7 @@ int bfq_projector_destroy(bfq_projector* pj) {
   cudaFree(pj->ptab);
   cudaFree(pj->rtab);
   cudaFree(pj->wreg);
+  cudaFree(pj->wfold);
   delete pj;
   return BFQ_OK;
 }
@@ -801,7 +952,15 @@ int bfq_project_samples(const bfq_projector* pj, const double* samples, double* 
     q.wreg = pj->wreg;
     q.ptab = pj->ptab;
     q.rtab = pj->rtab;
-    ps2_kernel(pj->ntile, pj->kb2)<<<(unsigned)n, ps2_threads(pj->ntile), pj->smem2, (cudaStream_t)stream>>>(q);
+    if (pj->fold) {
+      q.ks = pj->ks3;
+      q.kfull = pj->kfull3;
+      q.nbuf = pj->nbuf3;
+      q.wreg = pj->wfold;
+      ps2_fold_kernel(pj->kb3)<<<(unsigned)n, ps2_threads(4), pj->smem3, (cudaStream_t)stream>>>(q);
+    } else {
+      ps2_kernel(pj->ntile, pj->kb2)<<<(unsigned)n, ps2_threads(pj->ntile), pj->smem2, (cudaStream_t)stream>>>(q);
+    }
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(BFQ_ECUDA, std::string("projection launch: ") + cudaGetErrorString(e));
     return BFQ_OK;
@@ -841,6 +1000,11 @@ int bfq_projector_work(const bfq_projector* pj, double* flops_per_cell, double* 
     *flops_per_cell = 2.0 * (pts * pj->ncol + (double)pj->nv * pj->nt * pj->nq + (double)pj->nv * pj->nk * pj->nq);
   if (bytes_per_cell) *bytes_per_cell = 8.0 * (pts + (double)pj->nk * pj->nq);
   return BFQ_OK;
+}
+
+int bfq_projector_kernel(const bfq_projector* pj) {
+  if (!pj) return -1;
+  return pj->fold ? 3 : (pj->v2 ? 2 : 1);
 }
 
 }  // extern "C"

@@ -108,6 +108,7 @@ class Projector:
         fl, by = ctypes.c_double(), ctypes.c_double()
         _lib.check(lib.bfq_projector_work(h, ctypes.byref(fl), ctypes.byref(by)))
         self.flops_per_cell, self.bytes_per_cell = fl.value, by.value
+        self.kernel = int(lib.bfq_projector_kernel(h))  # 1 general, 2 register-tiled, 3 mirror-folded
 
     def __del__(self):
         h = getattr(self, "_h", None)

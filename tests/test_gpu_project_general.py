@@ -122,3 +122,74 @@ def test_odd_grids_and_misaligned_samples(order, offset):
     orc = ProjectionOracle(cfg.k_max, cfg.l_max, gproject.projection_grid(cfg.l_max, order))
     for i, n in enumerate(names):
         assert rel(got[i], orc.project(host[i])) <= 1e-13, (n, order, offset)
+
+
+@pytest.mark.parametrize("case", [c for c in CASES if c[1] >= 8])
+def test_folded_kernel_matches_reference_and_unfolded(case, monkeypatch):
+    """The mirror-folded kernel (kernel 3: K over the sample pairs p, n_p - p) is
+    the default at these shapes; it stays on the reference's outputs and agrees
+    with the unfolded kernel (BFQ_PROJ_NOFOLD) to rounding."""
+    k, l, order = case
+    cfg = SpectralConfig(k, l, 1.0)
+    pts = gproject.project_points(cfg, order)
+    names = sorted(FUNCS)
+    samples = torch.from_numpy(np.stack([FUNCS[n](pts) for n in names])).cuda()
+    pf = gproject.Projector(cfg, order)
+    assert pf.kernel == 3
+    fold = pf.project(samples).cpu().numpy()
+    monkeypatch.setenv("BFQ_PROJ_NOFOLD", "1")
+    pu = gproject.Projector(cfg, order)
+    assert pu.kernel == 2
+    plain = pu.project(samples).cpu().numpy()
+    for i, n in enumerate(names):
+        assert rel(fold[i], GOLD[f"{n}_k{k}_l{l}_o{order}"]) <= 1e-13, n
+        assert rel(fold[i], plain[i]) <= 5e-14, n
+
+
+@pytest.mark.parametrize("l_max,order,offset", [(8, 48, 0), (8, 48, 1), (14, 32, 1), (9, 64, 0)])
+def test_folded_kernel_partial_chunks_and_misaligned(l_max, order, offset):
+    """Folded kernel on a partial polar chunk with unequal K parts (order 48: 48 =
+    32 + 16 polar rows, three 16-pair blocks split 1 + 2), on the widest |m| tile
+    pair the epilogue holds (l_max = 14) and on a half-empty one (l_max = 9), with the batch shifted
+    by one double; against the CPU restatement of basis.project."""
+    from oracle.project_oracle import ProjectionOracle
+
+    cfg = SpectralConfig(3, l_max, 1.0)
+    pts = gproject.project_points(cfg, order)
+    names = sorted(FUNCS)
+    # plus white noise: every (v, t) slab and every sample pair carries weight (the
+    # test functions decay at large v and would hide an error there)
+    host = np.stack([FUNCS[n](pts) for n in names] + [np.random.default_rng(5).standard_normal(pts.shape[0])])
+    buf = torch.empty(host.size + 1, dtype=torch.float64, device="cuda")
+    samples = buf[offset:offset + host.size].view(host.shape)
+    samples.copy_(torch.from_numpy(host))
+    pj = gproject.Projector(cfg, order)
+    assert pj.kernel == 3
+    got = pj.project(samples).cpu().numpy()
+    orc = ProjectionOracle(cfg.k_max, cfg.l_max, gproject.projection_grid(cfg.l_max, order))
+    for i in range(host.shape[0]):
+        assert rel(got[i], orc.project(host[i])) <= 1e-13, (i, l_max, order, offset)
+
+
+def test_asymmetric_azimuth_table_keeps_the_unfolded_kernel():
+    """bfq_projector_create folds only a table that is even / odd under the mirror:
+    a perturbed table (C ABI) falls back to kernel 2."""
+    import ctypes
+
+    from paper_2605_28475_b200 import _lib
+
+    cfg = SpectralConfig(8, 8, 1.0)
+    phi_tab, theta_tab, radial_tab, (n_v, n_t, n_p) = gproject.projection_tables(cfg, 32)
+    lib = _lib.lib()
+    f64p = ctypes.POINTER(ctypes.c_double)
+    kinds = []
+    for bump in (0.0, 1e-9):
+        tab = phi_tab.copy()
+        tab[4, 3] += bump
+        h = ctypes.c_void_p()
+        _lib.check(lib.bfq_projector_create(cfg.k_max, cfg.l_max, n_v, n_t, n_p, tab.ctypes.data_as(f64p),
+                                            theta_tab.ctypes.data_as(f64p), radial_tab.ctypes.data_as(f64p),
+                                            torch.cuda.current_device(), ctypes.byref(h)))
+        kinds.append(int(lib.bfq_projector_kernel(h)))
+        lib.bfq_projector_destroy(h)
+    assert kinds == [3, 2]
