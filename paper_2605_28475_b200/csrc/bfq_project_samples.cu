@@ -44,6 +44,7 @@ struct bfq_projector {
   size_t smem = 0;
   double* wfrag = nullptr;  // [ks][ntile][32] B fragments of W (zero padded)
   double* ptab = nullptr;   // [nchunk][(L+1)(L+2)/2][TC] polar table, t-chunked, zero padded
+  double* ptab2 = nullptr;  // the same with |m|-major rows (v2 kernels)
   double* rtab = nullptr;   // [nv][L+1][nk] radial table
   // v2 kernel (k_project_v2): used when the shape fits its register tiles
   bool v2 = false;
@@ -309,8 +310,10 @@ __global__ void __launch_bounds__(PS_THREADS, 1) k_project_samples(const PsParam
 //   FP64 pipe with the DMMA stream, so it runs on 8 warps with 4 G buffers of
 //   slack behind the GEMM.
 constexpr int V2_EPI_WARPS = 8;
-constexpr int V2_GA = 2 * TC + 4;  // doubles per |m| block of a G buffer ([t][sin, cos]); = 4 (mod 16):
-                                   // the epilogue's 16-byte loads of a quarter-warp hit distinct banks
+constexpr int V2_GA = 2 * TC + 6;  // doubles per |m| block of a G buffer ([t][sin, cos]); = 6 (mod 16): the GEMM
+                                   // warps' stores (lanes = 8 |m| x 4 t) spread over all banks (16-byte (sin, cos)
+                                   // stores of the folded kernel: 4 wavefronts for 512 bytes), and the two or three
+                                   // |m| blocks an epilogue warp reads (rows are |m|-major) do not collide
 constexpr int V2_TCP = TC + 2;     // row stride of the polar chunk: = 2 (mod 16), the lane pairs
                                    // (row r, half h) of a half-warp read r V2_TCP + h: distinct banks
 constexpr int V2_NKMAX = 17;       // n_k <= 17: radial accumulators (half of them per lane) in registers
@@ -326,7 +329,7 @@ struct Ps2Params {
   long long n;
   int nk, L, nq, nv, nt, np, ncol, ks, kfull, nchunk, npl, nbuf, slot;
   const double* wreg;  // [ntile][ks][32] A fragments of W^T, K permuted as above
-  const double* ptab;  // [nchunk][npl][TC]
+  const double* ptab;  // [nchunk][npl][TC], rows |m|-major: row(l, a) = a (L + 1) - a (a - 1) / 2 + l - a
   const double* rtab;  // [nv][L+1][nk]
 };
 
@@ -342,6 +345,9 @@ struct V2Shape {
 };
 constexpr int V2_TAIL = 4;  // tail k-steps: ceil(15 / 4)
 
+__device__ __forceinline__ void sts128_v(uint32_t addr, double x, double y) {
+  asm volatile("st.shared.v2.f64 [%0], {%1, %2};\n" ::"r"(addr), "d"(x), "d"(y) : "memory");
+}
 __device__ __forceinline__ double2 lds128_v(uint32_t addr) {
   double2 v;
   asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(addr) : "memory");
@@ -559,8 +565,7 @@ __global__ void __launch_bounds__(V2Shape<NTILE>::THREADS, 1) k_project_v2(const
 #pragma unroll
               for (int e = 0; e < 2; ++e) {
                 const uint32_t t2 = (uint32_t)(2 * (8 * (2 * ph + i) + 2 * kq + e)) * 8u;
-                sts_v(gb + t2 + 8u, acc[2 * i][e]);  // cos side
-                if (mm > 0) sts_v(gb + t2, acc[2 * i + 1][e]);
+                sts128_v(gb + t2, acc[2 * i + 1][e], acc[2 * i][e]);  // (sin, cos); m = 0: sin weights are 0
               }
           }
         } else if (col < p.ncol) {
@@ -579,11 +584,14 @@ __global__ void __launch_bounds__(V2Shape<NTILE>::THREADS, 1) k_project_v2(const
     }
   } else {
     // ------------------------------------------------ consumer: G -> coefficients
-    const int et = tid - NT_G, r = et >> 1, hf = et & 1;  // (l, |m|) row of this lane pair, half
-    int l = (int)((sqrtf(8.0f * (float)r + 1.0f) - 1.0f) * 0.5f);
-    while (l * (l + 1) / 2 > r) --l;
-    while ((l + 1) * (l + 2) / 2 <= r) ++l;
-    const int a = r - l * (l + 1) / 2;
+    // (l, |m|) row of this lane pair, half.  Rows are |m|-major (all l of one |m|
+    // consecutive): the 16 rows of a warp span two or three |m|, so their 16-byte
+    // G loads are broadcasts of 2-3 distinct addresses per t (one wavefront
+    // instead of four with l-major rows)
+    const int et = tid - NT_G, r = et >> 1, hf = et & 1;
+    int a = 0;
+    while (a < p.L && (a + 1) * (p.L + 1) - (a + 1) * a / 2 <= r) ++a;
+    const int l = a + (r - (a * (p.L + 1) - a * (a - 1) / 2));
     const bool live = r < p.npl;
     const int kh = (p.nk + 1) / 2, kb = hf ? kh : 0, ke = hf ? p.nk : kh;  // this lane's radial indices
     double racc[2][V2_KH];
@@ -825,6 +833,14 @@ int bfq_projector_create(int32_t k_max, int32_t l_max, int32_t n_v, int32_t n_t,
     int nb = V2_MAXBUF;
     while (nb > 2 && smem2_for(nb) > (size_t)optin) --nb;
     if (smem2_for(nb) <= (size_t)optin) {
+      // polar table with |m|-major rows: row(l, a) = a (L + 1) - a (a - 1) / 2 + l - a
+      std::vector<double> pt2((size_t)pj->nchunk * npl * TC, 0.0);
+      for (int l = 0; l <= l_max; ++l)
+        for (int am = 0; am <= l; ++am) {
+          const int row = l * (l + 1) / 2 + am, row2 = am * (l_max + 1) - am * (am - 1) / 2 + l - am;
+          for (int t = 0; t < n_t; ++t)
+            pt2[((size_t)(t / TC) * npl + row2) * TC + t % TC] = theta_tab[(size_t)row * n_t + t];
+        }
       std::vector<double> wr((size_t)pj->ntile * pj->ks2 * 32, 0.0);
       for (int j = 0; j < pj->ntile; ++j)
         for (int k = 0; k < pj->ks2; ++k)
@@ -835,7 +851,7 @@ int bfq_projector_create(int32_t k_max, int32_t l_max, int32_t n_v, int32_t n_t,
           }
       pj->nbuf2 = nb;
       pj->smem2 = smem2_for(nb);
-      if (!up(wr, &pj->wreg) ||
+      if (!up(wr, &pj->wreg) || !up(pt2, &pj->ptab2) ||
           cudaFuncSetAttribute(ps2_kernel(pj->ntile, pj->kb2), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pj->smem2) !=
               cudaSuccess) {
         bfq_projector_destroy(pj);
@@ -920,6 +936,7 @@ int bfq_projector_destroy(bfq_projector* pj) {
   cudaFree(pj->ptab);
   cudaFree(pj->rtab);
   cudaFree(pj->wreg);
+  cudaFree(pj->ptab2);
   cudaFree(pj->wfold);
   delete pj;
   return BFQ_OK;
@@ -950,7 +967,7 @@ int bfq_project_samples(const bfq_projector* pj, const double* samples, double* 
     q.nbuf = pj->nbuf2;
     q.slot = pj->slot2;
     q.wreg = pj->wreg;
-    q.ptab = pj->ptab;
+    q.ptab = pj->ptab2;
     q.rtab = pj->rtab;
     if (pj->fold) {
       q.ks = pj->ks3;
