@@ -52,7 +52,7 @@ struct bfq_projector {
   size_t smem2 = 0;
   double* wreg = nullptr;   // [ntile][ks2][32] A fragments of W^T, K permuted
   // mirror-folded v2 (FOLD): azimuth table even / odd under p <-> n_p - p (checked at create)
-  bool fold = false;
+  bool fold = false, fold_whole = false;
   int kfull3 = 0, ks3 = 0, kb3 = 0, nbuf3 = 0;
   size_t smem3 = 0;
   double* wfold = nullptr;  // [|m| tile][cos, sin][ks3][32] A fragments of the folded W^T
@@ -362,10 +362,18 @@ __device__ __forceinline__ double2 lds128_v(uint32_t addr) {
 // for a (cos, sin) tile pair instead of 4 gathers + 4 DMMA: half the tensor
 // work and half the shared-memory reads.  A GEMM warp owns one |m| tile (its
 // cos and its sin columns), one half of the chunk's polar rows and one K part.
-template <int NTILE, int KB, bool FOLD = false>  // KB: most 16-sample blocks of any K part (the others may have one fewer)
+// FOLD = 1: two K parts per (|m| tile, polar half) group, reduced through shared
+// memory (any pair count in whole blocks).  FOLD = 2: no K split -- a warp owns
+// one |m| tile, ONE polar tile and the whole K axis (<= 4 blocks: the cos and
+// sin fragments fill 66 registers), two accumulator chains per warp, which is
+// what two warps per scheduler need to keep the pipe fed; no partials, no
+// reduction barrier, every GEMM warp stores its own G tile.
+template <int NTILE, int KB, int FOLD = 0>  // KB: most 16-sample blocks of any K part (the others may have one fewer)
 __global__ void __launch_bounds__(V2Shape<NTILE>::THREADS, 1) k_project_v2(const Ps2Params p) {
-  static_assert(!FOLD || NTILE == 4, "the folded kernel uses the 4-group, 2-part warp layout");
-  constexpr int KP = V2Shape<NTILE>::KP, GW = V2Shape<NTILE>::GW;
+  static_assert(!FOLD || NTILE == 4, "the folded kernels use the 8-GEMM-warp layout");
+  constexpr int KP = FOLD == 2 ? 1 : V2Shape<NTILE>::KP, GW = V2Shape<NTILE>::GW;
+  constexpr int NGRP = GW / KP;  // groups = storing (part 0) warps
+  constexpr int NPT = FOLD == 2 ? 1 : 2;  // FOLD: polar tiles per warp
   constexpr int NTH = V2Shape<NTILE>::THREADS, NT_G = GW * 32, NT_E = V2_EPI_WARPS * 32;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);  // [V2_MAXBUF] slab landed
@@ -374,7 +382,7 @@ __global__ void __launch_bounds__(V2Shape<NTILE>::THREADS, 1) k_project_v2(const
   const int gsz = (p.L + 1) * V2_GA;
   double* gbuf = ring + (size_t)p.nbuf * p.slot;            // [NGB][L+1][GA]
   double* red = gbuf + (size_t)V2_NGB * gsz;                // [2][NTILE][KP-1][8][32] K-part partials
-  double* pt = red + (size_t)2 * NTILE * (KP - 1) * 8 * 32; // [npl][V2_TCP]
+  double* pt = red + (size_t)2 * NGRP * (KP - 1) * 8 * 32;  // [npl][V2_TCP]
   const long long cell = blockIdx.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, r0 = lane >> 2, kq = lane & 3;
   // the ring starts zeroed: samples past a row (K padding) and the rows of a
@@ -391,10 +399,12 @@ __global__ void __launch_bounds__(V2Shape<NTILE>::THREADS, 1) k_project_v2(const
   __syncthreads();
   const int nsteps = p.nchunk * p.nv;  // (chunk outer, v inner)
   const long long cell_off = cell * (long long)p.nv * p.nt * p.np;
-  // slab s: element range [e0, e0 + cnt) of f; smem index of element e is
-  // (e - e0) + m, m = 1 when f + e0 is not 16-byte aligned
-  auto geom = [&](int s, long long& e0, int& cnt, int& m) {
-    const int c = s / p.nv, v = s - c * p.nv, t0 = c * TC;
+  // slab (chunk c, radial node v), s = c n_v + v: element range [e0, e0 + cnt) of f;
+  // smem index of element e is (e - e0) + m, m = 1 when f + e0 is not 16-byte
+  // aligned.  Slab, ring-slot and buffer indices are carried as counters: the
+  // integer divisions of s by run-time sizes were 21% of a GEMM warp's time (ncu)
+  auto geom = [&](int c, int v, long long& e0, int& cnt, int& m) {
+    const int t0 = c * TC;
     e0 = cell_off + ((long long)v * p.nt + t0) * p.np;
     cnt = min(TC, p.nt - t0) * p.np;
     m = (int)((reinterpret_cast<uintptr_t>(p.f + e0) >> 3) & 1);
@@ -402,17 +412,17 @@ __global__ void __launch_bounds__(V2Shape<NTILE>::THREADS, 1) k_project_v2(const
 
   if (warp < GW) {
     // ------------------------------------------------ producer: samples -> G
-    const int j = warp % NTILE, part = warp / NTILE;
+    const int j = warp % NGRP, part = warp / NGRP;
     // this warp's blocks [b0, b0 + nb) of the n_p / 16 full blocks; the last
     // part also takes the tail k-steps [4 nfull, ks)
     const int nfull = p.kfull / 4, bq = nfull / KP, br = nfull - bq * KP;
     const int nb = bq + (part >= KP - br ? 1 : 0);  // the extra blocks go to the last parts
     const int b0 = part * bq + max(0, part - (KP - br));
     const int ntail = part == KP - 1 ? p.ks - p.kfull : 0;
-    // FOLD: group j = (|m| tile jp, polar half ph); W^T fragments of the cos and the
+    // FOLD: group j = (|m| tile jp, polar tiles pt0 .. pt0 + NPT - 1); W^T fragments of the cos and the
     // sin columns m = 8 jp + r0 ([jp][cos, sin][ks][32], K = pairs in 16-pair blocks,
     // then the p = 0 step)
-    const int jp = j & 1, ph = j >> 1;
+    const int jp = j & 1, pt0 = NPT * (j >> 1);  // first polar tile of this warp
     double wc[FOLD ? KB * 4 : 1], wsn[FOLD ? KB * 4 : 1], w0 = 0.0;
     if constexpr (FOLD) {
       const double* wq = p.wreg + ((size_t)(2 * jp) * p.ks + 4 * b0) * 32 + lane;
@@ -436,33 +446,43 @@ __global__ void __launch_bounds__(V2Shape<NTILE>::THREADS, 1) k_project_v2(const
     // one thread issues: head / tail elements by hand, the rest in one bulk
     // copy; a refilled slot waits for every GEMM warp's release of its
     // previous slab (empty[]); the mbarrier arrive publishes the generic stores
-    auto issue = [&](int s) {
-      if (s >= nsteps) return;
+    int is = 0, ic = 0, iv = 0, ib = 0, ir = 0;  // next slab to issue: index, chunk, v, ring slot, round
+    auto issue = [&]() {
+      if (is >= nsteps) return;
       long long e0;
       int cnt, m;
-      geom(s, e0, cnt, m);
-      const int b = s % p.nbuf;
-      if (s >= p.nbuf) mbar_wait(&empty[b], (unsigned)(((s / p.nbuf) - 1) & 1));
-      double* dst = ring + (size_t)b * p.slot;
+      geom(ic, iv, e0, cnt, m);
+      if (ir > 0) mbar_wait(&empty[ib], (unsigned)((ir - 1) & 1));
+      double* dst = ring + (size_t)ib * p.slot;
       const int nin = (cnt - m) & ~1;
       if (m) dst[1] = __ldg(p.f + e0);
       if ((cnt - m) & 1) dst[m + cnt - 1] = __ldg(p.f + e0 + cnt - 1);
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // earlier generic stores to the slot
-      mbar_arrive_expect_tx(&full[b], (unsigned)nin * 8u);
-      if (nin > 0) bulk_g2s(dst + 2 * m, p.f + e0 + m, (unsigned)nin * 8u, &full[b]);
+      mbar_arrive_expect_tx(&full[ib], (unsigned)nin * 8u);
+      if (nin > 0) bulk_g2s(dst + 2 * m, p.f + e0 + m, (unsigned)nin * 8u, &full[ib]);
+      ++is;
+      if (++iv == p.nv) {
+        iv = 0;
+        ++ic;
+      }
+      if (++ib == p.nbuf) {
+        ib = 0;
+        ++ir;
+      }
     };
     if (tid == 0)
-      for (int s = 0; s < p.nbuf - 1; ++s) issue(s);
+      for (int k = 0; k < p.nbuf - 1; ++k) issue();
     const int col = 8 * j + r0;
     const int ga = (col + 1) >> 1, side = (col & 1) ? 0 : 1;  // col 2a-1: sin (m = -a), col 2a: cos (m = +a)
+    int cc = 0, cv = 0, b = 0, b2 = 0;  // this slab's chunk, v, ring slot, G buffer
+    unsigned fph = 0;                   // phase parity of full[b]
     for (int s = 0; s < nsteps; ++s) {
       // slab s + nbuf - 2 into the slot of slab s - 2 (one slab of slack for its release)
-      if (tid == 0 && s >= 1) issue(s + p.nbuf - 2);
-      const int b = s % p.nbuf;
-      mbar_wait(&full[b], (unsigned)((s / p.nbuf) & 1));
+      if (tid == 0 && s >= 1) issue();
+      mbar_wait(&full[b], fph);
       long long e0;
       int cnt, m;
-      geom(s, e0, cnt, m);
+      geom(cc, cv, e0, cnt, m);
       // the B gathers are plain (reorderable) loads; this zero, produced after
       // the wait, keeps them from being hoisted above it
       uint32_t after_wait;
@@ -473,18 +493,18 @@ __global__ void __launch_bounds__(V2Shape<NTILE>::THREADS, 1) k_project_v2(const
 #pragma unroll
       for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = 0.0;
       if constexpr (FOLD) {
-        // acc[2 i + cs]: polar tile 2 ph + i, cs = 0 cos / 1 sin.  Pair kappa = 16 block + 4 kq + jj
+        // acc[2 i + cs]: polar tile pt0 + i, cs = 0 cos / 1 sin.  Pair kappa = 16 block + 4 kq + jj
         // is the samples p = kappa + 1 (forward) and n_p - 1 - kappa (mirror).
-        uint32_t rowf[2], rowm[2];
+        uint32_t rowf[NPT], rowm[NPT];
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const uint32_t r = base + (uint32_t)(8 * (2 * ph + i)) * (uint32_t)p.np * 8u;
+        for (int i = 0; i < NPT; ++i) {
+          const uint32_t r = base + (uint32_t)(8 * (pt0 + i)) * (uint32_t)p.np * 8u;
           rowf[i] = r + (uint32_t)(1 + 16 * b0 + 4 * kq) * 8u;
           rowm[i] = r + (uint32_t)(p.np - 1 - 16 * b0 - 4 * kq) * 8u;
         }
         auto kstep = [&](double c, double sn, uint32_t off) {
 #pragma unroll
-          for (int i = 0; i < 2; ++i) {
+          for (int i = 0; i < NPT; ++i) {
             const double a = lds_ro(rowf[i] + off), bm = lds_ro(rowm[i] - off);
             dmma884(acc[2 * i][0], acc[2 * i][1], c, a + bm);
             dmma884(acc[2 * i + 1][0], acc[2 * i + 1][1], sn, a - bm);
@@ -501,9 +521,9 @@ __global__ void __launch_bounds__(V2Shape<NTILE>::THREADS, 1) k_project_v2(const
         }
         if (ntail > 0) {  // p = 0: its own mirror image; the weight sits on the kq = 0 lanes
 #pragma unroll
-          for (int i = 0; i < 2; ++i)
+          for (int i = 0; i < NPT; ++i)
             dmma884(acc[2 * i][0], acc[2 * i][1], w0,
-                    lds_ro(base + (uint32_t)(8 * (2 * ph + i)) * (uint32_t)p.np * 8u));
+                    lds_ro(base + (uint32_t)(8 * (pt0 + i)) * (uint32_t)p.np * 8u));
         }
       } else {
       uint32_t rowb[4];  // block b0, lane offset 4 kq, polar tile i: k-step (block, jj) is +(16 block + jj) doubles
@@ -528,11 +548,10 @@ __global__ void __launch_bounds__(V2Shape<NTILE>::THREADS, 1) k_project_v2(const
           if (u < ntail) kstep(wt[u], tb + (uint32_t)(4 * u) * 8u);
       }
       }
-      const int b2 = s % V2_NGB;
       // partials of the K parts, double-buffered by slab parity: a part writes
       // buffer (s & 1) again at slab s + 2, after the pair barrier of s + 1,
       // which part 0 reaches only after reading it at slab s
-      double* rbuf = red + (size_t)(s & 1) * NTILE * (KP - 1) * 8 * 32;
+      double* rbuf = red + (size_t)(s & 1) * NGRP * (KP - 1) * 8 * 32;
       if (part > 0) {
         const uint32_t rw = smem_u32(rbuf + (size_t)(j * (KP - 1) + part - 1) * 8 * 32 + lane);
 #pragma unroll
@@ -542,7 +561,7 @@ __global__ void __launch_bounds__(V2Shape<NTILE>::THREADS, 1) k_project_v2(const
         }
         bar_sync(V2_BAR_RED0 + j, KP * 32);
       } else {
-        bar_sync(V2_BAR_RED0 + j, KP * 32);
+        if constexpr (KP > 1) bar_sync(V2_BAR_RED0 + j, KP * 32);
         if constexpr (KP > 1) {
           // fixed order: ((p0 + p1) + p2) + p3
 #pragma unroll
@@ -555,16 +574,16 @@ __global__ void __launch_bounds__(V2Shape<NTILE>::THREADS, 1) k_project_v2(const
             }
           }
         }
-        if (s >= V2_NGB) bar_sync(V2_BAR_EMPTY0 + b2, NTH - (GW - NTILE) * 32);  // epilogue consumed b2
+        if (s >= V2_NGB) bar_sync(V2_BAR_EMPTY0 + b2, NTH - (GW - NGRP) * 32);  // epilogue consumed b2
         if constexpr (FOLD) {
           const int mm = 8 * jp + r0;  // |m| of this lane's cos and sin columns
           if (mm <= p.L) {
             const uint32_t gb = smem_u32(gbuf + (size_t)b2 * gsz + (size_t)mm * V2_GA);
 #pragma unroll
-            for (int i = 0; i < 2; ++i)
+            for (int i = 0; i < NPT; ++i)
 #pragma unroll
               for (int e = 0; e < 2; ++e) {
-                const uint32_t t2 = (uint32_t)(2 * (8 * (2 * ph + i) + 2 * kq + e)) * 8u;
+                const uint32_t t2 = (uint32_t)(2 * (8 * (pt0 + i) + 2 * kq + e)) * 8u;
                 sts128_v(gb + t2, acc[2 * i + 1][e], acc[2 * i][e]);  // (sin, cos); m = 0: sin weights are 0
               }
           }
@@ -576,11 +595,20 @@ __global__ void __launch_bounds__(V2Shape<NTILE>::THREADS, 1) k_project_v2(const
             for (int e = 0; e < 2; ++e) sts_v(gb + (uint32_t)(2 * (8 * i + 2 * kq + e)) * 8u, acc[i][e]);
         }
         __threadfence_block();
-        bar_arrive(V2_BAR_FULL0 + b2, NTH - (GW - NTILE) * 32);
+        bar_arrive(V2_BAR_FULL0 + b2, NTH - (GW - NGRP) * 32);
       }
       // release ring slot b: after the stores above, which consume every gather
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[b]);
+      if (++cv == p.nv) {
+        cv = 0;
+        ++cc;
+      }
+      if (++b == p.nbuf) {
+        b = 0;
+        fph ^= 1u;
+      }
+      b2 = (b2 + 1) & (V2_NGB - 1);
     }
   } else {
     // ------------------------------------------------ consumer: G -> coefficients
@@ -598,8 +626,8 @@ __global__ void __launch_bounds__(V2Shape<NTILE>::THREADS, 1) k_project_v2(const
 #pragma unroll
     for (int k = 0; k < V2_KH; ++k) racc[0][k] = racc[1][k] = 0.0;
     const uint32_t prow = smem_u32(pt + (size_t)r * V2_TCP + hf);  // this lane's polar rows: t = 2 u + hf
+    int c = 0, v = 0, b2 = 0;
     for (int s = 0; s < nsteps; ++s) {
-      const int c = s / p.nv, v = s - c * p.nv, b2 = s % V2_NGB;
       if (v == 0) {  // new chunk: its polar table (after every epilogue thread finished the old one)
         bar_sync(V2_BAR_EPI, NT_E);
         for (int i = et; i < p.npl * TC; i += NT_E) {
@@ -612,7 +640,7 @@ __global__ void __launch_bounds__(V2Shape<NTILE>::THREADS, 1) k_project_v2(const
       const double* rv = p.rtab + ((size_t)v * (p.L + 1) + l) * p.nk + kb;
 #pragma unroll
       for (int k = 0; k < V2_KH; ++k) rk[k] = (live && kb + k < ke) ? __ldg(rv + k) : 0.0;
-      bar_sync(V2_BAR_FULL0 + b2, NTH - (GW - NTILE) * 32);  // G buffer b2 written (also orders pt)
+      bar_sync(V2_BAR_FULL0 + b2, NTH - (GW - NGRP) * 32);  // G buffer b2 written (also orders pt)
       double as = 0.0, ac = 0.0;
       if (live) {
         // the pair interleaves its rows (t = 2 u + hf): the two lanes hit adjacent banks
@@ -632,7 +660,7 @@ __global__ void __launch_bounds__(V2Shape<NTILE>::THREADS, 1) k_project_v2(const
         ac = (ca[0] + ca[1]) + (ca[2] + ca[3]);
       }
       __threadfence_block();
-      bar_arrive(V2_BAR_EMPTY0 + b2, NTH - (GW - NTILE) * 32);  // buffer b2 may be rewritten
+      bar_arrive(V2_BAR_EMPTY0 + b2, NTH - (GW - NGRP) * 32);  // buffer b2 may be rewritten
       // both halves of the row, added in the same order on both lanes
       const double os = __shfl_xor_sync(0xffffffffu, as, 1), oc = __shfl_xor_sync(0xffffffffu, ac, 1);
       const double ts = hf ? os + as : as + os, tcv = hf ? oc + ac : ac + oc;
@@ -641,6 +669,11 @@ __global__ void __launch_bounds__(V2Shape<NTILE>::THREADS, 1) k_project_v2(const
         racc[0][k] = fma(rk[k], ts, racc[0][k]);
         racc[1][k] = fma(rk[k], tcv, racc[1][k]);
       }
+      if (++v == p.nv) {
+        v = 0;
+        ++c;
+      }
+      b2 = (b2 + 1) & (V2_NGB - 1);
     }
     if (live) {
       double* oc = p.out + cell * (long long)p.nk * p.nq;
@@ -676,11 +709,21 @@ Ps2Kernel ps2_kernel(int ntile, int kb) {
     default: return nullptr;
   }
 }
-Ps2Kernel ps2_fold_kernel(int kb) {
+// whole: no K split (kb = all blocks, <= 4); else two K parts (kb = blocks of the larger part, <= 3)
+Ps2Kernel ps2_fold_kernel(int kb, bool whole) {
+  if (whole) {
+    switch (kb) {
+      case 1: return k_project_v2<4, 1, 2>;
+      case 2: return k_project_v2<4, 2, 2>;
+      case 3: return k_project_v2<4, 3, 2>;
+      case 4: return k_project_v2<4, 4, 2>;
+      default: return nullptr;
+    }
+  }
   switch (kb) {
-    case 1: return k_project_v2<4, 1, true>;
-    case 2: return k_project_v2<4, 2, true>;
-    case 3: return k_project_v2<4, 3, true>;
+    case 1: return k_project_v2<4, 1, 1>;
+    case 2: return k_project_v2<4, 2, 1>;
+    case 3: return k_project_v2<4, 3, 1>;
     default: return nullptr;
   }
 }
@@ -871,8 +914,9 @@ int bfq_projector_create(int32_t k_max, int32_t l_max, int32_t n_v, int32_t n_t,
   // Anything else keeps the unfolded kernel.
   if (pj->v2 && (n_p & 1) && l_max >= 8 && l_max <= 15 && npl <= V2_EPI_WARPS * 16 && !std::getenv("BFQ_PROJ_NOFOLD")) {
     const int H = (n_p - 1) / 2, nfull = H / 16;
-    const int kb3 = (nfull + 1) / 2;
-    bool ok = H % 16 == 0 && nfull >= 2 && kb3 <= FOLD_MAXKB;
+    const bool whole = nfull <= 4 && !std::getenv("BFQ_PROJ_FOLD_SPLITK");  // K unsplit: order <= 64
+    const int kb3 = whole ? nfull : (nfull + 1) / 2;
+    bool ok = H % 16 == 0 && nfull >= (whole ? 1 : 2) && kb3 <= (whole ? 4 : FOLD_MAXKB);
     for (int col = 0; ok && col < pj->ncol; ++col) {
       const double* w = phi_tab + (size_t)col * n_p;
       double mx = 0.0;
@@ -889,9 +933,10 @@ int bfq_projector_create(int32_t k_max, int32_t l_max, int32_t n_v, int32_t n_t,
       pj->kb3 = kb3;
       auto smem3_for = [&](int nbuf) {
         return (size_t)128 + (size_t)8 * ((size_t)nbuf * pj->slot2 + (size_t)V2_NGB * (l_max + 1) * V2_GA +
-                                          (size_t)ps2_red_doubles(4) + (size_t)npl * V2_TCP);
+                                          (size_t)(whole ? 0 : ps2_red_doubles(4)) + (size_t)npl * V2_TCP);
       };
       int nb = V2_MAXBUF;
+      if (const char* e = std::getenv("BFQ_PROJ_NBUF")) nb = std::max(3, std::min(V2_MAXBUF, std::atoi(e)));  // experiments
       while (nb > 2 && smem3_for(nb) > (size_t)optin) --nb;
       std::vector<double> wf3((size_t)2 * 2 * pj->ks3 * 32, 0.0);
       for (int jp = 0; jp < 2; ++jp)
@@ -916,12 +961,13 @@ int bfq_projector_create(int32_t k_max, int32_t l_max, int32_t n_v, int32_t n_t,
         pj->nbuf3 = nb;
         pj->smem3 = smem3_for(nb);
         if (!up(wf3, &pj->wfold) ||
-            cudaFuncSetAttribute(ps2_fold_kernel(kb3), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pj->smem3) !=
+            cudaFuncSetAttribute(ps2_fold_kernel(kb3, whole), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pj->smem3) !=
                 cudaSuccess) {
           bfq_projector_destroy(pj);
           return fail(BFQ_ECUDA, "cannot set up the folded projection kernel");
         }
         pj->fold = true;
+        pj->fold_whole = whole;
       }
     }
   }
@@ -974,7 +1020,7 @@ int bfq_project_samples(const bfq_projector* pj, const double* samples, double* 
       q.kfull = pj->kfull3;
       q.nbuf = pj->nbuf3;
       q.wreg = pj->wfold;
-      ps2_fold_kernel(pj->kb3)<<<(unsigned)n, ps2_threads(4), pj->smem3, (cudaStream_t)stream>>>(q);
+      ps2_fold_kernel(pj->kb3, pj->fold_whole)<<<(unsigned)n, ps2_threads(4), pj->smem3, (cudaStream_t)stream>>>(q);
     } else {
       ps2_kernel(pj->ntile, pj->kb2)<<<(unsigned)n, ps2_threads(pj->ntile), pj->smem2, (cudaStream_t)stream>>>(q);
     }

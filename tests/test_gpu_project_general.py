@@ -137,21 +137,29 @@ def test_folded_kernel_matches_reference_and_unfolded(case, monkeypatch):
     pf = gproject.Projector(cfg, order)
     assert pf.kernel == 3
     fold = pf.project(samples).cpu().numpy()
+    # the two-K-part layout of the folded kernel (the default above keeps K whole at these orders)
+    monkeypatch.setenv("BFQ_PROJ_FOLD_SPLITK", "1")
+    ps = gproject.Projector(cfg, order)
+    assert ps.kernel == 3
+    split = ps.project(samples).cpu().numpy()
     monkeypatch.setenv("BFQ_PROJ_NOFOLD", "1")
     pu = gproject.Projector(cfg, order)
     assert pu.kernel == 2
     plain = pu.project(samples).cpu().numpy()
     for i, n in enumerate(names):
         assert rel(fold[i], GOLD[f"{n}_k{k}_l{l}_o{order}"]) <= 1e-13, n
+        assert rel(split[i], GOLD[f"{n}_k{k}_l{l}_o{order}"]) <= 1e-13, n
         assert rel(fold[i], plain[i]) <= 5e-14, n
+        assert rel(fold[i], split[i]) <= 1e-14, n
 
 
-@pytest.mark.parametrize("l_max,order,offset", [(8, 48, 0), (8, 48, 1), (14, 32, 1), (9, 64, 0)])
+@pytest.mark.parametrize("l_max,order,offset", [(8, 48, 0), (8, 48, 1), (14, 32, 1), (9, 64, 0), (8, 80, 1), (8, 16, 0)])
 def test_folded_kernel_partial_chunks_and_misaligned(l_max, order, offset):
     """Folded kernel on a partial polar chunk with unequal K parts (order 48: 48 =
     32 + 16 polar rows, three 16-pair blocks split 1 + 2), on the widest |m| tile
     pair the epilogue holds (l_max = 14) and on a half-empty one (l_max = 9), with the batch shifted
-    by one double; against the CPU restatement of basis.project."""
+    by one double; order 80 (five 16-pair blocks) takes the two-K-part layout,
+    order 16 a single block; against the CPU restatement of basis.project."""
     from oracle.project_oracle import ProjectionOracle
 
     cfg = SpectralConfig(3, l_max, 1.0)
