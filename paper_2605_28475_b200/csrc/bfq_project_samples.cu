@@ -320,6 +320,7 @@ constexpr int V2_NKMAX = 17;       // n_k <= 17: radial accumulators (half of th
 constexpr int V2_KH = (V2_NKMAX + 1) / 2;
 constexpr int V2_MAXBUF = 6;
 constexpr int V2_NGB = 4;  // G buffers: the epilogue may lag the GEMM by three slabs
+constexpr int V2_HDR = 256;  // mbarriers: full / empty [V2_MAXBUF], gfull / gempty [V2_NGB]
 constexpr unsigned V2_BAR_FULL0 = 2, V2_BAR_EMPTY0 = 2 + V2_NGB, V2_BAR_EPI = 2 + 2 * V2_NGB,
                    V2_BAR_RED0 = 3 + 2 * V2_NGB;  // + column tile: the K-part reduction
 
@@ -378,7 +379,13 @@ __global__ void __launch_bounds__(V2Shape<NTILE>::THREADS, 1) k_project_v2(const
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);  // [V2_MAXBUF] slab landed
   uint64_t* empty = full + V2_MAXBUF;                         // [V2_MAXBUF] slab released by every GEMM warp
-  double* ring = reinterpret_cast<double*>(smem_raw + 128);  // [nbuf][slot]
+  // G-buffer handoff through mbarriers (one arrival per warp): a GEMM warp waits
+  // only for the epilogue's release of the buffer it is about to write, not for
+  // its peers (the named FULL / EMPTY barriers re-synchronised all GEMM warps
+  // every slab: 14% of their time, ncu)
+  uint64_t* gfull = empty + V2_MAXBUF;                        // [V2_NGB] G buffer written by every storing warp
+  uint64_t* gempty = gfull + V2_NGB;                          // [V2_NGB] G buffer read by every epilogue warp
+  double* ring = reinterpret_cast<double*>(smem_raw + V2_HDR);  // [nbuf][slot]
   const int gsz = (p.L + 1) * V2_GA;
   double* gbuf = ring + (size_t)p.nbuf * p.slot;            // [NGB][L+1][GA]
   double* red = gbuf + (size_t)V2_NGB * gsz;                // [2][NTILE][KP-1][8][32] K-part partials
@@ -392,6 +399,10 @@ __global__ void __launch_bounds__(V2Shape<NTILE>::THREADS, 1) k_project_v2(const
     for (int b = 0; b < p.nbuf; ++b) {
       mbar_init(&full[b], 1);
       mbar_init(&empty[b], GW);
+    }
+    for (int b = 0; b < V2_NGB; ++b) {
+      mbar_init(&gfull[b], NGRP);
+      mbar_init(&gempty[b], V2_EPI_WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -475,7 +486,7 @@ __global__ void __launch_bounds__(V2Shape<NTILE>::THREADS, 1) k_project_v2(const
     const int col = 8 * j + r0;
     const int ga = (col + 1) >> 1, side = (col & 1) ? 0 : 1;  // col 2a-1: sin (m = -a), col 2a: cos (m = +a)
     int cc = 0, cv = 0, b = 0, b2 = 0;  // this slab's chunk, v, ring slot, G buffer
-    unsigned fph = 0;                   // phase parity of full[b]
+    unsigned fph = 0, gph = 0;          // phase parity of full[b]; of G buffer b2's current round
     for (int s = 0; s < nsteps; ++s) {
       // slab s + nbuf - 2 into the slot of slab s - 2 (one slab of slack for its release)
       if (tid == 0 && s >= 1) issue();
@@ -574,7 +585,7 @@ __global__ void __launch_bounds__(V2Shape<NTILE>::THREADS, 1) k_project_v2(const
             }
           }
         }
-        if (s >= V2_NGB) bar_sync(V2_BAR_EMPTY0 + b2, NTH - (GW - NGRP) * 32);  // epilogue consumed b2
+        if (s >= V2_NGB) mbar_wait(&gempty[b2], gph ^ 1u);  // the epilogue released b2 (previous round)
         if constexpr (FOLD) {
           const int mm = 8 * jp + r0;  // |m| of this lane's cos and sin columns
           if (mm <= p.L) {
@@ -594,8 +605,8 @@ __global__ void __launch_bounds__(V2Shape<NTILE>::THREADS, 1) k_project_v2(const
 #pragma unroll
             for (int e = 0; e < 2; ++e) sts_v(gb + (uint32_t)(2 * (8 * i + 2 * kq + e)) * 8u, acc[i][e]);
         }
-        __threadfence_block();
-        bar_arrive(V2_BAR_FULL0 + b2, NTH - (GW - NGRP) * 32);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&gfull[b2]);  // release: the stores above are visible to the waiters
       }
       // release ring slot b: after the stores above, which consume every gather
       __syncwarp();
@@ -609,6 +620,7 @@ __global__ void __launch_bounds__(V2Shape<NTILE>::THREADS, 1) k_project_v2(const
         fph ^= 1u;
       }
       b2 = (b2 + 1) & (V2_NGB - 1);
+      if (b2 == 0) gph ^= 1u;
     }
   } else {
     // ------------------------------------------------ consumer: G -> coefficients
@@ -627,6 +639,7 @@ __global__ void __launch_bounds__(V2Shape<NTILE>::THREADS, 1) k_project_v2(const
     for (int k = 0; k < V2_KH; ++k) racc[0][k] = racc[1][k] = 0.0;
     const uint32_t prow = smem_u32(pt + (size_t)r * V2_TCP + hf);  // this lane's polar rows: t = 2 u + hf
     int c = 0, v = 0, b2 = 0;
+    unsigned gph = 0;
     for (int s = 0; s < nsteps; ++s) {
       if (v == 0) {  // new chunk: its polar table (after every epilogue thread finished the old one)
         bar_sync(V2_BAR_EPI, NT_E);
@@ -634,13 +647,14 @@ __global__ void __launch_bounds__(V2Shape<NTILE>::THREADS, 1) k_project_v2(const
           const int row = i / TC;
           pt[row * V2_TCP + (i - row * TC)] = p.ptab[(size_t)c * p.npl * TC + i];
         }
+        bar_sync(V2_BAR_EPI, NT_E);  // table complete before any epilogue warp reads it
       }
       // radial factors of this slab's v (global / L1; issued before the wait)
       double rk[V2_KH];
       const double* rv = p.rtab + ((size_t)v * (p.L + 1) + l) * p.nk + kb;
 #pragma unroll
       for (int k = 0; k < V2_KH; ++k) rk[k] = (live && kb + k < ke) ? __ldg(rv + k) : 0.0;
-      bar_sync(V2_BAR_FULL0 + b2, NTH - (GW - NGRP) * 32);  // G buffer b2 written (also orders pt)
+      mbar_wait(&gfull[b2], gph);  // G buffer b2 written by every storing warp
       double as = 0.0, ac = 0.0;
       if (live) {
         // the pair interleaves its rows (t = 2 u + hf): the two lanes hit adjacent banks
@@ -659,8 +673,8 @@ __global__ void __launch_bounds__(V2Shape<NTILE>::THREADS, 1) k_project_v2(const
         as = (sa[0] + sa[1]) + (sa[2] + sa[3]);
         ac = (ca[0] + ca[1]) + (ca[2] + ca[3]);
       }
-      __threadfence_block();
-      bar_arrive(V2_BAR_EMPTY0 + b2, NTH - (GW - NGRP) * 32);  // buffer b2 may be rewritten
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&gempty[b2]);  // buffer b2 may be rewritten
       // both halves of the row, added in the same order on both lanes
       const double os = __shfl_xor_sync(0xffffffffu, as, 1), oc = __shfl_xor_sync(0xffffffffu, ac, 1);
       const double ts = hf ? os + as : as + os, tcv = hf ? oc + ac : ac + oc;
@@ -674,6 +688,7 @@ __global__ void __launch_bounds__(V2Shape<NTILE>::THREADS, 1) k_project_v2(const
         ++c;
       }
       b2 = (b2 + 1) & (V2_NGB - 1);
+      if (b2 == 0) gph ^= 1u;
     }
     if (live) {
       double* oc = p.out + cell * (long long)p.nk * p.nq;
@@ -870,7 +885,7 @@ int bfq_projector_create(int32_t k_max, int32_t l_max, int32_t n_v, int32_t n_t,
                        pj->kb2 <= 4 && !std::getenv("BFQ_PROJ_V1");
   if (v2_fits) {
     auto smem2_for = [&](int nbuf) {
-      return (size_t)128 + (size_t)8 * ((size_t)nbuf * pj->slot2 + (size_t)V2_NGB * (l_max + 1) * V2_GA +
+      return (size_t)V2_HDR + (size_t)8 * ((size_t)nbuf * pj->slot2 + (size_t)V2_NGB * (l_max + 1) * V2_GA +
                                         (size_t)ps2_red_doubles(pj->ntile) + (size_t)npl * V2_TCP);
     };
     int nb = V2_MAXBUF;
@@ -932,7 +947,7 @@ int bfq_projector_create(int32_t k_max, int32_t l_max, int32_t n_v, int32_t n_t,
       pj->ks3 = pj->kfull3 + 1;
       pj->kb3 = kb3;
       auto smem3_for = [&](int nbuf) {
-        return (size_t)128 + (size_t)8 * ((size_t)nbuf * pj->slot2 + (size_t)V2_NGB * (l_max + 1) * V2_GA +
+        return (size_t)V2_HDR + (size_t)8 * ((size_t)nbuf * pj->slot2 + (size_t)V2_NGB * (l_max + 1) * V2_GA +
                                           (size_t)(whole ? 0 : ps2_red_doubles(4)) + (size_t)npl * V2_TCP);
       };
       int nb = V2_MAXBUF;
