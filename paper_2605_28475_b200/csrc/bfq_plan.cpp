@@ -516,7 +516,28 @@ static double pack_program(const HostPlan& hp, Program& pg, const std::vector<in
       out[i].lock = cta_cost(m, &ok);
     }
     out.erase(std::remove_if(out.begin(), out.end(), [](const Cta& x) { return x.team_l1.empty(); }), out.end());
-    ctas.swap(out);
+    // self-check before the refined schedule replaces the greedy one: every unit
+    // exactly once, CTA shape respected
+    bool valid = true;
+    size_t placed = 0;
+    std::vector<std::vector<char>> seen(pg.groups.size());
+    for (const Group& gr : pg.groups) seen[gr.l1].assign((size_t)std::max(gr.n_units, 0), 0);
+    for (const Cta& cta : out) {
+      int used = 0;
+      valid &= (int)cta.team_l1.size() <= c.nteams;
+      for (size_t t = 0; t < cta.team_l1.size(); ++t)
+        for (int u : cta.team_units[t]) {
+          std::vector<char>& sg = seen[cta.team_l1[t]];
+          if (u < 0 || u >= (int)sg.size() || sg[u]) valid = false;
+          else sg[u] = 1;
+          ++used;
+          ++placed;
+        }
+      valid &= used <= c.upc;
+    }
+    valid &= placed == units_all.size();
+    if (valid) ctas.swap(out);
+    else if (std::getenv("BFQ_PLAN_STATS")) std::fprintf(stderr, "plan: refined schedule rejected by the self-check\n");
   }
   // renumber units inside each group in order of appearance
   std::vector<int16_t> new_m1 = pg.unit_m1;

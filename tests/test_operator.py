@@ -106,3 +106,17 @@ def test_host_plan_large_configs_fit():
             continue
         info = engine.host_plan_info(load_op(name))
         assert info["folded"] == 1 and info["smem_bytes"] <= 232448
+
+
+def test_annealed_packing_keeps_a_valid_schedule(monkeypatch):
+    """The annealing refinement of the CTA packing (bfq_plan.cpp, on by default where
+    two R rings fit) never needs more CTAs per tile than the greedy packers, and the
+    plan stays valid (the builder self-checks every unit is scheduled exactly once)."""
+    op = load_op("hs_n8")
+    monkeypatch.setenv("BFQ_PACK_REFINE", "0")
+    greedy = engine.host_plan_info(op)
+    monkeypatch.setenv("BFQ_PACK_REFINE", "1")
+    refined = engine.host_plan_info(op)
+    assert refined["items_per_tile"] <= greedy["items_per_tile"]
+    for k in ("cells_per_cta", "warps_per_cta", "smem_bytes", "exec_macs_per_cell", "useful_macs_per_cell"):
+        assert refined[k] == greedy[k]
