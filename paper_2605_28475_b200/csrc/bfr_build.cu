@@ -540,8 +540,12 @@ struct TriParams {
   double* part;  // [block][split][rows_max][nk*nk]
 };
 
-template <int MT, int NPW>
-__global__ void __launch_bounds__(256) k_tri(TriParams p) {
+// NW warps per CTA: the (a,b) column tiles are dealt tile = warp + NW i, so NW x NPW
+// should just cover ceil(n_k^2 / 8) tiles -- 22 at n_k = 13: 11 warps x 2 (8 warps x 3
+// left warps 6 and 7 with two tiles where the others have three, idle a third of
+// every chunk behind the per-chunk barrier)
+template <int MT, int NPW, int NW = 8>
+__global__ void __launch_bounds__(NW * 32, 2) k_tri(TriParams p) {
   extern __shared__ double sm[];
   const TriBlock blk = p.blocks[blockIdx.y];
   const int split = blockIdx.x;
@@ -564,7 +568,7 @@ __global__ void __launch_bounds__(256) k_tri(TriParams p) {
   int uoff[NPW], woff[NPW];
 #pragma unroll
   for (int i = 0; i < NPW; ++i) {
-    const int n = min((warp + 8 * i) * 8 + r0, nn - 1);
+    const int n = min((warp + NW * i) * 8 + r0, nn - 1);
     const int a = n / nk, b = n - a * nk;
     uoff[i] = (rows + a) * SROW;
     woff[i] = (rows + nk + b) * SROW;
@@ -610,7 +614,7 @@ __global__ void __launch_bounds__(256) k_tri(TriParams p) {
       for (int mt = 0; mt < MT; ++mt) a[mt] = s[xoff[mt] + col];
 #pragma unroll
       for (int i = 0; i < NPW; ++i) {
-        if (warp + 8 * i < ntiles) {
+        if (warp + NW * i < ntiles) {
           const double b = s[uoff[i] + col] * s[woff[i] + col];
 #pragma unroll
           for (int mt = 0; mt < MT; ++mt)
@@ -626,7 +630,7 @@ __global__ void __launch_bounds__(256) k_tri(TriParams p) {
     if (row >= rows) continue;
 #pragma unroll
     for (int i = 0; i < NPW; ++i) {
-      const int tile = warp + 8 * i;
+      const int tile = warp + NW * i;
       if (tile >= ntiles) continue;
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
@@ -893,9 +897,15 @@ int assemble(const bfr_desc& d, int device, double* r_out, double* halves_out, b
 
   // 8-row tiles per contraction block: 5 while the accumulators (MT x NPW x 2) keep
   // k_tri at <= 128 registers (two CTAs per SM), 3 for the wider n_k = 14..17 tiling
-  const int npw = ((nn + 7) / 8 + 7) / 8;
+  int npw = ((nn + 7) / 8 + 7) / 8, tri_warps = 8;
   const int MT_BLK = npw <= 3 ? 5 : 3;
   TriKernel tri = pick_tri(MT_BLK, npw);
+  // 17..22 column tiles (n_k = 12, 13): 11 warps x 2 tiles instead of 8 x 3
+  if ((nn + 7) / 8 > 16 && (nn + 7) / 8 <= 22 && !std::getenv("BFR_TRI_8WARPS")) {
+    npw = 2;
+    tri_warps = 11;
+    tri = k_tri<5, 2, 11>;
+  }
   if (!tri) {
     set_error("n_k outside the contraction kernel's tiling (n_k <= 17)");
     return BFQ_EINVAL;
@@ -1081,7 +1091,7 @@ int assemble(const bfr_desc& d, int device, double* r_out, double* halves_out, b
       BFR_LAUNCH_CHECK("xr");
       BFR_TRY(cudaEventRecord(evs[2 + 2 * ib]));
       TriParams tp{X, phi, d_blocks[bi], d_rowtab[bi], nk, S, PR, rows_max, P, PS, part};
-      tri<<<dim3(S, nblk), 256, tri_smem>>>(tp);
+      tri<<<dim3(S, nblk), tri_warps * 32, tri_smem>>>(tp);
       BFR_LAUNCH_CHECK("tri");
       BFR_TRY(cudaEventRecord(evs[3 + 2 * ib]));
       k_reduce<<<blocks_for((long long)nblk * rows_max * nn, 256), 256>>>(part, d_blocks[bi], nblk, d_rowmap[bi],
