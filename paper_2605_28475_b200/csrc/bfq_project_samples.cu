@@ -52,6 +52,7 @@ struct bfq_projector {
   size_t smem2 = 0;
   double* wreg = nullptr;   // [ntile][ks2][32] A fragments of W^T, K permuted
   // mirror-folded v2 (FOLD): azimuth table even / odd under p <-> n_p - p (checked at create)
+  int sms = 1;  // v2 kernels are persistent: one CTA per SM, cells strided over the grid
   bool fold = false, fold_whole = false;
   int kfull3 = 0, ks3 = 0, kb3 = 0, nbuf3 = 0;
   size_t smem3 = 0;
@@ -390,7 +391,11 @@ __global__ void __launch_bounds__(V2Shape<NTILE>::THREADS, 1) k_project_v2(const
   double* gbuf = ring + (size_t)p.nbuf * p.slot;            // [NGB][L+1][GA]
   double* red = gbuf + (size_t)V2_NGB * gsz;                // [2][NTILE][KP-1][8][32] K-part partials
   double* pt = red + (size_t)2 * NGRP * (KP - 1) * 8 * 32;  // [npl][V2_TCP]
-  const long long cell = blockIdx.x;
+  // persistent: this CTA projects the cells blockIdx.x, blockIdx.x + gridDim.x, ... back to back;
+  // the sample ring, the G buffers and every barrier phase run on across cell boundaries, so
+  // the next cell's first slabs stream in while the epilogue finishes the current cell
+  const long long cell0 = blockIdx.x, cstride = gridDim.x;
+  const long long ncl = p.n > cell0 ? (p.n - cell0 + cstride - 1) / cstride : 0;  // cells of this CTA
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, r0 = lane >> 2, kq = lane & 3;
   // the ring starts zeroed: samples past a row (K padding) and the rows of a
   // partial polar chunk are read as finite values that meet W = 0 / P = 0
@@ -408,15 +413,16 @@ __global__ void __launch_bounds__(V2Shape<NTILE>::THREADS, 1) k_project_v2(const
   }
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // zeros before the bulk copies
   __syncthreads();
-  const int nsteps = p.nchunk * p.nv;  // (chunk outer, v inner)
-  const long long cell_off = cell * (long long)p.nv * p.nt * p.np;
+  const int nsteps = p.nchunk * p.nv;  // slabs per cell (chunk outer, v inner)
+  const long long total = ncl * nsteps;  // slabs of this CTA
+  const long long cell_elems = (long long)p.nv * p.nt * p.np;
   // slab (chunk c, radial node v), s = c n_v + v: element range [e0, e0 + cnt) of f;
   // smem index of element e is (e - e0) + m, m = 1 when f + e0 is not 16-byte
   // aligned.  Slab, ring-slot and buffer indices are carried as counters: the
   // integer divisions of s by run-time sizes were 21% of a GEMM warp's time (ncu)
-  auto geom = [&](int c, int v, long long& e0, int& cnt, int& m) {
+  auto geom = [&](long long cell, int c, int v, long long& e0, int& cnt, int& m) {
     const int t0 = c * TC;
-    e0 = cell_off + ((long long)v * p.nt + t0) * p.np;
+    e0 = cell * cell_elems + ((long long)v * p.nt + t0) * p.np;
     cnt = min(TC, p.nt - t0) * p.np;
     m = (int)((reinterpret_cast<uintptr_t>(p.f + e0) >> 3) & 1);
   };
@@ -457,12 +463,13 @@ __global__ void __launch_bounds__(V2Shape<NTILE>::THREADS, 1) k_project_v2(const
     // one thread issues: head / tail elements by hand, the rest in one bulk
     // copy; a refilled slot waits for every GEMM warp's release of its
     // previous slab (empty[]); the mbarrier arrive publishes the generic stores
-    int is = 0, ic = 0, iv = 0, ib = 0, ir = 0;  // next slab to issue: index, chunk, v, ring slot, round
+    long long is = 0, icell = cell0;     // next slab to issue: index, cell,
+    int ic = 0, iv = 0, ib = 0, ir = 0;  // chunk, v, ring slot, round
     auto issue = [&]() {
-      if (is >= nsteps) return;
+      if (is >= total) return;
       long long e0;
       int cnt, m;
-      geom(ic, iv, e0, cnt, m);
+      geom(icell, ic, iv, e0, cnt, m);
       if (ir > 0) mbar_wait(&empty[ib], (unsigned)((ir - 1) & 1));
       double* dst = ring + (size_t)ib * p.slot;
       const int nin = (cnt - m) & ~1;
@@ -474,7 +481,10 @@ __global__ void __launch_bounds__(V2Shape<NTILE>::THREADS, 1) k_project_v2(const
       ++is;
       if (++iv == p.nv) {
         iv = 0;
-        ++ic;
+        if (++ic == p.nchunk) {
+          ic = 0;
+          icell += cstride;
+        }
       }
       if (++ib == p.nbuf) {
         ib = 0;
@@ -485,15 +495,16 @@ __global__ void __launch_bounds__(V2Shape<NTILE>::THREADS, 1) k_project_v2(const
       for (int k = 0; k < p.nbuf - 1; ++k) issue();
     const int col = 8 * j + r0;
     const int ga = (col + 1) >> 1, side = (col & 1) ? 0 : 1;  // col 2a-1: sin (m = -a), col 2a: cos (m = +a)
-    int cc = 0, cv = 0, b = 0, b2 = 0;  // this slab's chunk, v, ring slot, G buffer
+    long long ccell = cell0;            // this slab's cell,
+    int cc = 0, cv = 0, b = 0, b2 = 0;  // chunk, v, ring slot, G buffer
     unsigned fph = 0, gph = 0;          // phase parity of full[b]; of G buffer b2's current round
-    for (int s = 0; s < nsteps; ++s) {
+    for (long long s = 0; s < total; ++s) {
       // slab s + nbuf - 2 into the slot of slab s - 2 (one slab of slack for its release)
       if (tid == 0 && s >= 1) issue();
       mbar_wait(&full[b], fph);
       long long e0;
       int cnt, m;
-      geom(cc, cv, e0, cnt, m);
+      geom(ccell, cc, cv, e0, cnt, m);
       // the B gathers are plain (reorderable) loads; this zero, produced after
       // the wait, keeps them from being hoisted above it
       uint32_t after_wait;
@@ -613,7 +624,10 @@ __global__ void __launch_bounds__(V2Shape<NTILE>::THREADS, 1) k_project_v2(const
       if (lane == 0) mbar_arrive(&empty[b]);
       if (++cv == p.nv) {
         cv = 0;
-        ++cc;
+        if (++cc == p.nchunk) {
+          cc = 0;
+          ccell += cstride;
+        }
       }
       if (++b == p.nbuf) {
         b = 0;
@@ -638,10 +652,13 @@ __global__ void __launch_bounds__(V2Shape<NTILE>::THREADS, 1) k_project_v2(const
 #pragma unroll
     for (int k = 0; k < V2_KH; ++k) racc[0][k] = racc[1][k] = 0.0;
     const uint32_t prow = smem_u32(pt + (size_t)r * V2_TCP + hf);  // this lane's polar rows: t = 2 u + hf
+    long long cell = cell0;
     int c = 0, v = 0, b2 = 0;
     unsigned gph = 0;
-    for (int s = 0; s < nsteps; ++s) {
-      if (v == 0) {  // new chunk: its polar table (after every epilogue thread finished the old one)
+    for (long long s = 0; s < total; ++s) {
+      // new chunk: its polar table (after every epilogue thread finished the old one);
+      // with a single chunk the table of the first cell serves every cell
+      if (v == 0 && (p.nchunk > 1 || s == 0)) {
         bar_sync(V2_BAR_EPI, NT_E);
         for (int i = et; i < p.npl * TC; i += NT_E) {
           const int row = i / TC;
@@ -683,22 +700,27 @@ __global__ void __launch_bounds__(V2Shape<NTILE>::THREADS, 1) k_project_v2(const
         racc[0][k] = fma(rk[k], ts, racc[0][k]);
         racc[1][k] = fma(rk[k], tcv, racc[1][k]);
       }
-      if (++v == p.nv) {
-        v = 0;
-        ++c;
-      }
       b2 = (b2 + 1) & (V2_NGB - 1);
       if (b2 == 0) gph ^= 1u;
-    }
-    if (live) {
-      double* oc = p.out + cell * (long long)p.nk * p.nq;
-      const int qc = l * l + l + a, qs = l * l + l - a;  // cos side: m = +a (m = 0: column 0); sin side: m = -a
+      if (++v == p.nv) {
+        v = 0;
+        if (++c == p.nchunk) {  // the cell is complete: store its coefficients, start the next from zero
+          c = 0;
+          if (live) {
+            double* oc = p.out + cell * (long long)p.nk * p.nq;
+            const int qc = l * l + l + a, qs = l * l + l - a;  // cos side: m = +a (m = 0: column 0); sin side: m = -a
 #pragma unroll
-      for (int k = 0; k < V2_KH; ++k)
-        if (kb + k < ke) {
-          oc[(size_t)(kb + k) * p.nq + qc] = racc[1][k];
-          if (a > 0) oc[(size_t)(kb + k) * p.nq + qs] = racc[0][k];
+            for (int k = 0; k < V2_KH; ++k)
+              if (kb + k < ke) {
+                oc[(size_t)(kb + k) * p.nq + qc] = racc[1][k];
+                if (a > 0) oc[(size_t)(kb + k) * p.nq + qs] = racc[0][k];
+              }
+          }
+#pragma unroll
+          for (int k = 0; k < V2_KH; ++k) racc[0][k] = racc[1][k] = 0.0;
+          cell += cstride;
         }
+      }
     }
   }
 }
@@ -819,6 +841,7 @@ int bfq_projector_create(int32_t k_max, int32_t l_max, int32_t n_v, int32_t n_t,
   pj->ks = (n_p + 3) / 4;
   pj->sp = conflict_free_stride_dev(n_p);
   pj->nchunk = (n_t + TC - 1) / TC;
+  cudaDeviceGetAttribute(&pj->sms, cudaDevAttrMultiProcessorCount, device);
   const int npl = (l_max + 1) * (l_max + 2) / 2;
   const int gs = conflict_free_stride_dev(pj->ntile * 8);
   int optin = 0;
@@ -1030,14 +1053,15 @@ int bfq_project_samples(const bfq_projector* pj, const double* samples, double* 
     q.wreg = pj->wreg;
     q.ptab = pj->ptab2;
     q.rtab = pj->rtab;
+    const unsigned grid = (unsigned)std::min<int64_t>(n, std::max(pj->sms, 1));
     if (pj->fold) {
       q.ks = pj->ks3;
       q.kfull = pj->kfull3;
       q.nbuf = pj->nbuf3;
       q.wreg = pj->wfold;
-      ps2_fold_kernel(pj->kb3, pj->fold_whole)<<<(unsigned)n, ps2_threads(4), pj->smem3, (cudaStream_t)stream>>>(q);
+      ps2_fold_kernel(pj->kb3, pj->fold_whole)<<<grid, ps2_threads(4), pj->smem3, (cudaStream_t)stream>>>(q);
     } else {
-      ps2_kernel(pj->ntile, pj->kb2)<<<(unsigned)n, ps2_threads(pj->ntile), pj->smem2, (cudaStream_t)stream>>>(q);
+      ps2_kernel(pj->ntile, pj->kb2)<<<grid, ps2_threads(pj->ntile), pj->smem2, (cudaStream_t)stream>>>(q);
     }
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(BFQ_ECUDA, std::string("projection launch: ") + cudaGetErrorString(e));

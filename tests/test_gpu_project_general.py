@@ -201,3 +201,24 @@ def test_asymmetric_azimuth_table_keeps_the_unfolded_kernel():
         kinds.append(int(lib.bfq_projector_kernel(h)))
         lib.bfq_projector_destroy(h)
     assert kinds == [3, 2]
+
+
+@pytest.mark.parametrize("l_max,order", [(8, 32), (8, 48), (4, 16)])
+def test_persistent_ctas_are_position_independent(l_max, order):
+    """The v2 kernels run one CTA per SM over cells blockIdx.x, + gridDim.x, ... with the
+    sample ring and the barrier phases carried across cell boundaries: a batch of more
+    than two cells per SM (ragged) must give every cell bitwise the result it gets in a
+    batch of its own (one cell per CTA)."""
+    cfg = SpectralConfig(3, l_max, 1.0)
+    pts = gproject.project_points(cfg, order)
+    names = sorted(FUNCS)
+    rng = np.random.default_rng(11)
+    base = np.stack([FUNCS[n](pts) for n in names] + [rng.standard_normal(pts.shape[0])])
+    pj = gproject.Projector(cfg, order)
+    alone = pj.project(torch.from_numpy(base).cuda())
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    n = 2 * sms + 5
+    idx = rng.integers(0, base.shape[0], size=n)
+    big = torch.from_numpy(base).cuda()[torch.from_numpy(idx).cuda()].contiguous()
+    got = pj.project(big)
+    assert torch.equal(got, alone[torch.from_numpy(idx).cuda()])
