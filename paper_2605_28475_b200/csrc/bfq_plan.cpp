@@ -1023,7 +1023,9 @@ int build_host_plan(const bfq_desc& d, int smem_limit, HostPlan& hp) {
     for (const Group& gr : pg.groups) {
       for (int e = 0; e < gr.n_chan; ++e) {
         const ChanEntry& ce = pg.chans[gr.chan_off + e];
-        const double tiles = ce.diag ? mte * (mte + 1) / 2 : mte * mte;
+        // n_k = 11, four cells per tile: the (1, 1) tiles of a warp's two cells share one DMMA (MIX)
+        const bool mix = c.pairsplit && nk == 11 && hp.qs == 124 && c.cells == 4 && !std::getenv("BFQ_GENERIC");
+        const double tiles = (ce.diag ? mte * (mte + 1) / 2 : mte * mte) - (mix ? 0.5 : 0.0);
         for (int m1 = 0; m1 < gr.d1; ++m1) {
           const int rows = hp.sstart[ce.slice_base + m1 + 1] - hp.sstart[ce.slice_base + m1];
           total += tiles * 256.0 * ((rows + 3) / 4);  // per cell

@@ -35,6 +35,14 @@ __global__ void __launch_bounds__(MT == 3 ? (CELLS == 1 ? 384 : 256) : 512, 1) b
   // per axis go through DMMA
   constexpr bool X1 = FIXED && (NKT % 8 == 1) && MT >= 2;
   constexpr int MTM = X1 ? MT - 1 : MT;
+  // n_k = 9..12 with two cells per warp (MIX): tile (1, 1) of Phi holds at most
+  // 4 x 4 useful entries per cell, so the two cells share ONE DMMA -- A rows 0..3
+  // from cell 0 (radial rows 8..11), rows 4..7 from cell 1, B columns likewise;
+  // the diagonal 4 x 4 blocks of the product are the two cells' tiles, the
+  // off-diagonal blocks (cell 0 x cell 1) are dropped.  7 DMMAs per k-step and
+  // cell pair instead of 8, for two more gathers.  Same products, same
+  // accumulation order, same K numbering: bitwise the unmixed result.
+  constexpr bool MIX = FIXED && !X1 && MT == 2 && HC == 2 && NKT > 8 && NKT <= 12;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r0 = lane >> 2, kq = lane & 3;
@@ -196,6 +204,9 @@ __global__ void __launch_bounds__(MT == 3 ? (CELLS == 1 ? 384 : 256) : 512, 1) b
       rrow[t] = (uint32_t)(r * K2S + kq) * 8u;
       rrowd[t] = (uint32_t)(r * K2SD + kq) * 8u;
     }
+    if constexpr (MIX) {  // mixed tile: lane row r0 -> cell r0 / 4, radial row 8 + r0 % 4 (clamped)
+      fx_a = f0 + (r0 >= 4 ? cell_bytes : 0u) + (uint32_t)(min(8 + (r0 & 3), NK - 1) * QS) * 8u;
+    } else
     fx_a = f0 + (uint32_t)((NK - 1) * QS) * 8u;
     fx_b = fx_a + f3off;
     fa_lo = f0;
@@ -229,6 +240,14 @@ __global__ void __launch_bounds__(MT == 3 ? (CELLS == 1 ? 384 : 256) : 512, 1) b
 #pragma unroll
     for (int e = 0; e < 2; ++e)
       dpre[a][e] = phid_base(NK, a, a, e) + diag_rows_before(NK, a, e, r0) - kq_min_diag(r0, e) + kq;
+  // MIX: cell 1's tile (1, 1) sits in rows 4..7 x columns 4..7 of the shared accumulator:
+  // lane (r0, kq) plays lane (r0 - 4, kq - 2) of an unmixed tile
+  const int r0m = r0 & 3, kqm = kq & 1;
+  const bool mix_hi = r0 >= 4 && kq >= 2, mix_lo = r0 < 4 && kq < 2;
+  int dprem[2];
+#pragma unroll
+  for (int e = 0; e < 2; ++e)
+    dprem[e] = MIX ? phid_base(NK, 1, 1, e) + diag_rows_before(NK, 1, e, r0m) - kq_min_diag(r0m, e) + kqm : 0;
   auto store_phi = [&](int ml, double (&acc)[HC][MT][MT][2], bool dg) {
 #pragma unroll
     for (int cc = 0; cc < HC; ++cc) {
@@ -239,6 +258,16 @@ __global__ void __launch_bounds__(MT == 3 ? (CELLS == 1 ? 384 : 256) : 512, 1) b
         for (int b = 0; b < MTM; ++b)
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
+            if constexpr (MIX) {
+              if (a == 1 && b == 1) {  // shared accumulator acc[0][1][1]
+                const int ia = 8 + r0m, ib = 8 + 2 * kqm + e;
+                if ((cc == 0 ? mix_lo : mix_hi) && ia < NK && ib < NK && (!dg || ia <= ib)) {
+                  const int k = dg ? dprem[e] : phi_base(NK, 1, 1, e) + r0m * kq_count(NK, 1, e) + kqm;
+                  sts_v(BFQ_CHK(ph + (uint32_t)k * 8u, ph, ph + (uint32_t)K2S * 8u, CHK_PHI_ST), acc[0][1][1][e]);
+                }
+                continue;
+              }
+            }
             const int ia = 8 * a + r0, ib = 8 * b + 2 * kq + e;
             if (!dg) {
               if (ia < NK && ib < NK) {
@@ -327,7 +356,8 @@ __global__ void __launch_bounds__(MT == 3 ? (CELLS == 1 ? 384 : 256) : 512, 1) b
             for (int a = 0; a < MTM; ++a)
 #pragma unroll
               for (int b = 0; b < MTM; ++b)
-                if (b >= a || !DGC) dmma884(ac[cc][a][b][0], ac[cc][a][b][1], av[a], bv[b]);
+                if ((b >= a || !DGC) && !(MIX && a == 1 && b == 1))
+                  dmma884(ac[cc][a][b][0], ac[cc][a][b][1], av[a], bv[b]);
             if constexpr (X1) {
               // g f2[n_k-1, q2], f3[n_k-1, q3] of this lane's row kq, cell cc (broadcast
               // loads; one gather + shuffles measured 3.5% slower, profiles/r02_ab_xsh_dual.txt)
@@ -340,6 +370,11 @@ __global__ void __launch_bounds__(MT == 3 ? (CELLS == 1 ? 384 : 256) : 512, 1) b
               }
               xd_[cc] = fma(ea, eb, xd_[cc]);
             }
+          }
+          if constexpr (MIX) {  // tile (1, 1) of both cells in one DMMA
+            const double am = rw.g * lds_ro(BFQ_CHK(fx_a + qa, fa_lo, fa_lo + fspan, CHK_F2));
+            const double bm = lds_ro(BFQ_CHK(fx_b + qb, fb_lo, fb_lo + fspan, CHK_F3));
+            dmma884(ac[0][1][1][0], ac[0][1][1][1], am, bm);
           }
         };
         const int zn = ml + 1 < MS ? zs[ml + 1 < MS ? ml + 1 : ml] : zs_n[0];
