@@ -37,7 +37,7 @@ def _run(env_extra, ops, cells):
     ({"BFQ_GENERIC": "1"}, "hs_n4,hs_n8,mm_n10", 9),  # run-time-size instantiations
     ({"BFQ_STAGES": "2"}, "hs_n8,hs_n12", 9),         # two-stage R ring
     ({"BFQ_CELLS": "1"}, "hs_n16", 5),                # one cell per tile, slices split over the warps
-    ({"BFQ_HALF_DIAG": "0"}, "hs_n4,hs_n8,hs_n12", 9),  # packed-triangle self-symmetric channels
+    ({"BFQ_HALF_DIAG": "0"}, "hs_n4,hs_n8,mm_n10,hs_n12", 9),  # packed-triangle self-symmetric channels (n_k = 11: shared tile)
     ({"BFQ_RK4_FUSED": "1"}, "mm_n4,hs_n8", 9),       # RK4 stages fused into the Q epilogue
     ({"BFQ_GENERIC": "1"}, "hs_n16", 3),              # run-time-size kernel with three tiles per axis
 ], ids=["default", "fallback", "generic", "stages2", "splitm", "packed_diag", "rk4_fused", "generic_mt3"])
