@@ -39,6 +39,7 @@ cp(os.path.join(ev, "dropin_latency.json"), f"{R}_dropin_latency.json")
 cp(os.path.join(pp, "sum.txt"), f"{R}_ncu_project_fold_proj12.txt")
 for src, dst in ((os.path.join(ev, "ncu_sum_hs_n12.txt"), f"{R}_ncu_hs12_final.txt"),
                  (os.path.join(prof, "ncu_sum_hs_n16.txt"), f"{R}_ncu_hs_n16.txt"),
+                 (os.path.join(prof, "ncu_sum_mm_n10.txt"), f"{R}_ncu_mm_n10.txt"),
                  (os.path.join(prof, "ncu_sum_hs_n8.txt"), f"{R}_ncu_hs_n8.txt")):
     if os.path.exists(src):
         txt = open(src).read()
